@@ -1,0 +1,250 @@
+/*
+ * gear.h -- C-ABI of the B200-native GEAR replay hot path.
+ *
+ * GEAR (arXiv 2310.05205, /root/reference/PAPER.md) keeps RL trajectories in
+ * column tables sharded across the training servers' memory,
+ * selects a batch with GPU kernels and collects the selected
+ * rows into a training batch with GPU kernels that read HBM, host memory
+ * (zero-copy) and remote shards.  This library is that hot
+ * path for one 8xB200 box: one process (rank) per GPU, the table sharded by
+ * trajectory id, one or more shards per rank.
+ *
+ * Conventions (all functions):
+ *  - Every function returns gear_status; GEAR_OK is 0, errors are negative.
+ *    On error the thread-local gear_last_error() string explains it.
+ *  - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *    All device work of a call is enqueued on that stream; calls return
+ *    before the work completes.  Outputs are valid after the stream reaches
+ *    the call.  Errors that only the device can see (an id out of range, a
+ *    bad priority, nothing selectable) are latched into a per-table word and
+ *    returned by gear_table_sync().
+ *  - Small per-call arrays (ids, priorities, generations, sample outputs) may
+ *    be DEVICE or HOST pointers; the library detects which.  Pinned host
+ *    memory keeps the call asynchronous; pageable host memory makes the copy
+ *    synchronous.  Collect outputs must be device memory (or mapped pinned).
+ *  - The caller owns every argument buffer and must keep it alive until the
+ *    stream has reached the call.  The table owns its columns, keys, CDFs and
+ *    scratch.
+ *  - "Collective" calls must be made by every rank of the table's comm, in
+ *    the same order, with the same scalar arguments (SPMD).
+ *  - One host thread per table per rank.
+ *
+ * Global ids.  With W ranks and R shards per rank there are S = W*R shards
+ * of equal capacity C_s = capacity_global / S; shard s owns global ids
+ * [s*C_s, (s+1)*C_s) and lives on rank s / R.  Translation of a global id g
+ * is shard = g / C_s, local = g mod C_s.
+ */
+#ifndef GEAR_H
+#define GEAR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t gear_status;
+#define GEAR_OK 0
+#define GEAR_ERR_INVALID_ARG (-1)   /* bad argument, size or combination */
+#define GEAR_ERR_OUT_OF_MEMORY (-2) /* device or pinned host allocation failed */
+#define GEAR_ERR_CUDA (-3)          /* a CUDA runtime call failed */
+#define GEAR_ERR_NCCL (-4)          /* an NCCL call failed */
+#define GEAR_ERR_EMPTY (-5)         /* nothing (or too little) selectable */
+#define GEAR_ERR_INDEX_RANGE (-6)   /* a global id >= capacity_global */
+#define GEAR_ERR_BAD_PRIORITY (-7)  /* NaN, +-inf or negative priority */
+#define GEAR_ERR_STATE (-8)         /* wrong call order / latched device error */
+#define GEAR_ERR_UNSUPPORTED (-9)   /* valid request this build does not do */
+
+/* Bits of the device-side error word returned by gear_table_sync(). */
+#define GEAR_DEVERR_INDEX_RANGE 1u  /* an update/collect id was >= capacity_global */
+#define GEAR_DEVERR_BAD_PRIORITY 2u /* an update priority was NaN/inf/negative */
+#define GEAR_DEVERR_STALE 4u        /* an update hit a never-inserted slot or a stale generation */
+#define GEAR_DEVERR_EMPTY 8u        /* a sample found nothing (or < W*B for FIFO/LIFO) selectable */
+
+/* Padding id: update entries with this id are ignored (lets ranks with fewer
+ * updates pass the common n of a collective update). */
+#define GEAR_IDX_NONE UINT64_MAX
+
+typedef void* gear_stream; /* cudaStream_t */
+
+typedef enum {
+  GEAR_U8 = 0,
+  GEAR_I32 = 1,
+  GEAR_I64 = 2,
+  GEAR_F32 = 3,
+  GEAR_F64 = 4,
+  GEAR_BF16 = 5
+} gear_dtype;
+
+/* Where a column's rows live: device HBM of the owning rank, or pinned host
+ * memory read by the GPUs zero-copy over PCIe. */
+typedef enum { GEAR_DEVICE = 0, GEAR_HOST = 1 } gear_placement;
+
+/* Selection strategies.  FIFO/LIFO select the W*B
+ * oldest / newest selectable trajectories (decentralised);
+ * UNIFORM/WEIGHTED/PRIORITIZED draw W*B ids with replacement from the CDF of
+ * [key>0] / key (centralised).  PRIORITIZED also returns
+ * importance-sampling weights (q_min/q)^beta over the rank's slice. */
+typedef enum {
+  GEAR_FIFO = 0,
+  GEAR_LIFO = 1,
+  GEAR_UNIFORM = 2,
+  GEAR_WEIGHTED = 3,
+  GEAR_PRIORITIZED = 4
+} gear_strategy;
+
+/* Victim choice when a shard is full. */
+typedef enum { GEAR_REMOVE_FIFO = 0, GEAR_REMOVE_LIFO = 1 } gear_removal;
+
+/* One column table: a field of every trajectory; its row
+ * ("block") is seq_len * prod(shape) elements of dtype, stored contiguously. */
+typedef struct {
+  const char* name;        /* unique, non-empty, <= 63 chars */
+  gear_dtype dtype;
+  uint32_t ndim;           /* <= 8; 0 means a scalar per step */
+  const int64_t* shape;    /* per-step shape, ndim entries, all > 0 */
+  gear_placement placement;
+} gear_column_desc;
+
+typedef struct {
+  uint64_t capacity_global;    /* N: trajectories in the whole table; divisible by S */
+  uint32_t seq_len;            /* steps per trajectory (>= 1), folded into every row */
+  uint32_t ncols;              /* 1..16 */
+  const gear_column_desc* cols;
+  uint32_t priority_frac_bits; /* F of the fixed-point priority Q_F (0 -> 32; max 62) */
+  gear_removal removal;        /* victim rule of gear_insert when a shard is full */
+  uint32_t shards_per_rank;    /* R (0 -> 1); W*R <= 32.  R > 1 emulates a
+                                  larger world on fewer GPUs (tests). */
+  uint32_t max_batch;          /* upper bound of B and of per-call n (0 -> 4096) */
+} gear_table_desc;
+
+typedef struct {
+  uint64_t capacity_global;  /* N */
+  uint64_t shard_capacity;   /* C_s */
+  uint32_t n_ranks;          /* W */
+  uint32_t rank;
+  uint32_t shards_per_rank;  /* R */
+  uint32_t ncols;
+  uint64_t row_bytes_total;  /* sum of the columns' row bytes */
+  uint64_t q_max;            /* largest fixed-point key = floor((2^62-1)/N) */
+  double p_max;              /* q_max / 2^F: priorities above it saturate */
+  uint32_t frac_bits;
+  uint32_t max_batch;
+} gear_table_info;
+
+typedef struct gear_comm gear_comm;
+typedef struct gear_table gear_table;
+
+/* Thread-local description of the last error on this thread ("" if none). */
+const char* gear_last_error(void);
+
+/* Library version string. */
+const char* gear_version(void);
+
+/* --- communicator (one per rank; wraps an NCCL communicator) ------------ */
+
+/* Rank 0 creates the 128-byte unique id and the caller broadcasts it to the
+ * other ranks by any means (the Python binding uses torch.distributed). */
+gear_status gear_get_unique_id(uint8_t out[128]);
+
+/* Collective over all nranks.  `device` is this rank's CUDA device; it is
+ * made current.  Peer access is enabled to every other rank's device. */
+gear_status gear_comm_create(int nranks, int rank, const uint8_t id[128], int device,
+                             gear_comm** out);
+gear_status gear_comm_destroy(gear_comm* comm);
+
+/* --- table ------------------------------------------------------------- */
+
+/* Collective when comm != NULL (comm == NULL means W = 1).  Allocates this
+ * rank's R shards: DEVICE columns with cudaMalloc, HOST columns as pinned
+ * mapped host memory (W > 1: POSIX shared memory registered with every GPU so
+ * any rank can read any shard's host rows over its own PCIe link), plus keys
+ * (u64 fixed point), seq (u64), gen (u32), two CDF buffers and scratch, and
+ * exchanges peer pointers (CUDA IPC) so kernels can read peer shards over
+ * NVLink.  Errors: INVALID_ARG (N not divisible by S, duplicate or empty
+ * names, zero-size rows, S > 32, ncols > 16), OUT_OF_MEMORY, CUDA, NCCL. */
+gear_status gear_table_create(const gear_table_desc* desc, gear_comm* comm, gear_table** out);
+
+/* Collective when the table has a comm.  Frees everything. */
+gear_status gear_table_destroy(gear_table* t);
+
+gear_status gear_table_info_get(const gear_table* t, gear_table_info* info);
+
+/* Column index of `name`, or INVALID_ARG. */
+gear_status gear_column_id(const gear_table* t, const char* name, uint32_t* out);
+
+/* Row bytes of column `col`. */
+gear_status gear_column_row_bytes(const gear_table* t, uint32_t col, uint64_t* out);
+
+/* --- hot path ---------------------------------------------------------- */
+
+/* Insert n trajectories into global shard `shard`, which must be owned by
+ * this rank (online data goes to the local shard).  Not
+ * collective.  Allocation follows PAPER.md:186-195: a per-shard free queue
+ * seeded 0..C_s-1 ascending; when it is empty the victim is the oldest (FIFO
+ * removal) or newest (LIFO removal) committed slot.  Each inserted slot gets
+ * seq = the shard's next counter value (starting at 1), gen += 1, and
+ * key = Q_F(prio[k]).
+ *   col_src[c]: n rows of column c, [n][row_bytes_c], host or device.
+ *   prio:       HOST array of n f64 priorities (0 = stored, not selectable).
+ *   out_idx:    n u64 global ids (host or device), may be NULL.
+ * If two of the n rows land in one slot (LIFO removal, or n > C_s) the later
+ * row wins.  Errors: INVALID_ARG, BAD_PRIORITY (nothing inserted).  Must not
+ * overlap a sample/collect of the same step on any rank (caller barrier). */
+gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* const* col_src,
+                        const double* prio, uint64_t* out_idx, gear_stream stream);
+
+/* Set the priorities of n trajectories.  Collective: every rank passes the
+ * same n; pad with GEAR_IDX_NONE.  idx: u64 global ids; prio: n values of
+ * prio_dtype (GEAR_F32 or GEAR_F64); gen: optional u32 generations (entries
+ * whose generation differs from the slot's are skipped as stale).  The
+ * priority becomes key = Q_F(p): p == 0 -> 0 (not selectable), else
+ * clamp(round_half_even(p * 2^F), 1, q_max).  Entries of all ranks are
+ * applied in (rank, position) order -- the last writer wins.  Device-side
+ * errors (id >= N, bad p, stale) skip the entry and are latched. */
+gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* idx,
+                                   const void* prio, gear_dtype prio_dtype, const uint32_t* gen,
+                                   gear_stream stream);
+
+/* Select this rank's B trajectories.  Collective.  One global batch of W*B
+ * is selected; rank r receives positions [r*B, (r+1)*B).
+ *  UNIFORM/WEIGHTED/PRIORITIZED: draw j uses
+ *    Philox4x32-10(counter=(j_lo, j_hi, 0, 0), key=(seed_lo, seed_hi)),
+ *    r = x0 | x1<<32, u = floor(r*T/2^64) with T the total weight, and
+ *    returns min{g : CDF[g] > u}.  Deterministic in (table, seed), independent
+ *    of W, R and launch shape.
+ *  FIFO/LIFO: the W*B selectable trajectories with the
+ *    smallest / largest (seq, shard), in that order.
+ *  out_idx: u64[B] global ids (required).  out_w: f32[B] importance weights
+ *  (PRIORITIZED: (q_min/q)^beta in f64 rounded to f32; otherwise 1).
+ *  out_p: f64[B] selection probability q/T (FIFO/LIFO: 1).  out_gen: u32[B]
+ *  generation of each selected slot.  Optional outputs may be NULL.
+ *  Nothing selectable: outputs get GEAR_IDX_NONE and EMPTY is latched. */
+gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint64_t seed,
+                        double beta, uint64_t* out_idx, float* out_w, double* out_p,
+                        uint32_t* out_gen, gear_stream stream);
+
+/* Gather rows of ncols columns for n global ids into contiguous batches,
+ * rows in request order.  out[c] is a device buffer of
+ * n * row_bytes(col_ids[c]) bytes.  DEVICE columns are read from local HBM
+ * or a peer's HBM over NVLink; HOST columns are read zero-copy over PCIe.
+ * Not collective (peers' memory is read directly).  idx: device or host.
+ * An id >= N leaves its output row untouched and latches INDEX_RANGE. */
+gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_t ncols,
+                         const uint32_t* col_ids, void* const* out, gear_stream stream);
+
+/* Synchronise the device, return and clear the latched device error bits
+ * (GEAR_DEVERR_*) and the count of stale update entries.  Either output may
+ * be NULL.  Returns STATE if any bit was set, else OK. */
+gear_status gear_table_sync(gear_table* t, uint32_t* dev_errors, uint64_t* n_stale);
+
+/* Read back this rank's slot state (device -> host, synchronous), for tests
+ * and checkpoints: keys u64[R*C_s], seq u64[R*C_s], gen u32[R*C_s]; any
+ * pointer may be NULL. */
+gear_status gear_read_state(gear_table* t, uint64_t* key, uint64_t* seq, uint32_t* gen);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GEAR_H */

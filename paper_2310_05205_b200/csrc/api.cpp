@@ -1,0 +1,810 @@
+// api.cpp -- the C-ABI of include/gear.h: argument validation, table memory,
+// peer mappings and the orchestration of the sm_100a kernels.
+//
+// Every step of the hot path runs on the GPU: this file only validates,
+// allocates, stages small host arrays and enqueues kernels / NCCL calls on the
+// caller's stream.  The only host-side algorithm is the per-shard ring
+// allocator of gear_insert, which the paper also keeps in
+// the host-resident index manager.
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <unordered_map>
+
+#include "runtime.h"
+
+using namespace gear;
+
+namespace {
+
+uint64_t dtype_size(gear_dtype d) {
+  switch (d) {
+    case GEAR_U8: return 1;
+    case GEAR_I32: return 4;
+    case GEAR_I64: return 8;
+    case GEAR_F32: return 4;
+    case GEAR_F64: return 8;
+    case GEAR_BF16: return 2;
+  }
+  return 0;
+}
+
+template <class T>
+gear_status dalloc(T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(GEAR_ERR_OUT_OF_MEMORY, "cudaMalloc(%zu bytes): %s", n * sizeof(T),
+                     cudaGetErrorString(e));
+  }
+  return GEAR_OK;
+}
+
+template <class T>
+void dfree(T*& p) {
+  if (p) cudaFree(const_cast<void*>(reinterpret_cast<const void*>(p)));
+  p = nullptr;
+}
+
+// Maps `bytes` of host memory and registers it with CUDA as mapped pinned
+// memory.  shm_name empty: private anonymous memory (W = 1); otherwise a POSIX
+// shared-memory object (created if `create`), so every rank's GPU can map the
+// same pages.
+gear_status map_host(const std::string& shm_name, bool create, size_t bytes, void** out) {
+  *out = nullptr;
+  void* p = MAP_FAILED;
+  if (shm_name.empty()) {
+    p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  } else {
+    int fd = shm_open(shm_name.c_str(), create ? (O_CREAT | O_EXCL | O_RDWR) : O_RDWR, 0600);
+    if (fd < 0) return set_error(GEAR_ERR_OUT_OF_MEMORY, "shm_open(%s) failed", shm_name.c_str());
+    if (create && ftruncate(fd, (off_t)bytes) != 0) {
+      close(fd);
+      shm_unlink(shm_name.c_str());
+      return set_error(GEAR_ERR_OUT_OF_MEMORY, "ftruncate(%s, %zu) failed", shm_name.c_str(),
+                       bytes);
+    }
+    p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+  }
+  if (p == MAP_FAILED) return set_error(GEAR_ERR_OUT_OF_MEMORY, "mmap(%zu) failed", bytes);
+  madvise(p, bytes, MADV_HUGEPAGE);
+  cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    munmap(p, bytes);
+    return set_error(GEAR_ERR_OUT_OF_MEMORY, "cudaHostRegister(%zu bytes): %s", bytes,
+                     cudaGetErrorString(e));
+  }
+  *out = p;
+  return GEAR_OK;
+}
+
+void unmap_host(void* p, size_t bytes) {
+  cudaHostUnregister(p);
+  munmap(p, bytes);
+}
+
+// Exchange a CUDA-IPC handle for `local` and open every peer's allocation.
+gear_status exchange_ipc(gear_table* t, void* local, void** views, std::vector<void*>& opened) {
+  gear_comm* c = t->comm;
+  cudaIpcMemHandle_t h;
+  GEAR_CUDA(cudaIpcGetMemHandle(&h, local));
+  uint8_t* d_send = nullptr;
+  uint8_t* d_recv = nullptr;
+  GEAR_TRY(dalloc(&d_send, sizeof(h)));
+  GEAR_TRY(dalloc(&d_recv, sizeof(h) * t->W));
+  GEAR_CUDA(cudaMemcpy(d_send, &h, sizeof(h), cudaMemcpyHostToDevice));
+  GEAR_TRY(allgather_bytes(c, d_send, d_recv, sizeof(h), c->stream));
+  GEAR_CUDA(cudaStreamSynchronize(c->stream));
+  std::vector<cudaIpcMemHandle_t> all(t->W);
+  GEAR_CUDA(cudaMemcpy(all.data(), d_recv, sizeof(h) * t->W, cudaMemcpyDeviceToHost));
+  dfree(d_send);
+  dfree(d_recv);
+  for (uint32_t r = 0; r < t->W; ++r) {
+    if (r == t->rank) {
+      views[r] = local;
+      continue;
+    }
+    void* p = nullptr;
+    GEAR_CUDA(cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess));
+    views[r] = p;
+    opened.push_back(p);
+  }
+  return GEAR_OK;
+}
+
+void destroy_table(gear_table* t) {
+  if (!t) return;
+  cudaSetDevice(t->device);
+  cudaDeviceSynchronize();
+  for (auto& c : t->cols) {
+    for (void* p : c.ipc_opened) cudaIpcCloseMemHandle(p);
+    for (auto& m : c.host_maps) unmap_host(m.first, m.second);
+    if (c.placement == GEAR_DEVICE && c.local) cudaFree(c.local);
+  }
+  for (void* p : t->ipc_opened) cudaIpcCloseMemHandle(p);
+  dfree(t->key); dfree(t->seq); dfree(t->gen); dfree(t->tag); dfree(t->ord);
+  for (int i = 0; i < 2; ++i) {
+    dfree(t->cdf[i]); dfree(t->scan_status[i]); dfree(t->scan_ticket[i]);
+  }
+  dfree(t->cdf_totals_local); dfree(t->cdf_totals_all);
+  dfree(t->fifo_totals_local); dfree(t->fifo_totals_all);
+  dfree(t->d_cdf_ptrs); dfree(t->d_gen_ptrs);
+  dfree(t->q_scratch); dfree(t->qmin_slot); dfree(t->done_ctr);
+  dfree(t->tmp_idx); dfree(t->tmp_w); dfree(t->tmp_p); dfree(t->tmp_gen);
+  dfree(t->cand_local); dfree(t->cand_all);
+  dfree(t->upd_local); dfree(t->upd_all); dfree(t->upd_idx); dfree(t->upd_prio); dfree(t->upd_gen);
+  dfree(t->n_stale); dfree(t->err);
+  dfree(t->col_idx.p);
+  dfree(t->d_meta); dfree(t->d_ord); dfree(t->d_out); dfree(t->d_rows);
+  if (t->h_meta) cudaFreeHost(t->h_meta);
+  if (t->h_ord) cudaFreeHost(t->h_ord);
+  if (t->h_out) cudaFreeHost(t->h_out);
+  if (t->staging_ev) cudaEventDestroy(t->staging_ev);
+  delete t;
+}
+
+gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* t) {
+  t->comm = comm;
+  GEAR_CUDA(cudaGetDevice(&t->device));
+  if (comm) {
+    t->device = comm->device;
+    GEAR_CUDA(cudaSetDevice(t->device));
+    t->W = (uint32_t)comm->nranks;
+    t->rank = (uint32_t)comm->rank;
+  }
+  t->R = d->shards_per_rank ? d->shards_per_rank : 1;
+  t->S = t->W * t->R;
+  if (t->S > (uint32_t)kMaxShards)
+    return set_error(GEAR_ERR_INVALID_ARG, "W*R = %u shards > %d", t->S, kMaxShards);
+  t->N = d->capacity_global;
+  if (t->N == 0 || t->N % t->S)
+    return set_error(GEAR_ERR_INVALID_ARG, "capacity_global %llu not a positive multiple of %u shards",
+                     (unsigned long long)t->N, t->S);
+  t->Cs = t->N / t->S;
+  if (t->Cs >= (1ull << 32))
+    return set_error(GEAR_ERR_INVALID_ARG, "shard capacity must be < 2^32");
+  t->Clocal = t->Cs * t->R;
+  t->F = d->priority_frac_bits ? d->priority_frac_bits : 32;
+  if (t->F > 62) return set_error(GEAR_ERR_INVALID_ARG, "priority_frac_bits > 62");
+  t->qmax = ((1ull << 62) - 1) / t->N;
+  t->removal = d->removal;
+  if (t->removal != GEAR_REMOVE_FIFO && t->removal != GEAR_REMOVE_LIFO)
+    return set_error(GEAR_ERR_INVALID_ARG, "bad removal");
+  t->max_batch = d->max_batch ? d->max_batch : 4096;
+  if (d->seq_len == 0) return set_error(GEAR_ERR_INVALID_ARG, "seq_len == 0");
+  if (d->ncols == 0 || d->ncols > (uint32_t)kMaxCols || d->cols == nullptr)
+    return set_error(GEAR_ERR_INVALID_ARG, "ncols must be 1..%d", kMaxCols);
+  if (const char* e = getenv("GEAR_COLLECT_CHUNK")) t->chunk_bytes = (uint32_t)atoi(e);
+  if (t->chunk_bytes < 512 || t->chunk_bytes % 512)
+    return set_error(GEAR_ERR_INVALID_ARG, "GEAR_COLLECT_CHUNK must be a multiple of 512");
+
+  // Column layout.
+  t->cols.resize(d->ncols);
+  for (uint32_t c = 0; c < d->ncols; ++c) {
+    const gear_column_desc& cd = d->cols[c];
+    ColumnState& cs = t->cols[c];
+    if (cd.name == nullptr || cd.name[0] == 0 || strlen(cd.name) > 63)
+      return set_error(GEAR_ERR_INVALID_ARG, "column %u: empty or long name", c);
+    for (uint32_t o = 0; o < c; ++o)
+      if (t->cols[o].name == cd.name)
+        return set_error(GEAR_ERR_INVALID_ARG, "duplicate column name %s", cd.name);
+    if (dtype_size(cd.dtype) == 0) return set_error(GEAR_ERR_INVALID_ARG, "column %s: bad dtype", cd.name);
+    if (cd.ndim > 8 || (cd.ndim > 0 && cd.shape == nullptr))
+      return set_error(GEAR_ERR_INVALID_ARG, "column %s: bad shape", cd.name);
+    uint64_t elems = d->seq_len;
+    for (uint32_t k = 0; k < cd.ndim; ++k) {
+      if (cd.shape[k] <= 0) return set_error(GEAR_ERR_INVALID_ARG, "column %s: zero-size shape", cd.name);
+      elems *= (uint64_t)cd.shape[k];
+    }
+    if (cd.placement != GEAR_DEVICE && cd.placement != GEAR_HOST)
+      return set_error(GEAR_ERR_INVALID_ARG, "column %s: bad placement", cd.name);
+    cs.name = cd.name;
+    cs.dtype = cd.dtype;
+    cs.placement = cd.placement;
+    cs.rb = elems * dtype_size(cd.dtype);
+    cs.bytes_local = cs.rb * t->Clocal;
+  }
+
+  // A per-table tag for shared-memory names (rank 0 draws it, all-gathered).
+  uint64_t tag = 0;
+  if (t->W > 1) {
+    std::random_device rd;
+    uint64_t mine = ((uint64_t)rd() << 32) ^ rd() ^ (uint64_t)getpid();
+    uint64_t *d_s = nullptr, *d_r = nullptr;
+    GEAR_TRY(dalloc(&d_s, 1));
+    GEAR_TRY(dalloc(&d_r, t->W));
+    GEAR_CUDA(cudaMemcpy(d_s, &mine, 8, cudaMemcpyHostToDevice));
+    GEAR_TRY(allgather_bytes(comm, d_s, d_r, 8, comm->stream));
+    GEAR_CUDA(cudaStreamSynchronize(comm->stream));
+    GEAR_CUDA(cudaMemcpy(&tag, d_r, 8, cudaMemcpyDeviceToHost));  // rank 0's value
+    dfree(d_s);
+    dfree(d_r);
+  }
+
+  // Column memory.
+  for (uint32_t c = 0; c < d->ncols; ++c) {
+    ColumnState& cs = t->cols[c];
+    if (cs.placement == GEAR_DEVICE) {
+      GEAR_TRY(dalloc(&cs.local, cs.bytes_local));
+      if (t->W > 1) {
+        void* views[kMaxRanks] = {};
+        GEAR_TRY(exchange_ipc(t, cs.local, views, cs.ipc_opened));
+        for (uint32_t r = 0; r < t->W; ++r) cs.view[r] = (const uint8_t*)views[r];
+      } else {
+        cs.view[0] = cs.local;
+      }
+    } else {
+      if (t->W == 1) {
+        void* p = nullptr;
+        GEAR_TRY(map_host("", true, cs.bytes_local, &p));
+        cs.host_maps.emplace_back(p, cs.bytes_local);
+        cs.local = (uint8_t*)p;
+        void* dp = nullptr;
+        GEAR_CUDA(cudaHostGetDevicePointer(&dp, p, 0));
+        cs.view[0] = (const uint8_t*)dp;
+      } else {
+        char nm[96];
+        snprintf(nm, sizeof(nm), "/gear_%016llx_c%u_r%u", (unsigned long long)tag, c, t->rank);
+        cs.shm_name = nm;
+        void* p = nullptr;
+        GEAR_TRY(map_host(cs.shm_name, true, cs.bytes_local, &p));
+        cs.host_maps.emplace_back(p, cs.bytes_local);
+        cs.local = (uint8_t*)p;
+        GEAR_TRY(barrier(comm));
+        for (uint32_t r = 0; r < t->W; ++r) {
+          void* q = p;
+          if (r != t->rank) {
+            snprintf(nm, sizeof(nm), "/gear_%016llx_c%u_r%u", (unsigned long long)tag, c, r);
+            GEAR_TRY(map_host(nm, false, cs.bytes_local, &q));
+            cs.host_maps.emplace_back(q, cs.bytes_local);
+          }
+          void* dp = nullptr;
+          GEAR_CUDA(cudaHostGetDevicePointer(&dp, q, 0));
+          cs.view[r] = (const uint8_t*)dp;
+        }
+        GEAR_TRY(barrier(comm));
+        shm_unlink(cs.shm_name.c_str());
+      }
+    }
+  }
+
+  // Slot state.
+  GEAR_TRY(dalloc(&t->key, t->Clocal));
+  GEAR_TRY(dalloc(&t->seq, t->Clocal));
+  GEAR_TRY(dalloc(&t->gen, t->Clocal));
+  GEAR_TRY(dalloc(&t->tag, t->Clocal));
+  GEAR_TRY(dalloc(&t->ord, t->Clocal));
+  GEAR_CUDA(cudaMemset(t->key, 0, t->Clocal * 8));
+  GEAR_CUDA(cudaMemset(t->seq, 0, t->Clocal * 8));
+  GEAR_CUDA(cudaMemset(t->gen, 0, t->Clocal * 4));
+  GEAR_CUDA(cudaMemset(t->tag, 0, t->Clocal * 8));
+  GEAR_CUDA(cudaMemset(t->ord, 0, t->Clocal * 4));
+  const uint32_t tiles = scan_tiles_per_shard(t->Cs) * t->R;
+  for (int i = 0; i < 2; ++i) {
+    GEAR_TRY(dalloc(&t->cdf[i], t->Clocal));
+    GEAR_CUDA(cudaMemset(t->cdf[i], 0, t->Clocal * 8));
+    GEAR_TRY(dalloc(&t->scan_status[i], tiles));
+    GEAR_CUDA(cudaMemset(t->scan_status[i], 0, tiles * 8));
+    GEAR_TRY(dalloc(&t->scan_ticket[i], 1));
+    GEAR_CUDA(cudaMemset(t->scan_ticket[i], 0, 4));
+  }
+  GEAR_TRY(dalloc(&t->cdf_totals_local, t->R));
+  GEAR_TRY(dalloc(&t->cdf_totals_all, t->S));
+  GEAR_TRY(dalloc(&t->fifo_totals_local, t->R));
+  GEAR_TRY(dalloc(&t->fifo_totals_all, t->S));
+  GEAR_CUDA(cudaMemset(t->cdf_totals_local, 0, t->R * sizeof(ShardTotals)));
+  GEAR_CUDA(cudaMemset(t->cdf_totals_all, 0, t->S * sizeof(ShardTotals)));
+
+  // Pointer tables: every shard's two CDF buffers and every rank's gen array.
+  std::vector<const uint64_t*> cdf_ptrs(2 * t->S);
+  std::vector<const uint32_t*> gen_ptrs(t->W);
+  if (t->W > 1) {
+    void* v0[kMaxRanks] = {};
+    void* v1[kMaxRanks] = {};
+    void* vg[kMaxRanks] = {};
+    GEAR_TRY(exchange_ipc(t, t->cdf[0], v0, t->ipc_opened));
+    GEAR_TRY(exchange_ipc(t, t->cdf[1], v1, t->ipc_opened));
+    GEAR_TRY(exchange_ipc(t, t->gen, vg, t->ipc_opened));
+    for (uint32_t r = 0; r < t->W; ++r) {
+      gen_ptrs[r] = (const uint32_t*)vg[r];
+      for (uint32_t ls = 0; ls < t->R; ++ls) {
+        cdf_ptrs[0 * t->S + r * t->R + ls] = (const uint64_t*)v0[r] + ls * t->Cs;
+        cdf_ptrs[1 * t->S + r * t->R + ls] = (const uint64_t*)v1[r] + ls * t->Cs;
+      }
+    }
+  } else {
+    gen_ptrs[0] = t->gen;
+    for (uint32_t ls = 0; ls < t->R; ++ls) {
+      cdf_ptrs[ls] = t->cdf[0] + ls * t->Cs;
+      cdf_ptrs[t->S + ls] = t->cdf[1] + ls * t->Cs;
+    }
+  }
+  GEAR_TRY(dalloc(&t->d_cdf_ptrs, 2 * t->S));
+  GEAR_TRY(dalloc(&t->d_gen_ptrs, t->W));
+  GEAR_CUDA(cudaMemcpy(t->d_cdf_ptrs, cdf_ptrs.data(), 2 * t->S * sizeof(void*), cudaMemcpyHostToDevice));
+  GEAR_CUDA(cudaMemcpy(t->d_gen_ptrs, gen_ptrs.data(), t->W * sizeof(void*), cudaMemcpyHostToDevice));
+
+  // Scratch.
+  const uint64_t MB = t->max_batch, K = (uint64_t)t->W * MB;
+  GEAR_TRY(dalloc(&t->q_scratch, MB));
+  GEAR_TRY(dalloc(&t->qmin_slot, 1));
+  GEAR_CUDA(cudaMemset(t->qmin_slot, 0xff, 8));
+  GEAR_TRY(dalloc(&t->done_ctr, 1));
+  GEAR_CUDA(cudaMemset(t->done_ctr, 0, 4));
+  GEAR_TRY(dalloc(&t->tmp_idx, MB));
+  GEAR_TRY(dalloc(&t->tmp_w, MB));
+  GEAR_TRY(dalloc(&t->tmp_p, MB));
+  GEAR_TRY(dalloc(&t->tmp_gen, MB));
+  GEAR_TRY(dalloc(&t->cand_local, t->R * K));
+  GEAR_TRY(dalloc(&t->cand_all, t->S * K));
+  GEAR_TRY(dalloc(&t->upd_local, MB));
+  GEAR_TRY(dalloc(&t->upd_all, K));
+  GEAR_TRY(dalloc(&t->upd_idx, MB));
+  GEAR_TRY(dalloc(&t->upd_prio, MB));
+  GEAR_TRY(dalloc(&t->upd_gen, MB));
+  GEAR_TRY(dalloc(&t->n_stale, 1));
+  GEAR_TRY(dalloc(&t->err, 1));
+  GEAR_CUDA(cudaMemset(t->n_stale, 0, 8));
+  GEAR_CUDA(cudaMemset(t->err, 0, 4));
+  GEAR_CUDA(cudaHostAlloc((void**)&t->h_meta, MB * sizeof(InsMeta), cudaHostAllocDefault));
+  GEAR_CUDA(cudaHostAlloc((void**)&t->h_ord, MB * sizeof(OrdRec), cudaHostAllocDefault));
+  GEAR_CUDA(cudaHostAlloc((void**)&t->h_out, MB * sizeof(uint64_t), cudaHostAllocDefault));
+  GEAR_TRY(dalloc(&t->d_meta, MB));
+  GEAR_TRY(dalloc(&t->d_ord, MB));
+  GEAR_TRY(dalloc(&t->d_out, MB));
+  GEAR_CUDA(cudaEventCreateWithFlags(&t->staging_ev, cudaEventDisableTiming));
+  GEAR_CUDA(cudaEventRecord(t->staging_ev, 0));
+
+  t->rings.resize(t->R);
+  for (auto& r : t->rings) r.ord.assign(t->Cs, 0);
+  GEAR_CUDA(cudaDeviceSynchronize());
+  return GEAR_OK;
+}
+
+// Make `n` elements at `user` available on the device: device pointers pass
+// through, host pointers are copied into `scratch` on the stream.
+template <class T>
+gear_status stage_in(const T* user, size_t n, T* scratch, cudaStream_t s, const T** out) {
+  if (n == 0 || mem_kind(user) == MemKind::Device) {
+    *out = user;
+    return GEAR_OK;
+  }
+  GEAR_CUDA(cudaMemcpyAsync(scratch, user, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  *out = scratch;
+  return GEAR_OK;
+}
+
+uint32_t vec_width(uint64_t rb, uint32_t chunk, std::initializer_list<uintptr_t> ptrs) {
+  for (uint32_t v : {16u, 8u, 4u, 2u}) {
+    bool ok = rb % v == 0 && chunk % v == 0;
+    for (uintptr_t p : ptrs) ok = ok && (p % v == 0);
+    if (ok) return v;
+  }
+  return 1;
+}
+
+gear_status check_table(const gear_table* t) {
+  if (t == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "table is NULL");
+  return GEAR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+gear_status gear_table_create(const gear_table_desc* desc, gear_comm* comm, gear_table** out) {
+  clear_error();
+  if (desc == nullptr || out == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "NULL argument");
+  *out = nullptr;
+  auto* t = new gear_table();
+  gear_status st = create_table(desc, comm, t);
+  if (st != GEAR_OK) {
+    std::string msg = gear_last_error();
+    destroy_table(t);
+    set_error(st, "%s", msg.c_str());
+    return st;
+  }
+  *out = t;
+  return GEAR_OK;
+}
+
+gear_status gear_table_destroy(gear_table* t) {
+  if (t == nullptr) return GEAR_OK;
+  gear_comm* c = t->comm;
+  destroy_table(t);
+  if (c) GEAR_TRY(barrier(c));
+  return GEAR_OK;
+}
+
+gear_status gear_table_info_get(const gear_table* t, gear_table_info* info) {
+  GEAR_TRY(check_table(t));
+  if (info == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "info is NULL");
+  info->capacity_global = t->N;
+  info->shard_capacity = t->Cs;
+  info->n_ranks = t->W;
+  info->rank = t->rank;
+  info->shards_per_rank = t->R;
+  info->ncols = (uint32_t)t->cols.size();
+  info->row_bytes_total = 0;
+  for (auto& c : t->cols) info->row_bytes_total += c.rb;
+  info->q_max = t->qmax;
+  info->p_max = std::ldexp((double)t->qmax, -(int)t->F);
+  info->frac_bits = t->F;
+  info->max_batch = t->max_batch;
+  return GEAR_OK;
+}
+
+gear_status gear_column_id(const gear_table* t, const char* name, uint32_t* out) {
+  GEAR_TRY(check_table(t));
+  if (name == nullptr || out == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "NULL argument");
+  for (uint32_t c = 0; c < t->cols.size(); ++c)
+    if (t->cols[c].name == name) {
+      *out = c;
+      return GEAR_OK;
+    }
+  return set_error(GEAR_ERR_INVALID_ARG, "no column named %s", name);
+}
+
+gear_status gear_column_row_bytes(const gear_table* t, uint32_t col, uint64_t* out) {
+  GEAR_TRY(check_table(t));
+  if (out == nullptr || col >= t->cols.size())
+    return set_error(GEAR_ERR_INVALID_ARG, "bad column %u", col);
+  *out = t->cols[col].rb;
+  return GEAR_OK;
+}
+
+gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* const* col_src,
+                        const double* prio, uint64_t* out_idx, gear_stream stream) {
+  clear_error();
+  GEAR_TRY(check_table(t));
+  GEAR_CUDA(cudaSetDevice(t->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (shard / t->R != t->rank || shard >= t->S)
+    return set_error(GEAR_ERR_INVALID_ARG, "shard %u is not owned by rank %u", shard, t->rank);
+  if (n == 0) return GEAR_OK;
+  if (col_src == nullptr || prio == nullptr)
+    return set_error(GEAR_ERR_INVALID_ARG, "col_src / prio is NULL");
+  for (size_t c = 0; c < t->cols.size(); ++c)
+    if (col_src[c] == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "col_src[%zu] is NULL", c);
+  // Priorities are validated on the host before anything is inserted.
+  std::vector<double> p(n);
+  if (mem_kind(prio) == MemKind::Device)
+    GEAR_CUDA(cudaMemcpy(p.data(), prio, n * sizeof(double), cudaMemcpyDeviceToHost));
+  else
+    std::memcpy(p.data(), prio, n * sizeof(double));
+  for (uint32_t k = 0; k < n; ++k)
+    if (!(p[k] >= 0.0) || std::isinf(p[k]))
+      return set_error(GEAR_ERR_BAD_PRIORITY, "prio[%u] = %g is not a finite non-negative number", k, p[k]);
+
+  const uint32_t ls = shard % t->R;
+  ShardRing& ring = t->rings[ls];
+  uint64_t row_total = 0;
+  for (auto& c : t->cols) row_total += c.rb;
+  // Rows per chunk: bounded by the staging arrays and by 256 MB of row data.
+  const uint64_t by_bytes = std::max<uint64_t>(1, (256ull << 20) / row_total);
+  const uint32_t chunk_rows = (uint32_t)std::min<uint64_t>(t->max_batch, by_bytes);
+  std::vector<MemKind> kinds(t->cols.size());
+  for (size_t c = 0; c < t->cols.size(); ++c) kinds[c] = mem_kind(col_src[c]);
+
+  std::unordered_map<uint32_t, uint32_t> slot_at;   // slot -> meta index
+  std::unordered_map<uint32_t, uint32_t> pos_at;    // ring position -> ord index
+  for (uint32_t k0 = 0; k0 < n; k0 += chunk_rows) {
+    const uint32_t m = std::min(chunk_rows, n - k0);
+    GEAR_CUDA(cudaEventSynchronize(t->staging_ev));  // staging buffers free again
+    slot_at.clear();
+    pos_at.clear();
+    uint32_t n_meta = 0, n_ord = 0;
+    for (uint32_t k = 0; k < m; ++k) {
+      uint32_t slot;
+      if (ring.next_free < t->Cs) {
+        slot = (uint32_t)ring.next_free++;
+      } else if (t->removal == GEAR_REMOVE_FIFO) {  // evict the oldest: ring front
+        slot = ring.ord[ring.head];
+        ring.head = (uint32_t)((ring.head + 1) % t->Cs);
+        ring.len -= 1;
+      } else {  // evict the newest: ring back
+        slot = ring.ord[(ring.head + ring.len - 1) % t->Cs];
+        ring.len -= 1;
+      }
+      const uint32_t pos = (uint32_t)((ring.head + ring.len) % t->Cs);
+      ring.ord[pos] = slot;
+      ring.len += 1;
+      auto it = pos_at.find(pos);
+      if (it == pos_at.end()) {
+        pos_at[pos] = n_ord;
+        t->h_ord[n_ord++] = OrdRec{(uint32_t)(ls * t->Cs + pos), slot};
+      } else {
+        t->h_ord[it->second].slot = slot;
+      }
+      const uint64_t seqv = ring.seq_ctr++;
+      auto jt = slot_at.find(slot);
+      if (jt == slot_at.end()) {
+        slot_at[slot] = n_meta;
+        t->h_meta[n_meta++] = InsMeta{ls * t->Cs + slot, seqv, 1u, k, p[k0 + k]};
+      } else {
+        InsMeta& im = t->h_meta[jt->second];
+        im.seq = seqv;
+        im.gen_inc += 1;
+        im.src_row = k;
+        im.prio = p[k0 + k];
+      }
+      t->h_out[k] = (uint64_t)shard * t->Cs + slot;
+    }
+    GEAR_CUDA(cudaMemcpyAsync(t->d_meta, t->h_meta, n_meta * sizeof(InsMeta), cudaMemcpyHostToDevice, s));
+    GEAR_CUDA(cudaMemcpyAsync(t->d_ord, t->h_ord, n_ord * sizeof(OrdRec), cudaMemcpyHostToDevice, s));
+    // Row sources: device / pinned host are read in place; pageable host is
+    // staged into device memory first.
+    ScatterParams sp{};
+    sp.meta = t->d_meta;
+    sp.ncols = (uint32_t)t->cols.size();
+    sp.m = n_meta;
+    sp.chunk_bytes = t->chunk_bytes;
+    uint64_t chunks = 0, stage_off = 0, stage_need = 0;
+    for (size_t c = 0; c < t->cols.size(); ++c)
+      if (kinds[c] == MemKind::HostPageable) stage_need += (uint64_t)m * t->cols[c].rb;
+    if (stage_need > t->d_rows_bytes) {
+      dfree(t->d_rows);
+      GEAR_TRY(dalloc(&t->d_rows, stage_need));
+      t->d_rows_bytes = stage_need;
+    }
+    for (size_t c = 0; c < t->cols.size(); ++c) {
+      ColumnState& cs = t->cols[c];
+      const uint8_t* src = (const uint8_t*)col_src[c] + (uint64_t)k0 * cs.rb;
+      if (kinds[c] == MemKind::HostPageable) {
+        GEAR_CUDA(cudaMemcpyAsync(t->d_rows + stage_off, src, (uint64_t)m * cs.rb, cudaMemcpyHostToDevice, s));
+        src = t->d_rows + stage_off;
+        stage_off += (uint64_t)m * cs.rb;
+      } else if (kinds[c] == MemKind::HostPinned) {
+        void* dp = nullptr;
+        GEAR_CUDA(cudaHostGetDevicePointer(&dp, (void*)src, 0));
+        src = (const uint8_t*)dp;
+      }
+      uint8_t* dst = (uint8_t*)cs.view[t->rank];
+      ScatterCol& sc = sp.col[c];
+      sc.dst = dst;
+      sc.src = src;
+      sc.rb = cs.rb;
+      sc.chunks_per_row = (uint32_t)((cs.rb + t->chunk_bytes - 1) / t->chunk_bytes);
+      sc.chunk_begin = chunks;
+      sc.vec = vec_width(cs.rb, t->chunk_bytes, {(uintptr_t)dst, (uintptr_t)src});
+      chunks += (uint64_t)n_meta * sc.chunks_per_row;
+    }
+    sp.total_chunks = chunks;
+    GEAR_CUDA(launch_scatter(sp, s));
+    GEAR_CUDA(launch_insert_meta(t->d_meta, n_meta, t->d_ord, n_ord, t->F, t->qmax, t->key,
+                                 t->seq, t->gen, t->ord, s));
+    if (out_idx) {
+      if (mem_kind(out_idx) == MemKind::Device) {
+        GEAR_CUDA(cudaMemcpyAsync(out_idx + k0, t->h_out, m * 8, cudaMemcpyHostToDevice, s));
+      } else {
+        std::memcpy(out_idx + k0, t->h_out, m * 8);
+      }
+    }
+    GEAR_CUDA(cudaEventRecord(t->staging_ev, s));
+  }
+  t->dirty = true;
+  return GEAR_OK;
+}
+
+gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* idx,
+                                   const void* prio, gear_dtype prio_dtype, const uint32_t* gen,
+                                   gear_stream stream) {
+  clear_error();
+  GEAR_TRY(check_table(t));
+  GEAR_CUDA(cudaSetDevice(t->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n > t->max_batch) return set_error(GEAR_ERR_INVALID_ARG, "n %u > max_batch %u", n, t->max_batch);
+  if (prio_dtype != GEAR_F32 && prio_dtype != GEAR_F64)
+    return set_error(GEAR_ERR_INVALID_ARG, "prio_dtype must be GEAR_F32 or GEAR_F64");
+  if (n > 0 && (idx == nullptr || prio == nullptr))
+    return set_error(GEAR_ERR_INVALID_ARG, "idx / prio is NULL");
+  const uint64_t* d_idx = idx;
+  const void* d_prio = prio;
+  const uint32_t* d_gen = gen;
+  if (n > 0) {
+    GEAR_TRY(stage_in(idx, n, t->upd_idx, s, &d_idx));
+    if (prio_dtype == GEAR_F64) {
+      const double* dp = nullptr;
+      GEAR_TRY(stage_in((const double*)prio, n, t->upd_prio, s, &dp));
+      d_prio = dp;
+    } else {
+      const float* dp = nullptr;
+      GEAR_TRY(stage_in((const float*)prio, n, (float*)t->upd_prio, s, &dp));
+      d_prio = dp;
+    }
+    if (gen) GEAR_TRY(stage_in(gen, n, t->upd_gen, s, &d_gen));
+  }
+  GEAR_CUDA(launch_update_quantize(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N, t->F,
+                                   t->qmax, t->upd_local, t->err, s));
+  const UpdRec* recs = t->upd_local;
+  uint32_t m = n;
+  if (t->W > 1) {
+    GEAR_TRY(allgather_bytes(t->comm, t->upd_local, t->upd_all, (size_t)n * sizeof(UpdRec), s));
+    recs = t->upd_all;
+    m = n * t->W;
+  }
+  t->epoch += 1;
+  const uint64_t local_begin = (uint64_t)t->rank * t->Clocal;
+  GEAR_CUDA(launch_update_tag(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->epoch,
+                              t->n_stale, t->err, s));
+  GEAR_CUDA(launch_update_apply(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->epoch,
+                                t->key, s));
+  t->dirty = true;
+  return GEAR_OK;
+}
+
+gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint64_t seed,
+                        double beta, uint64_t* out_idx, float* out_w, double* out_p,
+                        uint32_t* out_gen, gear_stream stream) {
+  clear_error();
+  GEAR_TRY(check_table(t));
+  GEAR_CUDA(cudaSetDevice(t->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (strategy < GEAR_FIFO || strategy > GEAR_PRIORITIZED)
+    return set_error(GEAR_ERR_INVALID_ARG, "bad strategy %d", (int)strategy);
+  if (B > t->max_batch) return set_error(GEAR_ERR_INVALID_ARG, "B %u > max_batch %u", B, t->max_batch);
+  if (B == 0) return GEAR_OK;
+  if (out_idx == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "out_idx is NULL");
+  if (!std::isfinite(beta)) return set_error(GEAR_ERR_INVALID_ARG, "beta is not finite");
+  // Outputs: device pointers are written in place, host ones via scratch.
+  const bool h_idx = mem_kind(out_idx) != MemKind::Device;
+  const bool h_w = out_w && mem_kind(out_w) != MemKind::Device;
+  const bool h_p = out_p && mem_kind(out_p) != MemKind::Device;
+  const bool h_gen = out_gen && mem_kind(out_gen) != MemKind::Device;
+  uint64_t* d_idx = h_idx ? t->tmp_idx : out_idx;
+  float* d_w = out_w ? (h_w ? t->tmp_w : out_w) : nullptr;
+  double* d_p = out_p ? (h_p ? t->tmp_p : out_p) : nullptr;
+  uint32_t* d_gen = out_gen ? (h_gen ? t->tmp_gen : out_gen) : nullptr;
+
+  if (strategy == GEAR_FIFO || strategy == GEAR_LIFO) {
+    const uint32_t K = t->W * B;
+    FifoRings rings{};
+    for (uint32_t ls = 0; ls < t->R; ++ls) {
+      rings.head[ls] = t->rings[ls].head;
+      rings.len[ls] = t->rings[ls].len;
+    }
+    const int lifo = strategy == GEAR_LIFO;
+    GEAR_CUDA(launch_fifo_local(t->key, t->seq, t->ord, rings, t->Cs, t->R, t->rank * t->R, K,
+                                lifo, t->cand_local, t->fifo_totals_local, s));
+    GEAR_TRY(allgather_bytes(t->comm, t->cand_local, t->cand_all, (size_t)t->R * K * sizeof(Cand), s));
+    GEAR_TRY(allgather_bytes(t->comm, t->fifo_totals_local, t->fifo_totals_all,
+                             t->R * sizeof(ShardTotals), s));
+    GEAR_CUDA(launch_fifo_merge(t->cand_all, t->fifo_totals_all, t->S, K, lifo, t->Cs, t->rank,
+                                B, t->d_gen_ptrs, t->R, d_idx, d_w, d_p, d_gen, t->err, s));
+  } else {
+    const int mode = strategy == GEAR_UNIFORM ? 1 : 0;
+    if (t->dirty || t->cdf_mode != mode) {
+      // Rebuild into the other buffer: peers may still search the current one.
+      t->cdf_parity ^= 1;
+      const int l = (int)(t->scan_launches & 1);
+      GEAR_CUDA(launch_scan(t->key, t->cdf[t->cdf_parity], t->Cs, t->R, mode, t->cdf_parity,
+                            t->cdf_totals_local, t->scan_status[l], t->scan_status[l ^ 1],
+                            t->scan_ticket[l], t->scan_ticket[l ^ 1], s));
+      t->scan_launches += 1;
+      t->cdf_mode = mode;
+      t->dirty = false;
+    }
+    // Every step publishes the totals; the all-gather is also the barrier
+    // that makes every shard's CDF visible before anyone searches it.
+    GEAR_TRY(allgather_bytes(t->comm, t->cdf_totals_local, t->cdf_totals_all,
+                             t->R * sizeof(ShardTotals), s));
+    SampleParams sp{};
+    sp.totals = t->cdf_totals_all;
+    sp.cdf_ptrs = t->d_cdf_ptrs;
+    sp.gen_ptrs = t->d_gen_ptrs;
+    sp.shard_cap = t->Cs;
+    sp.n_shards = t->S;
+    sp.shards_per_rank = t->R;
+    sp.seed = seed;
+    sp.rank = t->rank;
+    sp.B = B;
+    sp.beta = beta;
+    sp.strategy = (int)strategy;
+    sp.out_idx = d_idx;
+    sp.out_w = d_w;
+    sp.out_p = d_p;
+    sp.out_gen = d_gen;
+    sp.q_scratch = t->q_scratch;
+    sp.qmin_slot = t->qmin_slot;
+    sp.done_ctr = t->done_ctr;
+    sp.err = t->err;
+    GEAR_CUDA(launch_sample(sp, s));
+  }
+  if (h_idx) GEAR_CUDA(cudaMemcpyAsync(out_idx, d_idx, B * 8ull, cudaMemcpyDeviceToHost, s));
+  if (h_w) GEAR_CUDA(cudaMemcpyAsync(out_w, d_w, B * 4ull, cudaMemcpyDeviceToHost, s));
+  if (h_p) GEAR_CUDA(cudaMemcpyAsync(out_p, d_p, B * 8ull, cudaMemcpyDeviceToHost, s));
+  if (h_gen) GEAR_CUDA(cudaMemcpyAsync(out_gen, d_gen, B * 4ull, cudaMemcpyDeviceToHost, s));
+  return GEAR_OK;
+}
+
+gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_t ncols,
+                         const uint32_t* col_ids, void* const* out, gear_stream stream) {
+  clear_error();
+  GEAR_TRY(check_table(t));
+  GEAR_CUDA(cudaSetDevice(t->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0 || ncols == 0) return GEAR_OK;
+  if (idx == nullptr || col_ids == nullptr || out == nullptr)
+    return set_error(GEAR_ERR_INVALID_ARG, "NULL argument");
+  if (ncols > (uint32_t)kMaxCols) return set_error(GEAR_ERR_INVALID_ARG, "ncols > %d", kMaxCols);
+  const uint64_t* d_idx = idx;
+  if (mem_kind(idx) != MemKind::Device) {
+    if (t->col_idx.n < n) {
+      dfree(t->col_idx.p);
+      GEAR_TRY(dalloc(&t->col_idx.p, n));
+      t->col_idx.n = n;
+    }
+    GEAR_CUDA(cudaMemcpyAsync(t->col_idx.p, idx, n * 8ull, cudaMemcpyHostToDevice, s));
+    d_idx = t->col_idx.p;
+  }
+  CollectParams cp{};
+  cp.idx = d_idx;
+  cp.rows_per_rank = t->Clocal;
+  cp.n_global = t->N;
+  cp.ncols = ncols;
+  cp.n = n;
+  cp.chunk_bytes = t->chunk_bytes;
+  cp.err = t->err;
+  uint64_t chunks = 0;
+  for (uint32_t c = 0; c < ncols; ++c) {
+    if (col_ids[c] >= t->cols.size()) return set_error(GEAR_ERR_INVALID_ARG, "bad column id %u", col_ids[c]);
+    if (out[c] == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "out[%u] is NULL", c);
+    const ColumnState& cs = t->cols[col_ids[c]];
+    CollectCol& cc = cp.col[c];
+    cc.out = (uint8_t*)out[c];
+    cc.rb = cs.rb;
+    cc.chunks_per_row = (uint32_t)((cs.rb + t->chunk_bytes - 1) / t->chunk_bytes);
+    cc.chunk_begin = chunks;
+    uintptr_t align_or = (uintptr_t)out[c];
+    for (uint32_t r = 0; r < t->W; ++r) {
+      cc.src[r] = cs.view[r];
+      align_or |= (uintptr_t)cs.view[r];
+    }
+    cc.vec = vec_width(cs.rb, t->chunk_bytes, {align_or});
+    chunks += (uint64_t)n * cc.chunks_per_row;
+  }
+  cp.total_chunks = chunks;
+  GEAR_CUDA(launch_collect(cp, s));
+  return GEAR_OK;
+}
+
+gear_status gear_table_sync(gear_table* t, uint32_t* dev_errors, uint64_t* n_stale) {
+  clear_error();
+  GEAR_TRY(check_table(t));
+  GEAR_CUDA(cudaSetDevice(t->device));
+  GEAR_CUDA(cudaDeviceSynchronize());
+  uint32_t e = 0;
+  unsigned long long ns = 0;
+  GEAR_CUDA(cudaMemcpy(&e, t->err, 4, cudaMemcpyDeviceToHost));
+  GEAR_CUDA(cudaMemcpy(&ns, t->n_stale, 8, cudaMemcpyDeviceToHost));
+  GEAR_CUDA(cudaMemset(t->err, 0, 4));
+  GEAR_CUDA(cudaMemset(t->n_stale, 0, 8));
+  if (dev_errors) *dev_errors = e;
+  if (n_stale) *n_stale = ns;
+  if (e) return set_error(GEAR_ERR_STATE, "device error bits 0x%x", e);
+  return GEAR_OK;
+}
+
+gear_status gear_read_state(gear_table* t, uint64_t* key, uint64_t* seq, uint32_t* gen) {
+  clear_error();
+  GEAR_TRY(check_table(t));
+  GEAR_CUDA(cudaSetDevice(t->device));
+  GEAR_CUDA(cudaDeviceSynchronize());
+  if (key) GEAR_CUDA(cudaMemcpy(key, t->key, t->Clocal * 8, cudaMemcpyDeviceToHost));
+  if (seq) GEAR_CUDA(cudaMemcpy(seq, t->seq, t->Clocal * 8, cudaMemcpyDeviceToHost));
+  if (gen) GEAR_CUDA(cudaMemcpy(gen, t->gen, t->Clocal * 4, cudaMemcpyDeviceToHost));
+  return GEAR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,179 @@
+// gear_internal.h -- structures shared by the host runtime (api.cpp, comm.cpp)
+// and the sm_100a kernels (kernels/*.cu).  Not part of the C-ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace gear {
+
+constexpr int kMaxCols = 16;
+constexpr int kMaxRanks = 8;
+constexpr int kMaxShards = 32;
+constexpr uint64_t kIdxNone = ~0ull;
+
+// Device error latch bits (mirror GEAR_DEVERR_* of gear.h).
+constexpr uint32_t kErrIndexRange = 1u;
+constexpr uint32_t kErrBadPriority = 2u;
+constexpr uint32_t kErrStale = 4u;
+constexpr uint32_t kErrEmpty = 8u;
+
+// Strategy codes (mirror gear_strategy).
+constexpr int kFifo = 0, kLifo = 1, kUniform = 2, kWeighted = 3, kPrioritized = 4;
+
+// Per-shard totals record exchanged between ranks (16 B): total weight T_s of
+// the shard's CDF with the CDF buffer parity in bit 63 (T_s < 2^62 by q_max),
+// and the number of valid FIFO/LIFO candidates the shard offers.
+struct ShardTotals {
+  uint64_t total_and_parity;
+  uint64_t aux;
+};
+
+// One priority-update entry after quantisation (24 B), exchanged between
+// ranks for a collective update.
+struct UpdRec {
+  uint64_t idx;    // global id, or kIdxNone for a skipped entry
+  uint64_t q;      // fixed-point key Q_F(p)
+  uint32_t gen;    // expected generation when flags & 2
+  uint32_t flags;  // bit0 valid, bit1 has generation
+};
+
+// One slot written by gear_insert (after host-side de-duplication).
+struct InsMeta {
+  uint64_t local;    // rank-local slot (shard_local * C_s + i)
+  uint64_t seq;      // new seq value
+  uint32_t gen_inc;  // how many inserts landed in the slot in this call
+  uint32_t src_row;  // row of the caller's source arrays that wins the slot
+  double prio;       // priority of that row (validated on the host)
+};
+
+// One ring-order entry written by gear_insert: ord[pos] = slot (both
+// rank-local; pos indexes the rank's concatenated per-shard rings).
+struct OrdRec {
+  uint32_t pos;
+  uint32_t slot;
+};
+
+// FIFO/LIFO candidate (16 B): the ordering key is (seq, shard).
+struct Cand {
+  uint64_t seq;
+  uint32_t shard;
+  uint32_t slot;  // shard-local slot
+};
+
+struct CollectCol {
+  uint8_t* out;                       // [n][rb] output batch
+  const uint8_t* src[kMaxRanks];      // device-accessible base of each rank's rows
+  uint64_t rb;                        // row bytes
+  uint64_t chunk_begin;               // first global chunk id of this column
+  uint32_t chunks_per_row;
+  uint32_t vec;                       // vector width in bytes: 16, 8, 4 or 1
+};
+
+struct CollectParams {
+  CollectCol col[kMaxCols];
+  const uint64_t* idx;                // [n] global ids (device)
+  uint64_t rows_per_rank;             // R * C_s
+  uint64_t n_global;                  // N
+  uint64_t total_chunks;
+  uint32_t ncols;
+  uint32_t n;
+  uint32_t chunk_bytes;               // bytes per warp task
+  uint32_t* err;
+};
+
+// Insert-side row scatter: dst row slot[j] <- src row src_row[j].
+struct ScatterCol {
+  uint8_t* dst;
+  const uint8_t* src;
+  uint64_t rb;
+  uint64_t chunk_begin;
+  uint32_t chunks_per_row;
+  uint32_t vec;
+};
+
+struct ScatterParams {
+  ScatterCol col[kMaxCols];
+  const InsMeta* meta;                // [m]
+  uint64_t total_chunks;
+  uint32_t ncols;
+  uint32_t m;
+  uint32_t chunk_bytes;
+};
+
+struct SampleParams {
+  const ShardTotals* totals;          // [S]
+  const uint64_t* const* cdf_ptrs;    // [2*S]: parity p of shard s at [p*S + s]
+  const uint32_t* const* gen_ptrs;    // [W]: each rank's gen array
+  uint64_t shard_cap;                 // C_s
+  uint32_t n_shards;                  // S
+  uint32_t shards_per_rank;           // R
+  uint64_t seed;
+  uint32_t rank;
+  uint32_t B;
+  double beta;
+  int strategy;
+  uint64_t* out_idx;
+  float* out_w;
+  double* out_p;
+  uint32_t* out_gen;
+  uint64_t* q_scratch;                // [B]
+  unsigned long long* qmin_slot;      // reset to ~0 by the last block
+  uint32_t* done_ctr;                 // reset to 0 by the last block
+  uint32_t* err;
+};
+
+// ---- kernel launchers (kernels/*.cu) --------------------------------------
+
+// K1: per-shard inclusive u64 scan with decoupled look-back.  Writes cdf for
+// `n_shards_local` contiguous shards of `shard_cap` keys and their totals.
+// indicator != 0 scans [key > 0] instead of key.
+cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf, uint64_t shard_cap,
+                        uint32_t n_shards_local, int indicator, uint32_t parity,
+                        ShardTotals* totals_out, uint64_t* status_cur, uint64_t* status_next,
+                        uint32_t* ticket_cur, uint32_t* ticket_next, cudaStream_t s);
+uint32_t scan_tiles_per_shard(uint64_t shard_cap);
+
+// K2/K3/K7: draw + warp-cooperative search + IS weights.
+cudaError_t launch_sample(const SampleParams& p, cudaStream_t s);
+
+// K6: priority update.
+cudaError_t launch_update_quantize(const uint64_t* idx, const void* prio, int prio_is_f64,
+                                   const uint32_t* gen, uint32_t n, uint64_t n_global,
+                                   uint32_t frac_bits, uint64_t q_max, UpdRec* out,
+                                   uint32_t* err, cudaStream_t s);
+cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_begin,
+                              uint64_t local_rows, const uint32_t* gen, unsigned long long* tag,
+                              uint32_t epoch, unsigned long long* n_stale, uint32_t* err,
+                              cudaStream_t s);
+cudaError_t launch_update_apply(const UpdRec* recs, uint32_t m, uint64_t local_begin,
+                                uint64_t local_rows, const uint32_t* gen,
+                                const unsigned long long* tag, uint32_t epoch, uint64_t* key,
+                                cudaStream_t s);
+
+// K5: collect (gather) and the insert-side scatter.
+cudaError_t launch_collect(const CollectParams& p, cudaStream_t s);
+cudaError_t launch_scatter(const ScatterParams& p, cudaStream_t s);
+cudaError_t launch_insert_meta(const InsMeta* meta, uint32_t m, const OrdRec* ord_recs,
+                               uint32_t n_ord, uint32_t frac_bits, uint64_t q_max,
+                               uint64_t* key, uint64_t* seq, uint32_t* gen, uint32_t* ord,
+                               cudaStream_t s);
+
+// K4: FIFO/LIFO local selection and merge.
+struct FifoRings {
+  uint32_t head[kMaxShards];  // ring start of each local shard (oldest entry)
+  uint32_t len[kMaxShards];   // committed entries in the ring
+};
+cudaError_t launch_fifo_local(const uint64_t* key, const uint64_t* seq, const uint32_t* ord,
+                              const FifoRings& rings, uint64_t shard_cap,
+                              uint32_t n_shards_local, uint32_t first_shard, uint32_t K,
+                              int lifo, Cand* cand_out, ShardTotals* totals_out, cudaStream_t s);
+cudaError_t launch_fifo_merge(const Cand* cand_all, const ShardTotals* totals_all,
+                              uint32_t n_shards, uint32_t K, int lifo, uint64_t shard_cap,
+                              uint32_t rank, uint32_t B, const uint32_t* const* gen_ptrs,
+                              uint32_t shards_per_rank, uint64_t* out_idx, float* out_w,
+                              double* out_p, uint32_t* out_gen, uint32_t* err, cudaStream_t s);
+
+}  // namespace gear

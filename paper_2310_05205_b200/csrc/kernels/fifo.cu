@@ -1,0 +1,165 @@
+// fifo.cu -- K4: decentralised FIFO/LIFO selection.
+//
+// "all servers can perform a local scan to generate k samples before the
+// global gathering operation, which can significantly reduce the
+// communication overhead from O(n) to O(mk)".  Each shard keeps its committed
+// slots in insertion order in a ring (`ord`, maintained by gear_insert), so
+// seq is increasing along the ring.  Local step: one CTA per local shard
+// walks the ring from the oldest (FIFO) or newest (LIFO) end and compacts the
+// first K = W*B selectable slots (key > 0) with a block-wide ballot scan,
+// stopping as soon as it has K.  After the candidates of all S shards are
+// all-gathered, every rank runs the same merge: a candidate's global position
+// is its position in its own (sorted) list plus, for every other list, the
+// number of entries that order before it under (seq, shard) -- a binary
+// search per list.  Rank r keeps positions [r*B, (r+1)*B).
+#include "common.cuh"
+
+namespace gear {
+
+namespace {
+
+constexpr int kLocalThreads = 1024;
+constexpr int kMergeThreads = 256;
+
+__global__ void __launch_bounds__(kLocalThreads)
+    fifo_local_kernel(const uint64_t* __restrict__ key, const uint64_t* __restrict__ seq,
+                      const uint32_t* __restrict__ ord, const __grid_constant__ FifoRings rings,
+                      uint64_t shard_cap, uint32_t first_shard, uint32_t K, int lifo,
+                      Cand* __restrict__ cand_out, ShardTotals* __restrict__ totals_out) {
+  __shared__ uint32_t s_warp[kLocalThreads / 32];
+  __shared__ uint32_t s_count;
+  const uint32_t ls = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t base = (uint64_t)ls * shard_cap;
+  const uint32_t head = rings.head[ls], len = rings.len[ls];
+  Cand* out = cand_out + (uint64_t)ls * K;
+  if (tid == 0) s_count = 0;
+  __syncthreads();
+  for (uint32_t k0 = 0; k0 < len; k0 += kLocalThreads) {
+    const uint32_t count = s_count;
+    if (count >= K) break;
+    const uint32_t k = k0 + tid;
+    bool sel = false;
+    uint32_t slot = 0;
+    if (k < len) {
+      const uint64_t step = lifo ? (uint64_t)len - 1 - k : (uint64_t)k;
+      const uint64_t pos = ((uint64_t)head + step) % shard_cap;
+      slot = ord[base + pos];
+      sel = key[base + slot] > 0;
+    }
+    const unsigned m = __ballot_sync(kFull, sel);
+    if (lane == 0) s_warp[warp] = __popc(m);
+    __syncthreads();
+    uint32_t before = 0, total = 0;
+#pragma unroll 4
+    for (int w = 0; w < kLocalThreads / 32; ++w) {
+      const uint32_t x = s_warp[w];
+      before += w < warp ? x : 0u;
+      total += x;
+    }
+    const uint32_t at = count + before + __popc(m & ((1u << lane) - 1u));
+    if (sel && at < K) {
+      Cand c;
+      c.seq = seq[base + slot];
+      c.shard = first_shard + ls;
+      c.slot = slot;
+      out[at] = c;
+    }
+    __syncthreads();
+    if (tid == 0) s_count = count + total;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    ShardTotals t;
+    t.total_and_parity = 0;
+    t.aux = s_count < K ? s_count : K;
+    totals_out[ls] = t;
+  }
+}
+
+// Number of entries of the sorted list c[0..n) that order before (sq, s)
+// under (seq, shard) -- ascending lists for FIFO, descending for LIFO.
+__device__ __forceinline__ uint32_t count_before(const Cand* __restrict__ c, uint32_t n,
+                                                 uint32_t list_shard, uint64_t sq, uint32_t s,
+                                                 int lifo) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    const uint64_t e = c[mid].seq;
+    bool b;
+    if (!lifo) b = e < sq || (e == sq && list_shard < s);
+    else b = e > sq || (e == sq && list_shard > s);
+    if (b) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kMergeThreads)
+    fifo_merge_kernel(const Cand* __restrict__ cand_all, const ShardTotals* __restrict__ totals,
+                      uint32_t S, uint32_t K, int lifo, uint64_t shard_cap, uint32_t rank,
+                      uint32_t B, const uint32_t* const* gen_ptrs, uint32_t shards_per_rank,
+                      uint64_t* out_idx, float* out_w, double* out_p, uint32_t* out_gen,
+                      uint32_t* err) {
+  const uint64_t t = (uint64_t)blockIdx.x * kMergeThreads + threadIdx.x;
+  uint64_t avail = 0;
+  for (uint32_t s = 0; s < S; ++s) avail += totals[s].aux;
+  if (avail < K) {  // fewer than W*B selectable: EMPTY
+    if (t < B) {
+      out_idx[t] = kIdxNone;
+      if (out_w) out_w[t] = 0.0f;
+      if (out_p) out_p[t] = 0.0;
+      if (out_gen) out_gen[t] = 0;
+    }
+    if (t == 0) atomicOr(err, kErrEmpty);
+    return;
+  }
+  if (t >= (uint64_t)S * K) return;
+  const uint32_t s = (uint32_t)(t / K), p = (uint32_t)(t - (uint64_t)s * K);
+  if (p >= totals[s].aux) return;
+  const Cand me = cand_all[t];
+  uint64_t pos = p;
+  for (uint32_t s2 = 0; s2 < S; ++s2) {
+    if (s2 == s) continue;
+    pos += count_before(cand_all + (uint64_t)s2 * K, (uint32_t)totals[s2].aux, s2, me.seq, s,
+                        lifo);
+  }
+  const uint64_t lo = (uint64_t)rank * B;
+  if (pos < lo || pos >= lo + B) return;
+  const uint32_t b = (uint32_t)(pos - lo);
+  out_idx[b] = (uint64_t)me.shard * shard_cap + me.slot;
+  if (out_w) out_w[b] = 1.0f;
+  if (out_p) out_p[b] = 1.0;
+  if (out_gen) {
+    const uint32_t owner = me.shard / shards_per_rank;
+    const uint64_t local = (uint64_t)(me.shard % shards_per_rank) * shard_cap + me.slot;
+    out_gen[b] = gen_ptrs[owner][local];
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_fifo_local(const uint64_t* key, const uint64_t* seq, const uint32_t* ord,
+                              const FifoRings& rings, uint64_t shard_cap,
+                              uint32_t n_shards_local, uint32_t first_shard, uint32_t K,
+                              int lifo, Cand* cand_out, ShardTotals* totals_out, cudaStream_t s) {
+  fifo_local_kernel<<<n_shards_local, kLocalThreads, 0, s>>>(
+      key, seq, ord, rings, shard_cap, first_shard, K, lifo, cand_out, totals_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fifo_merge(const Cand* cand_all, const ShardTotals* totals_all,
+                              uint32_t n_shards, uint32_t K, int lifo, uint64_t shard_cap,
+                              uint32_t rank, uint32_t B, const uint32_t* const* gen_ptrs,
+                              uint32_t shards_per_rank, uint64_t* out_idx, float* out_w,
+                              double* out_p, uint32_t* out_gen, uint32_t* err, cudaStream_t s) {
+  const uint64_t n = (uint64_t)n_shards * K;
+  const uint64_t threads = n > B ? n : B;
+  const uint32_t grid = (uint32_t)((threads + kMergeThreads - 1) / kMergeThreads);
+  fifo_merge_kernel<<<grid, kMergeThreads, 0, s>>>(cand_all, totals_all, n_shards, K, lifo,
+                                                   shard_cap, rank, B, gen_ptrs, shards_per_rank,
+                                                   out_idx, out_w, out_p, out_gen, err);
+  return cudaGetLastError();
+}
+
+}  // namespace gear

@@ -1,0 +1,146 @@
+// sample.cu -- K2/K3/K7: batched inverse-CDF sampling.
+//
+// "performs binary searching to locate the bins associated with
+// uniformly generated random numbers".  One warp per draw j of the rank's
+// slice [rank*B, rank*B + B) of the global batch:
+//   r  = Philox4x32-10(counter j, key seed)            (64 bits)
+//   u  = floor(r * T / 2^64), T = sum of the S shard totals (exact, mulhi)
+//   s  = the shard whose exclusive offset range [G_s, G_s + T_s) holds u
+//   i  = min{ i : cdf_s[i] > u - G_s }  -- 32-ary warp-cooperative search:
+//        each round the 32 lanes probe 32 evenly spaced pivots of the live
+//        range and a ballot keeps the first bin that can hold the answer, so
+//        a shard of C_s keys takes ceil(log32 C_s) dependent rounds instead
+//        of ceil(log2 C_s).  cdf_s may live in a peer GPU's HBM (read over
+//        NVLink through a CUDA-IPC mapping).
+//   g  = s*C_s + i,  q = cdf_s[i] - cdf_s[i-1]
+// The IS weights (q_min/q)^beta need the min over the whole slice; the last
+// block to finish (threadfence + counter) computes them and re-arms the
+// counter and the min slot for the next launch.
+#include "common.cuh"
+
+namespace gear {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ uint64_t search_shard(const uint64_t* __restrict__ c, uint64_t n,
+                                                 uint64_t u, int lane, uint64_t* q_out) {
+  uint64_t lo = 0, hi = n;  // answer in [lo, hi); c[hi-1] > u
+  while (hi - lo > 32) {
+    const uint64_t len = hi - lo;
+    const uint64_t step = (len + 31) >> 5;
+    uint64_t piv = lo + (uint64_t)(lane + 1) * step - 1;
+    piv = piv > hi - 1 ? hi - 1 : piv;
+    const bool gt = c[piv] > u;
+    const unsigned m = __ballot_sync(kFull, gt);
+    const int f = __ffs(m) - 1;
+    const uint64_t piv_f = __shfl_sync(kFull, piv, f);
+    const uint64_t piv_b = __shfl_sync(kFull, piv, f > 0 ? f - 1 : 0);
+    hi = piv_f + 1;
+    lo = f > 0 ? piv_b + 1 : lo;
+  }
+  const uint64_t pos = lo + lane;
+  const uint64_t cv = pos < hi ? c[pos] : ~0ull;
+  const uint64_t before = (lane == 0 && lo > 0) ? c[lo - 1] : 0ull;
+  const unsigned m = __ballot_sync(kFull, pos < hi && cv > u);
+  const int f = __ffs(m) - 1;
+  const uint64_t cf = __shfl_sync(kFull, cv, f);
+  const uint64_t cprev_lane = __shfl_sync(kFull, cv, f > 0 ? f - 1 : 0);
+  const uint64_t cprev0 = __shfl_sync(kFull, before, 0);
+  *q_out = cf - (f > 0 ? cprev_lane : cprev0);
+  return lo + (uint64_t)f;
+}
+
+__global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
+  __shared__ unsigned long long s_min[kWarps];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t b = blockIdx.x * kWarps + warp;
+  const bool prioritized = p.strategy == kPrioritized;
+
+  // Shard totals -> exclusive offsets (S <= 32: one lane per shard).
+  const uint32_t S = p.n_shards;
+  uint64_t Ts = 0;
+  uint32_t par = 0;
+  if ((uint32_t)lane < S) {
+    const uint64_t tp = p.totals[lane].total_and_parity;
+    Ts = tp & ((1ull << 62) - 1);
+    par = (uint32_t)(tp >> 63);
+  }
+  const uint64_t G = warp_incl_scan_u64(Ts, lane);
+  const uint64_t T = __shfl_sync(kFull, G, 31);
+
+  uint64_t my_q = ~0ull;
+  if (b < p.B) {
+    const uint64_t j = (uint64_t)p.rank * p.B + b;
+    uint64_t g = kIdxNone, q = 0;
+    if (T > 0) {
+      const uint64_t r = draw_bits(p.seed, j);
+      const uint64_t u = __umul64hi(r, T);
+      const unsigned own = __ballot_sync(kFull, (uint32_t)lane < S && G > u);
+      const int s = __ffs(own) - 1;
+      const uint64_t Gs_incl = __shfl_sync(kFull, G, s);
+      const uint64_t Ts_s = __shfl_sync(kFull, Ts, s);
+      const uint32_t par_s = __shfl_sync(kFull, par, s);
+      const uint64_t* cdf = p.cdf_ptrs[(uint64_t)par_s * S + s];
+      const uint64_t i = search_shard(cdf, p.shard_cap, u - (Gs_incl - Ts_s), lane, &q);
+      g = (uint64_t)s * p.shard_cap + i;
+      if (lane == 0) {
+        if (p.out_gen) {
+          const uint32_t r_owner = (uint32_t)s / p.shards_per_rank;
+          const uint64_t local = (uint64_t)(s % p.shards_per_rank) * p.shard_cap + i;
+          p.out_gen[b] = p.gen_ptrs[r_owner][local];
+        }
+      }
+    } else if (lane == 0) {
+      atomicOr(p.err, kErrEmpty);
+      if (p.out_gen) p.out_gen[b] = 0;
+    }
+    if (lane == 0) {
+      p.out_idx[b] = g;
+      if (p.out_p) p.out_p[b] = T > 0 ? (double)q / (double)T : 0.0;
+      if (p.out_w && !prioritized) p.out_w[b] = T > 0 ? 1.0f : 0.0f;
+      p.q_scratch[b] = q;
+    }
+    my_q = T > 0 ? q : ~0ull;
+  }
+  if (!prioritized || p.out_w == nullptr) return;
+
+  // Slice-wide q_min, then the last block writes the weights.
+  if (lane == 0) s_min[warp] = my_q;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long m = ~0ull;
+    for (int w = 0; w < kWarps; ++w) m = s_min[w] < m ? s_min[w] : m;
+    atomicMin(p.qmin_slot, m);
+    __threadfence();
+    const uint32_t done = atomicAdd(p.done_ctr, 1u);
+    s_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const unsigned long long qmin = *(volatile unsigned long long*)p.qmin_slot;
+  for (uint32_t k = threadIdx.x; k < p.B; k += kThreads) {
+    const uint64_t q = *(volatile uint64_t*)(p.q_scratch + k);
+    p.out_w[k] = (T > 0 && q > 0) ? (float)pow((double)qmin / (double)q, p.beta) : 0.0f;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *p.qmin_slot = ~0ull;
+    *p.done_ctr = 0;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_sample(const SampleParams& p, cudaStream_t s) {
+  if (p.B == 0) return cudaSuccess;
+  const uint32_t grid = (p.B + kWarps - 1) / kWarps;
+  sample_kernel<<<grid, kThreads, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace gear

@@ -1,0 +1,171 @@
+// scan.cu -- K1: the CDF of each shard as a single-pass u64 inclusive scan
+// with decoupled look-back ("computes a prefix sum array using
+// the decoupled look-back algorithm").
+//
+// Layout: a rank's R shards are contiguous in `key` (R * C_s u64); tile t of
+// the launch covers kTile keys of shard t / tiles_per_shard.  Tile ids come
+// from an atomic ticket so a tile only ever waits on tiles that already run
+// (forward progress).  Each tile publishes one 64-bit status word: the top
+// two bits are the flag (0 = not ready, 1 = aggregate, 2 = inclusive prefix)
+// and the low 62 bits the value -- the keys are capped so every shard total
+// is < 2^62 (gear.h q_max), so flag and value travel in one relaxed 64-bit
+// store and need no fence.  Integer addition is associative, so the result is
+// bit-identical to a sequential sum whatever the tiling.
+//
+// Two status arrays and two tickets alternate between launches; each launch
+// clears the other pair for the next one, so no memset launch is needed.
+#include "common.cuh"
+
+namespace gear {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kItems = 16;                  // keys per thread
+constexpr int kTile = kThreads * kItems;    // 4096 keys = 32 KB per tile
+constexpr uint64_t kFlagA = 1ull << 62;
+constexpr uint64_t kFlagP = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+template <bool kIndicator>
+__global__ void __launch_bounds__(kThreads) scan_kernel(
+    const uint64_t* __restrict__ key, uint64_t* __restrict__ cdf, uint64_t shard_cap,
+    uint32_t tiles_per_shard, uint32_t n_tiles, uint32_t parity, ShardTotals* totals,
+    uint64_t* status, uint64_t* status_next, uint32_t* ticket, uint32_t* ticket_next) {
+  __shared__ uint32_t s_tile;
+  __shared__ uint64_t s_warp[kThreads / 32];
+  __shared__ uint64_t s_excl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t t = s_tile;
+  // Clear this tile's slot of the next launch's status pair.
+  if (tid == 0) {
+    status_next[t] = 0;
+    if (t == 0) *ticket_next = 0;
+  }
+  const uint32_t shard = t / tiles_per_shard;
+  const uint32_t tt = t - shard * tiles_per_shard;
+  const uint64_t shard_base = (uint64_t)shard * shard_cap;
+  const uint64_t tile_begin = (uint64_t)tt * kTile;
+  const uint64_t my_begin = tile_begin + (uint64_t)tid * kItems;  // within shard
+
+  // Load kItems consecutive keys (16-byte vector loads when fully inside).
+  uint64_t v[kItems];
+  if (my_begin + kItems <= shard_cap && ((shard_base + my_begin) & 1) == 0) {
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(key + shard_base + my_begin);
+#pragma unroll
+    for (int i = 0; i < kItems / 2; ++i) {
+      const ulonglong2 x = __ldg(src + i);
+      v[2 * i] = x.x;
+      v[2 * i + 1] = x.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kItems; ++i)
+      v[i] = (my_begin + i < shard_cap) ? key[shard_base + my_begin + i] : 0ull;
+  }
+  if (kIndicator) {
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) v[i] = v[i] > 0 ? 1ull : 0ull;
+  }
+  // Thread-local inclusive prefix.
+#pragma unroll
+  for (int i = 1; i < kItems; ++i) v[i] += v[i - 1];
+  // Warp and block scan of the thread totals.
+  const uint64_t incl = warp_incl_scan_u64(v[kItems - 1], lane);
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  uint64_t warp_excl = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) {
+    const uint64_t x = s_warp[w];
+    warp_excl += (w < warp) ? x : 0ull;
+    agg += x;
+  }
+  const uint64_t thread_excl = warp_excl + incl - v[kItems - 1];
+
+  // Publish the aggregate (or the inclusive prefix for a shard's first tile)
+  // and look back over the predecessors of the same shard.
+  if (warp == 0) {
+    uint64_t excl = 0;
+    if (tt == 0) {
+      if (lane == 0) st_relaxed_u64(status + t, kFlagP | agg);
+    } else {
+      if (lane == 0) st_relaxed_u64(status + t, kFlagA | agg);
+      const int64_t first = (int64_t)t - (int64_t)tt;  // shard's first tile
+      int64_t pred = (int64_t)t - 1;
+      while (true) {
+        const int64_t idx = pred - lane;
+        const bool valid = idx >= first;
+        uint64_t s = valid ? ld_relaxed_u64(status + idx) : kFlagP;
+        while (__any_sync(kFull, (s >> 62) == 0)) {
+          if ((s >> 62) == 0) s = ld_relaxed_u64(status + idx);
+        }
+        const unsigned pmask = __ballot_sync(kFull, valid && (s >> 62) == 2);
+        const uint64_t val = valid ? (s & kValMask) : 0ull;
+        if (pmask) {
+          const int lp = __ffs(pmask) - 1;  // closest inclusive predecessor
+          uint64_t part = lane <= lp ? val : 0ull;
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(kFull, part, d);
+          excl += part;
+          break;
+        }
+        uint64_t part = val;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(kFull, part, d);
+        excl += part;
+        pred -= 32;
+      }
+      if (lane == 0) st_relaxed_u64(status + t, kFlagP | (excl + agg));
+    }
+    if (lane == 0) s_excl = excl;
+  }
+  __syncthreads();
+  const uint64_t base = s_excl + thread_excl;
+
+  // Store the CDF.
+  if (my_begin + kItems <= shard_cap && ((shard_base + my_begin) & 1) == 0) {
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(cdf + shard_base + my_begin);
+#pragma unroll
+    for (int i = 0; i < kItems / 2; ++i)
+      dst[i] = make_ulonglong2(base + v[2 * i], base + v[2 * i + 1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < kItems; ++i)
+      if (my_begin + i < shard_cap) cdf[shard_base + my_begin + i] = base + v[i];
+  }
+  if (tt == tiles_per_shard - 1 && tid == 0) {
+    ShardTotals r;
+    r.total_and_parity = (s_excl + agg) | ((uint64_t)parity << 63);
+    r.aux = 0;
+    totals[shard] = r;
+  }
+}
+
+}  // namespace
+
+uint32_t scan_tiles_per_shard(uint64_t shard_cap) {
+  return (uint32_t)((shard_cap + kTile - 1) / kTile);
+}
+
+cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf, uint64_t shard_cap,
+                        uint32_t n_shards_local, int indicator, uint32_t parity,
+                        ShardTotals* totals_out, uint64_t* status_cur, uint64_t* status_next,
+                        uint32_t* ticket_cur, uint32_t* ticket_next, cudaStream_t s) {
+  const uint32_t tps = scan_tiles_per_shard(shard_cap);
+  const uint32_t n_tiles = tps * n_shards_local;
+  if (indicator)
+    scan_kernel<true><<<n_tiles, kThreads, 0, s>>>(key, cdf, shard_cap, tps, n_tiles, parity,
+                                                   totals_out, status_cur, status_next,
+                                                   ticket_cur, ticket_next);
+  else
+    scan_kernel<false><<<n_tiles, kThreads, 0, s>>>(key, cdf, shard_cap, tps, n_tiles, parity,
+                                                    totals_out, status_cur, status_next,
+                                                    ticket_cur, ticket_next);
+  return cudaGetLastError();
+}
+
+}  // namespace gear

@@ -1,0 +1,125 @@
+// update.cu -- K6: priority update (quantise -> route -> last-writer-wins
+// scatter).  The paper keeps priorities in the status table
+// without a type; gear.h fixes the u64 fixed-point key Q_F(p).
+//
+// Duplicate ids must resolve deterministically to the LAST entry in (rank,
+// position) order.  Racing stores cannot promise that, so the scatter is two
+// passes over the concatenated entry list: a tag pass does
+// atomicMax(tag[slot], epoch<<32 | k+1) and an apply pass lets only the entry
+// whose tag survived write the key.  The epoch (one per update call) makes the
+// tags of earlier calls smaller, so the tag array never needs clearing.
+#include "common.cuh"
+
+namespace gear {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__global__ void __launch_bounds__(kThreads)
+    quantize_kernel(const uint64_t* __restrict__ idx, const void* __restrict__ prio,
+                    int prio_is_f64, const uint32_t* __restrict__ gen, uint32_t n,
+                    uint64_t n_global, uint32_t frac_bits, uint64_t q_max, UpdRec* out,
+                    uint32_t* err) {
+  const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
+  if (k >= n) return;
+  UpdRec r;
+  r.idx = idx[k];
+  r.q = 0;
+  r.gen = gen ? gen[k] : 0u;
+  r.flags = gen ? 2u : 0u;
+  const double p = prio_is_f64 ? static_cast<const double*>(prio)[k]
+                               : (double)static_cast<const float*>(prio)[k];
+  if (r.idx == kIdxNone) {
+    // padding entry: ignored
+  } else if (r.idx >= n_global) {
+    atomicOr(err, kErrIndexRange);
+  } else if (!quantize(p, frac_bits, q_max, &r.q)) {
+    atomicOr(err, kErrBadPriority);
+  } else {
+    r.flags |= 1u;
+  }
+  out[k] = r;
+}
+
+// Entry k is applied by the rank owning its id, if the slot has been inserted
+// (gen != 0) and the optional generation matches.
+__device__ __forceinline__ bool owned_and_fresh(const UpdRec& r, uint64_t local_begin,
+                                                uint64_t local_rows, const uint32_t* gen,
+                                                uint64_t* local, bool* stale) {
+  *stale = false;
+  if (!(r.flags & 1u)) return false;
+  if (r.idx < local_begin || r.idx >= local_begin + local_rows) return false;
+  *local = r.idx - local_begin;
+  const uint32_t gcur = gen[*local];
+  if (gcur == 0 || ((r.flags & 2u) && r.gen != gcur)) {
+    *stale = true;
+    return false;
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    tag_kernel(const UpdRec* __restrict__ recs, uint32_t m, uint64_t local_begin,
+               uint64_t local_rows, const uint32_t* __restrict__ gen, unsigned long long* tag,
+               uint32_t epoch, unsigned long long* n_stale, uint32_t* err) {
+  const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
+  if (k >= m) return;
+  const UpdRec r = recs[k];
+  uint64_t local;
+  bool stale;
+  if (owned_and_fresh(r, local_begin, local_rows, gen, &local, &stale)) {
+    atomicMax(tag + local, ((unsigned long long)epoch << 32) | (unsigned long long)(k + 1));
+  } else if (stale) {
+    atomicAdd(n_stale, 1ull);
+    atomicOr(err, kErrStale);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    apply_kernel(const UpdRec* __restrict__ recs, uint32_t m, uint64_t local_begin,
+                 uint64_t local_rows, const uint32_t* __restrict__ gen,
+                 const unsigned long long* __restrict__ tag, uint32_t epoch, uint64_t* key) {
+  const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
+  if (k >= m) return;
+  const UpdRec r = recs[k];
+  uint64_t local;
+  bool stale;
+  if (owned_and_fresh(r, local_begin, local_rows, gen, &local, &stale) &&
+      tag[local] == (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1)))
+    key[local] = r.q;
+}
+
+}  // namespace
+
+cudaError_t launch_update_quantize(const uint64_t* idx, const void* prio, int prio_is_f64,
+                                   const uint32_t* gen, uint32_t n, uint64_t n_global,
+                                   uint32_t frac_bits, uint64_t q_max, UpdRec* out,
+                                   uint32_t* err, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  quantize_kernel<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(
+      idx, prio, prio_is_f64, gen, n, n_global, frac_bits, q_max, out, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_begin,
+                              uint64_t local_rows, const uint32_t* gen, unsigned long long* tag,
+                              uint32_t epoch, unsigned long long* n_stale, uint32_t* err,
+                              cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  tag_kernel<<<(m + kThreads - 1) / kThreads, kThreads, 0, s>>>(
+      recs, m, local_begin, local_rows, gen, tag, epoch, n_stale, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update_apply(const UpdRec* recs, uint32_t m, uint64_t local_begin,
+                                uint64_t local_rows, const uint32_t* gen,
+                                const unsigned long long* tag, uint32_t epoch, uint64_t* key,
+                                cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  apply_kernel<<<(m + kThreads - 1) / kThreads, kThreads, 0, s>>>(recs, m, local_begin,
+                                                                  local_rows, gen, tag, epoch, key);
+  return cudaGetLastError();
+}
+
+}  // namespace gear

@@ -1,0 +1,157 @@
+// runtime.h -- host-side state of a gear_table / gear_comm (C++17).
+#pragma once
+
+#include <nccl.h>
+
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/gear.h"
+#include "gear_internal.h"
+
+struct gear_comm {
+  ncclComm_t nccl = nullptr;
+  int nranks = 1;
+  int rank = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;  // for create-time exchanges
+};
+
+namespace gear {
+
+// Thread-local error string + status helpers.
+gear_status set_error(gear_status code, const char* fmt, ...);
+void clear_error();
+
+#define GEAR_CUDA(x)                                                                    \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      return ::gear::set_error(GEAR_ERR_CUDA, "%s failed: %s (%s:%d)", #x,              \
+                               cudaGetErrorString(e_), __FILE__, __LINE__);             \
+  } while (0)
+
+#define GEAR_NCCL(x)                                                                    \
+  do {                                                                                  \
+    ncclResult_t r_ = (x);                                                              \
+    if (r_ != ncclSuccess)                                                              \
+      return ::gear::set_error(GEAR_ERR_NCCL, "%s failed: %s (%s:%d)", #x,              \
+                               ncclGetErrorString(r_), __FILE__, __LINE__);             \
+  } while (0)
+
+#define GEAR_TRY(x)                      \
+  do {                                   \
+    gear_status s_ = (x);                \
+    if (s_ != GEAR_OK) return s_;        \
+  } while (0)
+
+enum class MemKind { Device, HostPinned, HostPageable };
+MemKind mem_kind(const void* p);
+
+// Comm helpers (comm.cpp).  With comm == nullptr they are copies / no-ops.
+gear_status allgather_bytes(gear_comm* c, const void* send, void* recv, size_t bytes,
+                            cudaStream_t s);
+gear_status barrier(gear_comm* c);
+
+struct ColumnState {
+  std::string name;
+  gear_dtype dtype = GEAR_U8;
+  gear_placement placement = GEAR_DEVICE;
+  uint64_t rb = 0;                      // row bytes
+  uint64_t bytes_local = 0;             // R * C_s * rb
+  uint8_t* local = nullptr;             // this rank's rows (device ptr or host ptr)
+  const uint8_t* view[kMaxRanks] = {};  // device-accessible base of each rank's rows
+  std::vector<void*> ipc_opened;        // peer device mappings to close
+  std::vector<std::pair<void*, size_t>> host_maps;  // host mappings (own + peers) to unmap
+  std::string shm_name;                 // own shm object (W > 1 HOST columns)
+};
+
+struct ShardRing {
+  uint64_t next_free = 0;  // free queue seeded 0..C_s-1 ascending (cursor)
+  uint32_t head = 0;       // ring start: oldest committed slot
+  uint32_t len = 0;        // committed slots in the ring
+  uint64_t seq_ctr = 1;    // next seq value
+  std::vector<uint32_t> ord;  // host mirror of the ring (slot ids)
+};
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+};
+
+}  // namespace gear
+
+struct gear_table {
+  gear_comm* comm = nullptr;
+  int device = 0;
+  uint32_t W = 1, rank = 0, R = 1, S = 1;
+  uint64_t Cs = 0, Clocal = 0, N = 0;
+  uint32_t F = 32;
+  uint64_t qmax = 0;
+  gear_removal removal = GEAR_REMOVE_FIFO;
+  uint32_t max_batch = 4096;
+  std::vector<gear::ColumnState> cols;
+
+  // slot state (rank-local, R*C_s entries)
+  uint64_t* key = nullptr;
+  uint64_t* seq = nullptr;
+  uint32_t* gen = nullptr;
+  unsigned long long* tag = nullptr;
+  uint32_t* ord = nullptr;
+
+  // CDF double buffer + scan bookkeeping
+  uint64_t* cdf[2] = {nullptr, nullptr};
+  uint64_t* scan_status[2] = {nullptr, nullptr};
+  uint32_t* scan_ticket[2] = {nullptr, nullptr};
+  uint64_t scan_launches = 0;
+  int cdf_parity = 1;     // parity of the last built buffer (first build -> 0)
+  int cdf_mode = -1;      // -1 none, 0 weighted keys, 1 indicator
+  bool dirty = true;
+  gear::ShardTotals* cdf_totals_local = nullptr;  // [R]
+  gear::ShardTotals* cdf_totals_all = nullptr;    // [S]
+  gear::ShardTotals* fifo_totals_local = nullptr; // [R]
+  gear::ShardTotals* fifo_totals_all = nullptr;   // [S]
+  const uint64_t** d_cdf_ptrs = nullptr;          // [2*S]
+  const uint32_t** d_gen_ptrs = nullptr;          // [W]
+  std::vector<void*> ipc_opened;                  // peer cdf/gen mappings
+
+  // sample scratch
+  uint64_t* q_scratch = nullptr;
+  unsigned long long* qmin_slot = nullptr;
+  uint32_t* done_ctr = nullptr;
+  uint64_t* tmp_idx = nullptr;
+  float* tmp_w = nullptr;
+  double* tmp_p = nullptr;
+  uint32_t* tmp_gen = nullptr;
+  gear::Cand* cand_local = nullptr;  // [R * W*max_batch]
+  gear::Cand* cand_all = nullptr;    // [S * W*max_batch]
+
+  // update scratch
+  gear::UpdRec* upd_local = nullptr;  // [max_batch]
+  gear::UpdRec* upd_all = nullptr;    // [W*max_batch]
+  uint64_t* upd_idx = nullptr;
+  double* upd_prio = nullptr;
+  uint32_t* upd_gen = nullptr;
+  uint32_t epoch = 0;
+  unsigned long long* n_stale = nullptr;
+  uint32_t* err = nullptr;
+
+  // collect scratch (host-resident id lists)
+  gear::DevBuf<uint64_t> col_idx;
+
+  // insert staging
+  std::vector<gear::ShardRing> rings;
+  gear::InsMeta* h_meta = nullptr;  // pinned
+  gear::OrdRec* h_ord = nullptr;    // pinned
+  uint64_t* h_out = nullptr;        // pinned
+  gear::InsMeta* d_meta = nullptr;
+  gear::OrdRec* d_ord = nullptr;
+  uint64_t* d_out = nullptr;
+  uint8_t* d_rows = nullptr;        // staging for pageable row sources
+  size_t d_rows_bytes = 0;
+  cudaEvent_t staging_ev = nullptr;
+  uint32_t chunk_bytes = 8192;      // collect warp-task size
+};

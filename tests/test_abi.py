@@ -1,0 +1,74 @@
+"""CPU checks of the boundary: libgear.so builds, loads and exports every
+entry point include/gear.h declares, with the binding's names; the oracle and
+the product share no code.  No compute calls (no GPU here)."""
+import ctypes
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "gear.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return set(re.findall(r"^\s*(?:gear_status|const char\*)\s+(gear_\w+)\s*\(", src, flags=re.M))
+
+
+def test_header_declares_hot_path_calls():
+    names = _declared()
+    for n in ("gear_table_create", "gear_insert", "gear_update_priorities", "gear_sample",
+              "gear_collect", "gear_table_destroy", "gear_comm_create", "gear_get_unique_id"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2310_05205_b200 as gear
+    from paper_2310_05205_b200 import build
+    build.build()
+    lib = ctypes.CDLL(gear.LIB_PATH)
+    names = _declared()
+    for n in names:
+        assert hasattr(lib, n), f"libgear.so does not export {n}"
+    # the binding wraps every declared entry point under the same name
+    assert names == set(gear.SIGNATURES)
+    for n in names - {"gear_last_error", "gear_version"}:
+        assert callable(getattr(gear, n)), n
+    assert gear.load().gear_version().startswith(b"gear-b200")
+    assert gear.load().gear_last_error() == b""
+
+
+def test_kernels_are_sm100a():
+    """The fat binary carries sm_100a SASS (cuobjdump lists the arch)."""
+    import subprocess
+    import paper_2310_05205_b200 as gear
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", gear.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def _imports_and_includes(path):
+    out = []
+    for line in open(path):
+        m = re.match(r"\s*#\s*include\s*[<\"]([^>\"]+)[>\"]", line)
+        if m:
+            out.append(m.group(1))
+        m = re.match(r"\s*(?:from|import)\s+([\w.]+)", line)
+        if m and path.endswith(".py"):
+            out.append(m.group(1))
+    return out
+
+
+def test_oracle_and_product_share_no_code():
+    """Neither side includes, imports or links the other."""
+    prod = os.path.join(ROOT, "paper_2310_05205_b200")
+    for dp, _, fs in os.walk(prod):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                for dep in _imports_and_includes(os.path.join(dp, f)):
+                    assert "oracle" not in dep, (f, dep)
+    odir = os.path.join(ROOT, "oracle")
+    for f in os.listdir(odir):
+        if f.endswith((".c", ".h", ".py")):
+            for dep in _imports_and_includes(os.path.join(odir, f)):
+                assert "paper_2310_05205_b200" not in dep and "gear.h" != dep \
+                    and "synth" not in dep, (f, dep)

@@ -1,0 +1,235 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the
+same seeded inputs.  Indices, keys, seq/gen and collected bytes bit-exact;
+IS weights within 1e-6 relative (north star); q/T probabilities bit-exact
+(correctly rounded division on both sides)."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2310_05205_b200 as gear
+    gear.load()
+    return torch
+
+
+def _pair(**kw):
+    from gpu_harness import Pair
+    return Pair(**kw)
+
+
+C1 = synth.CONFIGS["c1"]
+G = __import__("paper_2310_05205_b200")
+
+
+@pytest.mark.parametrize("R", [1, 2, 4, 8])
+@pytest.mark.parametrize("placement", ["device", "host"])
+def test_c1_sample_collect_update(torch_cuda, R, placement):
+    """c1 shapes: insert every row, then steps of UNIFORM / WEIGHTED /
+    PRIORITIZED sampling, collection of the sampled rows and priority
+    updates of them (with duplicates), for 1/2/4/8 shards (virtual world:
+    the result must not depend on the shard count)."""
+    P = _pair(capacity=C1.capacity, seq_len=C1.seq_len, colspecs=C1.cols, R=R, placement=placement)
+    P.fill(synth.priorities(C1.capacity, seed=1, zero_frac=0.10))
+    P.check_state()
+    rng = np.random.default_rng(7)
+    for step in range(6):
+        for strat in (G.GEAR_UNIFORM, G.GEAR_WEIGHTED, G.GEAR_PRIORITIZED):
+            idx = P.check_sample(strat, 64, synth.SAMPLE_SEED_BASE + 10 * step + strat, beta=0.4)
+            P.check_collect(idx)
+        newp = rng.lognormal(0, 1, size=64)
+        newp[rng.random(64) < 0.05] = 0.0
+        ost, _, err, _ = P.update(idx, newp)
+        assert ost == 0 and err == 0
+        P.check_state()
+    P.close()
+
+
+def test_scan_multi_tile_ragged(torch_cuda):
+    """Shards spanning several 4096-key scan tiles with an odd shard capacity
+    (misaligned shard starts, ragged last tile) and a long look-back."""
+    cols = [synth.ColSpec("x", "u8", (3,))]
+    N = 5 * 20011
+    P = _pair(capacity=N, seq_len=1, colspecs=cols, R=5, mirror=True)
+    P.fill(synth.priorities(N, seed=3, zero_frac=0.2, sigma=2.0))
+    for s in range(4):
+        for strat in (G.GEAR_UNIFORM, G.GEAR_PRIORITIZED):
+            idx = P.check_sample(strat, 1000, 99 + s, beta=0.6)
+    P.check_collect(idx)
+    P.close()
+
+
+def test_single_shard_many_tiles(torch_cuda):
+    cols = [synth.ColSpec("x", "i32", (5,))]
+    N = 4096 * 37 + 1
+    P = _pair(capacity=N, seq_len=2, colspecs=cols, R=1)
+    P.fill(synth.priorities(N, seed=4, zero_frac=0.01))
+    for s in range(3):
+        P.check_sample(G.GEAR_WEIGHTED, 2048, 1234 + s)
+    P.close()
+
+
+def test_zero_weight_and_empty(torch_cuda):
+    cols = [synth.ColSpec("x", "f32", ())]
+    P = _pair(capacity=3, seq_len=1, colspecs=cols, R=1)
+    P.insert(0, [0.0, 5.0, 0.0])
+    for strat in (G.GEAR_UNIFORM, G.GEAR_WEIGHTED, G.GEAR_PRIORITIZED):
+        idx = P.check_sample(strat, 100, 5)
+        assert np.all(idx == 1)
+    P.update([1], [0.0])
+    for strat in (G.GEAR_UNIFORM, G.GEAR_WEIGHTED, G.GEAR_PRIORITIZED, G.GEAR_FIFO, G.GEAR_LIFO):
+        assert P.check_sample(strat, 4, 6) is None    # EMPTY latched, ids = IDX_NONE
+    P.close()
+
+
+def test_update_errors_duplicates_and_generations(torch_cuda):
+    cols = [synth.ColSpec("x", "u8", (8,))]
+    P = _pair(capacity=256, seq_len=1, colspecs=cols, R=2)
+    P.insert(0, np.ones(100))
+    P.insert(1, np.ones(128))
+    rng = np.random.default_rng(11)
+    idx = rng.integers(0, 256, size=600).astype(np.uint64)   # includes never-inserted slots
+    p = rng.lognormal(0, 2, size=600)
+    p[5], p[6], p[7] = np.nan, -1.0, np.inf
+    idx[8] = 256                                            # out of range
+    idx[9] = np.uint64(G.GEAR_IDX_NONE)                     # padding entry
+    ost, ons, err, ns = P.update(idx, p)
+    assert bool(ost & 1) == bool(err & G.GEAR_DEVERR_BAD_PRIORITY)
+    assert bool(ost & 2) == bool(err & G.GEAR_DEVERR_INDEX_RANGE)
+    assert bool(ost & 4) == bool(err & G.GEAR_DEVERR_STALE)
+    assert ns == ons and ns > 0
+    P.check_state()
+    # generation-checked update: half the entries carry a stale generation
+    key, seq, gen = P.t.read_state()
+    ids = np.arange(0, 100, dtype=np.uint64)
+    g = gen[:100].copy()
+    g[::2] += 1
+    ost, ons, err, ns = P.update(ids, np.full(100, 3.25), gen=g)
+    assert ns == ons == 50
+    P.check_state()
+    # f32 priorities widen exactly
+    ost, ons, err, ns = P.update(ids, rng.lognormal(0, 1, 100).astype(np.float32), f32=True)
+    P.check_state()
+    P.close()
+
+
+def test_quantize_edges_on_gpu(torch_cuda):
+    """Q_F special cases (ties to even, clamps, saturation) against the oracle."""
+    cols = [synth.ColSpec("x", "u8", ())]
+    P = _pair(capacity=1024, seq_len=1, colspecs=cols, R=1)
+    P.insert(0, np.ones(1024))
+    vals = [0.0, 2.0 ** -40, 1.0, 1.5, 2.0 ** 30, 1e300, 2.0 ** 20]
+    vals += [(k + 0.5) * 2.0 ** -32 for k in range(0, 40)]
+    vals += [(6.5 + 2.0 ** -20) * 2.0 ** -32, (7.5 - 2.0 ** -20) * 2.0 ** -32, 5e-324]
+    P.update(np.arange(len(vals), dtype=np.uint64), np.array(vals))
+    P.check_state()
+    P.close()
+
+
+@pytest.mark.parametrize("removal", [0, 1])
+@pytest.mark.parametrize("R", [1, 3])
+def test_fifo_lifo_with_ring_wrap(torch_cuda, removal, R):
+    """c4-style: each shard receives 1.25 x C_s inserts so the ring wraps;
+    some trajectories are made unselectable; FIFO/LIFO selection must equal
+    the oracle's global (seq, shard) order."""
+    cols = [synth.ColSpec("obs", "f32", (4,)), synth.ColSpec("done", "u8", (3,))]
+    Cs = 600
+    P = _pair(capacity=Cs * R, seq_len=4, colspecs=cols, R=R, removal=removal)
+    rng = np.random.default_rng(21)
+    total = int(Cs * 1.25)
+    for s in range(R):
+        k = 0
+        while k < total:
+            b = int(rng.integers(1, 300))
+            P.insert(s, np.ones(min(b, total - k)))
+            k += b
+    P.check_state()
+    zero = rng.choice(Cs * R, size=Cs * R // 5, replace=False).astype(np.uint64)
+    P.update(zero, np.zeros(zero.size))
+    for B in (1, 7, 64, 200):
+        for strat in (G.GEAR_FIFO, G.GEAR_LIFO):
+            idx = P.check_sample(strat, B, 0)
+            if idx is not None:
+                P.check_collect(idx)
+    P.check_sample(G.GEAR_FIFO, 4096, 0)  # more than selectable -> EMPTY
+    P.close()
+
+
+def test_insert_bad_priority_and_device_sources(torch_cuda):
+    cols = [synth.ColSpec("a", "u8", (7,)), synth.ColSpec("b", "i32", (3,))]
+    P = _pair(capacity=64, seq_len=3, colspecs=cols, R=2)
+    with pytest.raises(G.GearError) as e:
+        P.t.insert(0, [np.zeros((2, P.rb[0]), np.uint8), np.zeros((2, P.rb[1]), np.uint8)],
+                   np.array([1.0, np.nan]))
+    assert e.value.status == G.GEAR_ERR_BAD_PRIORITY
+    P.insert(0, np.linspace(0, 3, 32), device_src=True)
+    P.insert(1, np.linspace(1, 2, 40), device_src=True)    # wraps shard 1 (C_s = 32)
+    P.check_state()
+    P.check_collect(np.arange(64, dtype=np.uint64))
+    P.close()
+
+
+def test_collect_index_range_latched(torch_cuda):
+    cols = [synth.ColSpec("a", "u8", (16,))]
+    P = _pair(capacity=32, seq_len=1, colspecs=cols)
+    P.insert(0, np.ones(32))
+    P.collect_gpu(np.array([1, 40, 3], np.uint64))
+    err, _ = P.t.sync()
+    assert err & G.GEAR_DEVERR_INDEX_RANGE
+    P.close()
+
+
+def test_figure4_collect_two_shards(torch_cuda):
+    """collect([2, 4, 25, 26], [col0, col1]) over two shards of
+    capacity 24 returns the rows in request order."""
+    cols = [synth.ColSpec("col0", "f32", (3,)), synth.ColSpec("col1", "i32", ())]
+    P = _pair(capacity=48, seq_len=2, colspecs=cols, R=2)
+    P.insert(0, np.ones(24))
+    P.insert(1, np.ones(24))
+    P.check_collect(np.array([2, 4, 25, 26], np.uint64))
+    P.close()
+
+
+def test_host_buffers_through_abi(torch_cuda):
+    """The C-ABI accepts host ids / priorities / sample outputs (pinned or
+    pageable) and must give the same results as device buffers."""
+    import torch
+    P = _pair(capacity=C1.capacity, seq_len=C1.seq_len, colspecs=C1.cols, R=1)
+    P.fill(synth.priorities(C1.capacity, seed=2, zero_frac=0.1))
+    B = 64
+    for pinned in (False, True):
+        idx = torch.empty(B, dtype=torch.int64, pin_memory=pinned)
+        w = torch.empty(B, dtype=torch.float32, pin_memory=pinned)
+        P.t.sample(G.GEAR_PRIORITIZED, B, 77, 0.5, idx, w)
+        torch.cuda.synchronize()
+        st, oi, ow, op = P.sample_oracle(G.GEAR_PRIORITIZED, B, 77, 0.5)
+        assert np.array_equal(idx.numpy().view(np.uint64), oi)
+        np.testing.assert_allclose(w.numpy(), ow, rtol=1e-6)
+        hp = torch.from_numpy(np.linspace(0.5, 2, B))
+        hp = hp.pin_memory() if pinned else hp
+        G.gear_update_priorities(P.t.handle, B, idx, hp, G.GEAR_F64)
+        torch.cuda.synchronize()
+        P.o.update(oi, np.linspace(0.5, 2, B))
+        P.check_state()
+    P.close()
+
+
+def test_deterministic_across_repeats_and_beta(torch_cuda):
+    P = _pair(capacity=C1.capacity, seq_len=C1.seq_len, colspecs=C1.cols, R=4)
+    P.fill(synth.priorities(C1.capacity, seed=5))
+    a = P.sample_gpu(G.GEAR_PRIORITIZED, 512, 3, 0.0)
+    b = P.sample_gpu(G.GEAR_PRIORITIZED, 512, 3, 1.0)
+    assert np.array_equal(a[0], b[0])
+    assert np.all(a[1] == 1.0)
+    key = P.o.key[a[0].astype(np.int64)]
+    qmin = key.min()
+    assert np.array_equal(b[1], np.array([np.float32(int(qmin) / int(k)) for k in key]))
+    P.check_sample(G.GEAR_PRIORITIZED, 512, 3, 1.0)
+    P.close()
