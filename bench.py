@@ -1,0 +1,401 @@
+"""bench.py -- sampled+collected trajectories/s of the GEAR replay hot path.
+
+One step = the whole hot path on every rank: gear_sample (K1 scan of the
+dirty CDF + K2 draw/search + IS weights) -> gear_collect (K5, every column of
+the sampled rows into a contiguous batch) -> gear_update_priorities (K6, new
+priorities for the sampled ids), for the configuration's strategy.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+
+Default workload at N=1: BASELINE.json configs[1] (c2, Decision-Transformer
+Atari table: 100K trajectories x 847,080 B, HBM-resident, prioritized B=512
+per rank with per-step priority updates).  N>1 (torchrun, one rank per GPU):
+the same 100K-trajectory table sharded by id over N GPUs, B=512 per rank
+(weak scaling), remote rows read over NVLink by the collect kernel.
+
+Prints ONE JSON line (rank 0).  Time is measured with CUDA events on the
+launching stream, barrier + synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sampled+collected trajectories/sec and collect GB/s vs HBM/PCIe roofline, 1/2/4/8 B200"
+UNIT = "trajectories/s"
+PCIE_H2D_GBS = 55.62     # profiles/r01_probe_2gpu.jsonl: pinned cudaMemcpy H2D, 1 GiB, best of 5
+NVLINK_PEER_GBS = 775.27  # profiles/r01_probe_2gpu.jsonl: cudaMemcpyPeer pull, 1 GiB
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, read+write bytes)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s of B200_PROFILING.md (MEASURED_PEAKS.json absent)"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- workload
+def scaled_capacity(cfg, n_ranks: int) -> tuple[int, str]:
+    """Host-resident tables are scaled to fit 60% of this box's RAM."""
+    import synth
+    host_rb = sum(synth.row_bytes(cfg, c) for c in cfg.cols if c.placement == "host")
+    N = cfg.capacity
+    note = ""
+    if host_rb:
+        mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+        fit = int(0.6 * mem) // host_rb
+        if fit < N:
+            N = max(n_ranks * 1024, (fit // (n_ranks * 1024)) * n_ranks * 1024)
+            note = f"capacity scaled {cfg.capacity} -> {N} to fit 60% of {mem >> 30} GiB host RAM"
+    N -= N % n_ranks
+    return N, note
+
+
+def build_table(cfg, comm, n_ranks: int, rank: int, capacity: int, stream):
+    """Create the config's table and fill this rank's shard through gear_insert
+    (rows generated on the GPU by synth.fill_rows, priorities from synth)."""
+    import torch
+    import synth
+    import paper_2310_05205_b200 as gear
+    dt = {"u8": gear.GEAR_U8, "i32": gear.GEAR_I32, "f32": gear.GEAR_F32}
+    cols = [gear.Column(c.name, dt[c.dtype], tuple(c.shape),
+                        gear.GEAR_HOST if c.placement == "host" else gear.GEAR_DEVICE) for c in cfg.cols]
+    B = cfg.batch
+    t = gear.Table(capacity, cfg.seq_len, cols, comm, max_batch=max(4096, B))
+    Cs = capacity // n_ranks
+    if cfg.prio == "tasks":
+        prio_all = synth.task_weights(capacity, zero_frac=cfg.zero_frac)
+    else:
+        prio_all = synth.priorities(capacity, seed=synth.PRIO_SEED, zero_frac=cfg.zero_frac)
+    prio = prio_all[rank * Cs:(rank + 1) * Cs]
+    rows_per = max(1, min(4096, (512 << 20) // max(1, sum(t.row_bytes))))
+    stage = [torch.empty((rows_per, rb), dtype=torch.uint8, device="cuda") for rb in t.row_bytes]
+    for k0 in range(0, Cs, rows_per):
+        m = min(rows_per, Cs - k0)
+        for c, rb in enumerate(t.row_bytes):
+            synth.fill_rows(stage[c].data_ptr(), m, rb, c, rank * Cs + k0, stream=stream.cuda_stream)
+        gear.gear_insert(t.handle, rank, m, stage, prio[k0:k0 + m], None, stream)
+    stream.synchronize()
+    del stage
+    return t, prio_all
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    import synth
+    import paper_2310_05205_b200 as gear
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    gear.load()
+    comm = gear.comm_from_torch_distributed(local) if world > 1 else None
+    cfg = synth.CONFIGS[args.config]
+    capacity, cap_note = scaled_capacity(cfg, world)
+    stream = torch.cuda.Stream()
+    t, prio_all = build_table(cfg, comm, world, rank, capacity, stream)
+    strategy = gear.STRATEGIES[cfg.strategy]
+    B = cfg.batch
+    ncols = len(t.row_bytes)
+    col_ids = list(range(ncols))
+    row_total = sum(t.row_bytes)
+    payload = B * row_total
+    host_bytes = B * sum(rb for rb, c in zip(t.row_bytes, cfg.cols) if c.placement == "host")
+    dev_bytes = payload - host_bytes
+
+    with torch.cuda.stream(stream):
+        idx = torch.empty(B, dtype=torch.int64, device="cuda")
+        w = torch.empty(B, dtype=torch.float32, device="cuda")
+        outs = [torch.empty((B, rb), dtype=torch.uint8, device="cuda") for rb in t.row_bytes]
+        pool = [torch.from_numpy(synth.priorities(B, seed=1000 + k)).cuda() for k in range(16)]
+        h_idx = torch.empty(B, dtype=torch.int64, pin_memory=True)
+        h_w = torch.empty(B, dtype=torch.float32, pin_memory=True)
+        h_prio = [torch.from_numpy(synth.priorities(B, seed=1000 + k)).pin_memory() for k in range(16)]
+    ev_c0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_c1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+
+    def step(i, timed):
+        seed = synth.SAMPLE_SEED_BASE + i
+        gear.gear_sample(t.handle, strategy, B, seed, cfg.beta, idx, w, None, None, stream)
+        if timed:
+            ev_c0[i].record(stream)
+        gear.gear_collect(t.handle, B, idx, col_ids, outs, stream)
+        if timed:
+            ev_c1[i].record(stream)
+        if cfg.update:
+            gear.gear_update_priorities(t.handle, B, idx, pool[i % 16], gear.GEAR_F64, None, stream)
+
+    def barrier():
+        stream.synchronize()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    for i in range(args.warmup):
+        step(i, False)
+    barrier()
+    err, _ = t.sync()
+    assert err == 0, f"device error bits {err} during warm-up"
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = gear.gear_kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(i, True)
+    e1.record(stream)
+    barrier()
+    launches = gear.gear_kernel_launches() - l0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    coll_ms = [a.elapsed_time(b) for a, b in zip(ev_c0, ev_c1)]
+    err, _ = t.sync()
+    assert err == 0, f"device error bits {err} in the timed region"
+
+    # end-to-end through the C-ABI with HOST buffers: the step's priority update
+    # (ids + f64 priorities) comes from pinned host memory, and the sampled ids
+    # and weights go back to pinned host memory, read by the host every step.
+    barrier()
+    h_idx.copy_(idx.cpu())
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for i in range(args.steps):
+        if cfg.update:
+            gear.gear_update_priorities(t.handle, B, h_idx, h_prio[i % 16], gear.GEAR_F64, None, stream)
+        gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + 7919 + i, cfg.beta, idx, w,
+                         None, None, stream)
+        gear.gear_collect(t.handle, B, idx, col_ids, outs, stream)
+        with torch.cuda.stream(stream):
+            h_idx.copy_(idx, non_blocking=True)
+            h_w.copy_(w, non_blocking=True)
+        stream.synchronize()     # the host consumes the ids before the next step
+    e3.record(stream)
+    barrier()
+    e2e_ms = e2.elapsed_time(e3)
+
+    times = torch.tensor([ms, e2e_ms, float(np.mean(coll_ms))], device="cuda")
+    if world > 1:
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    ms, e2e_ms, coll_avg = (float(x) for x in times.cpu())
+
+    traj = world * B * args.steps
+    value = traj / (ms / 1e3)
+    hbm_peak, hbm_src = _peaks()
+    # Algorithmic bytes of one collect launch: every
+    # payload byte is read once from its source and written once to HBM.
+    if world == 1 and host_bytes == 0:
+        alg = 2 * payload
+        roof = {"bound": "hbm", "achieved": alg / (coll_avg / 1e3) / 1e9, "peak": hbm_peak,
+                "unit": "GB/s", "peak_source": hbm_src}
+    elif host_bytes and dev_bytes == 0:
+        roof = {"bound": "pcie", "achieved": payload / (coll_avg / 1e3) / 1e9, "peak": PCIE_H2D_GBS,
+                "unit": "GB/s", "peak_source": "probe: pinned H2D cudaMemcpy (profiles/r01_probe_2gpu.jsonl)"}
+    else:
+        # remote fraction (W-1)/W of the payload crosses NVLink into this GPU
+        remote = dev_bytes * (world - 1) / world
+        t_nvl = remote / (NVLINK_PEER_GBS * 1e9)
+        t_hbm = 2 * dev_bytes / (hbm_peak * 1e9)
+        t_pcie = host_bytes / (PCIE_H2D_GBS * 1e9)
+        bound = max((t_nvl, "nvlink"), (t_hbm, "hbm"), (t_pcie, "pcie"))
+        roof = {"bound": bound[1], "achieved": None, "peak": None, "unit": "GB/s",
+                "ideal_ms": bound[0] * 1e3}
+        roof["frac"] = bound[0] * 1e3 / coll_avg
+    if roof.get("achieved") is not None:
+        roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["kernel"] = "collect_kernel"
+    roof["avg_launch_ms"] = coll_avg
+    roof["algorithmic_bytes_per_launch"] = 2 * payload if roof["bound"] == "hbm" else payload
+    roof["traffic"] = args.traffic
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded splitmix64 row bytes, lognormal priorities)",
+        "config": {"workload": cfg.name, "capacity": capacity, "seq_len": cfg.seq_len,
+                   "row_bytes": row_total, "strategy": cfg.strategy, "batch_per_rank": B,
+                   "global_batch": world * B, "update_per_step": cfg.update,
+                   "table_bytes": capacity * row_total,
+                   "l2": "inputs larger than L2: random rows of a %.1f GB table, %.0f MB batch per rank"
+                         % (capacity * row_total / 1e9, payload / 1e6),
+                   "parallelism": f"dp{world} (table sharded by trajectory id, 1 shard per GPU)",
+                   **({"note": cap_note} if cap_note else {})},
+        "collect_gbps": payload / (coll_avg / 1e3) / 1e9,
+        "roofline": roof,
+        "e2e": {"value": traj / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": (16 * B if cfg.update else 0),
+                "d2h_bytes_per_step": 12 * B},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, capacity, prio_all, budget_s=args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    t.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- CPU oracle
+def cpu_baseline(cfg, capacity, prio_all, budget_s=15.0, max_steps=1000):
+    """The oracle (oracle/, single thread) timed as it stands on this host: the
+    same step (sample + collect of every column + update) on the same keys;
+    row bytes come from a host mirror of M rows (row g read from g mod M) so
+    the copy pattern is the same without a 2nd copy of the table."""
+    import oracle
+    import synth
+    oracle.build()
+    B = cfg.batch
+    row_total = sum(synth.row_bytes(cfg, c) for c in cfg.cols)
+    rbs = [synth.row_bytes(cfg, c) for c in cfg.cols]
+    M = max(1, min(capacity, (2 << 30) // row_total))    # <= 2 GiB mirror (>> LLC)
+    mirror = [np.zeros((M, rb), np.uint8) for rb in rbs]
+    for c, rb in enumerate(rbs):
+        for k0 in range(0, M, 256):
+            mirror[c][k0:k0 + 256] = synth.row_bytes_of(c, np.arange(k0, min(M, k0 + 256)), rb)
+    o = oracle.Table(capacity, 1)
+    for k0 in range(0, capacity, 1 << 20):
+        o.insert(0, prio_all[k0:k0 + (1 << 20)])
+    strat = {"prioritized": oracle.PRIORITIZED, "weighted": oracle.WEIGHTED, "uniform": oracle.UNIFORM,
+             "fifo": oracle.FIFO, "lifo": oracle.LIFO}[cfg.strategy]
+    steps = 0
+    t0 = time.perf_counter()
+    while True:
+        st, idx, w, p = o.sample(strat, 1, 0, B, synth.SAMPLE_SEED_BASE + steps, cfg.beta)
+        src = (idx % np.uint64(M)).astype(np.uint64)
+        for c in range(len(rbs)):
+            oracle.collect(mirror[c], src)
+        if cfg.update:
+            o.update(idx, synth.priorities(B, seed=1000 + steps % 16))
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or steps >= max_steps:
+            break
+    return {"value": steps * B / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{steps} steps of {cfg.name} (B={B}, N={capacity} keys; rows from a "
+                      f"{M}-row host mirror, row g <- g mod {M}), {el:.1f} s, single thread",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} cores)"
+    except Exception:
+        pass
+    return f"{os.cpu_count()} cores"
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, on rank 0's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    capacity, note = scaled_capacity(cfg, world)
+    if cfg.prio == "tasks":
+        prio_all = synth.task_weights(capacity, zero_frac=cfg.zero_frac)
+    else:
+        prio_all = synth.priorities(capacity, seed=synth.PRIO_SEED, zero_frac=cfg.zero_frac)
+    steps_total = args.steps + args.warmup
+    cb = cpu_baseline(cfg, capacity, prio_all, budget_s=args.cpu_budget, max_steps=max(steps_total, 1))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": cfg.name, "capacity": capacity, "batch_per_rank": cfg.batch,
+                   "strategy": cfg.strategy, **({"note": note} if note else {})},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="gear", choices=["gear", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes per collect launch from an ncu --set full capture")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

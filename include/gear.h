@@ -142,6 +142,10 @@ const char* gear_last_error(void);
 /* Library version string. */
 const char* gear_version(void);
 
+/* Number of kernels this library has launched in the process so far
+ * (diagnostics: bench.py reports the count inside its timed region). */
+uint64_t gear_kernel_launches(void);
+
 /* --- communicator (one per rank; wraps an NCCL communicator) ------------ */
 
 /* Rank 0 creates the 128-byte unique id and the caller broadcasts it to the

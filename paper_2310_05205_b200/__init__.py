@@ -86,6 +86,7 @@ _u32, _u64, _i32, _f64 = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.
 SIGNATURES = {
     "gear_last_error": ([], ctypes.c_char_p),
     "gear_version": ([], ctypes.c_char_p),
+    "gear_kernel_launches": ([], ctypes.c_uint64),
     "gear_get_unique_id": ([_P], _i32),
     "gear_comm_create": ([_i32, _i32, _P, _i32, _P], _i32),
     "gear_comm_destroy": ([_P], _i32),
@@ -148,6 +149,10 @@ def _stream(stream) -> int | None:
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream
+
+
+def gear_kernel_launches() -> int:
+    return int(load().gear_kernel_launches())
 
 
 # ---------------------------------------------------------------- comm

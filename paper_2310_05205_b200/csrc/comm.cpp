@@ -4,6 +4,7 @@
 // totals (16 B per shard), FIFO/LIFO candidates (16 B each) and priority
 // updates (24 B each); the payload itself is read peer-to-peer by the
 // collect kernel, never through NCCL.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -14,7 +15,10 @@ namespace gear {
 
 namespace {
 thread_local char g_err[1024] = "";
+std::atomic<uint64_t> g_launches{0};
 }
+
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 gear_status set_error(gear_status code, const char* fmt, ...) {
   va_list ap;
@@ -73,6 +77,8 @@ extern "C" {
 const char* gear_last_error(void) { return gear::last_error(); }
 
 const char* gear_version(void) { return "gear-b200 0.1 (sm_100a)"; }
+
+uint64_t gear_kernel_launches(void) { return gear::g_launches.load(); }
 
 gear_status gear_get_unique_id(uint8_t out[128]) {
   static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");

@@ -127,6 +127,9 @@ struct SampleParams {
 
 // ---- kernel launchers (kernels/*.cu) --------------------------------------
 
+// Counts every kernel launch of the library (gear_kernel_launches()).
+void count_launch(uint64_t n = 1);
+
 // K1: per-shard inclusive u64 scan with decoupled look-back.  Writes cdf for
 // `n_shards_local` contiguous shards of `shard_cap` keys and their totals.
 // indicator != 0 scans [key > 0] instead of key.

@@ -138,12 +138,16 @@ __global__ void __launch_bounds__(kThreads)
   if (k < n_ord) ord[ord_recs[k].pos] = ord_recs[k].slot;
 }
 
-int grid_for(uint64_t tasks) {
-  int dev = 0, sms = 148;
+// Persistent grid: as many CTAs as can be resident at once (no second wave
+// whose warps would start late on a static task split), capped by the work.
+template <class K>
+int grid_for(K kernel, uint64_t tasks) {
+  int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
   const uint64_t want = (tasks + kWarps - 1) / kWarps;
-  const uint64_t cap = (uint64_t)sms * 8;  // 8 resident CTAs (64 warps) per SM
+  const uint64_t cap = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
   return (int)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
@@ -151,13 +155,15 @@ int grid_for(uint64_t tasks) {
 
 cudaError_t launch_collect(const CollectParams& p, cudaStream_t s) {
   if (p.total_chunks == 0) return cudaSuccess;
-  collect_kernel<<<grid_for(p.total_chunks), kThreads, 0, s>>>(p);
+  count_launch();
+  collect_kernel<<<grid_for(collect_kernel, p.total_chunks), kThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_scatter(const ScatterParams& p, cudaStream_t s) {
   if (p.total_chunks == 0) return cudaSuccess;
-  scatter_kernel<<<grid_for(p.total_chunks), kThreads, 0, s>>>(p);
+  count_launch();
+  scatter_kernel<<<grid_for(scatter_kernel, p.total_chunks), kThreads, 0, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -167,6 +173,7 @@ cudaError_t launch_insert_meta(const InsMeta* meta, uint32_t m, const OrdRec* or
                                cudaStream_t s) {
   const uint32_t n = m > n_ord ? m : n_ord;
   if (n == 0) return cudaSuccess;
+  count_launch();
   insert_meta_kernel<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(
       meta, m, ord_recs, n_ord, frac_bits, q_max, key, seq, gen, ord);
   return cudaGetLastError();

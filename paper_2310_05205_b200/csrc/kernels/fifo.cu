@@ -143,6 +143,7 @@ cudaError_t launch_fifo_local(const uint64_t* key, const uint64_t* seq, const ui
                               const FifoRings& rings, uint64_t shard_cap,
                               uint32_t n_shards_local, uint32_t first_shard, uint32_t K,
                               int lifo, Cand* cand_out, ShardTotals* totals_out, cudaStream_t s) {
+  count_launch();
   fifo_local_kernel<<<n_shards_local, kLocalThreads, 0, s>>>(
       key, seq, ord, rings, shard_cap, first_shard, K, lifo, cand_out, totals_out);
   return cudaGetLastError();
@@ -156,6 +157,7 @@ cudaError_t launch_fifo_merge(const Cand* cand_all, const ShardTotals* totals_al
   const uint64_t n = (uint64_t)n_shards * K;
   const uint64_t threads = n > B ? n : B;
   const uint32_t grid = (uint32_t)((threads + kMergeThreads - 1) / kMergeThreads);
+  count_launch();
   fifo_merge_kernel<<<grid, kMergeThreads, 0, s>>>(cand_all, totals_all, n_shards, K, lifo,
                                                    shard_cap, rank, B, gen_ptrs, shards_per_rank,
                                                    out_idx, out_w, out_p, out_gen, err);

@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s) {
   if (p.B == 0) return cudaSuccess;
   const uint32_t grid = (p.B + kWarps - 1) / kWarps;
+  count_launch();
   sample_kernel<<<grid, kThreads, 0, s>>>(p);
   return cudaGetLastError();
 }

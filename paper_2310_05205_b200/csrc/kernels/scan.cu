@@ -157,6 +157,7 @@ cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf, uint64_t shard_cap,
                         uint32_t* ticket_cur, uint32_t* ticket_next, cudaStream_t s) {
   const uint32_t tps = scan_tiles_per_shard(shard_cap);
   const uint32_t n_tiles = tps * n_shards_local;
+  count_launch();
   if (indicator)
     scan_kernel<true><<<n_tiles, kThreads, 0, s>>>(key, cdf, shard_cap, tps, n_tiles, parity,
                                                    totals_out, status_cur, status_next,

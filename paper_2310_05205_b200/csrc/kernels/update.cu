@@ -97,6 +97,7 @@ cudaError_t launch_update_quantize(const uint64_t* idx, const void* prio, int pr
                                    uint32_t frac_bits, uint64_t q_max, UpdRec* out,
                                    uint32_t* err, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
+  count_launch();
   quantize_kernel<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(
       idx, prio, prio_is_f64, gen, n, n_global, frac_bits, q_max, out, err);
   return cudaGetLastError();
@@ -107,6 +108,7 @@ cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_beg
                               uint32_t epoch, unsigned long long* n_stale, uint32_t* err,
                               cudaStream_t s) {
   if (m == 0) return cudaSuccess;
+  count_launch();
   tag_kernel<<<(m + kThreads - 1) / kThreads, kThreads, 0, s>>>(
       recs, m, local_begin, local_rows, gen, tag, epoch, n_stale, err);
   return cudaGetLastError();
@@ -117,6 +119,7 @@ cudaError_t launch_update_apply(const UpdRec* recs, uint32_t m, uint64_t local_b
                                 const unsigned long long* tag, uint32_t epoch, uint64_t* key,
                                 cudaStream_t s) {
   if (m == 0) return cudaSuccess;
+  count_launch();
   apply_kernel<<<(m + kThreads - 1) / kThreads, kThreads, 0, s>>>(recs, m, local_begin,
                                                                   local_rows, gen, tag, epoch, key);
   return cudaGetLastError();

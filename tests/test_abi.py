@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _declared():
     src = open(os.path.join(ROOT, "include", "gear.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return set(re.findall(r"^\s*(?:gear_status|const char\*)\s+(gear_\w+)\s*\(", src, flags=re.M))
+    return set(re.findall(r"^\s*(?:gear_status|const char\*|uint64_t)\s+(gear_\w+)\s*\(", src, flags=re.M))
 
 
 def test_header_declares_hot_path_calls():
