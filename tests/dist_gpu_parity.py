@@ -1,0 +1,125 @@
+"""Multi-GPU parity (one process per GPU, NCCL over NVLink): launched by
+tests/test_gpu_multi.py as
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/dist_gpu_parity.py
+
+Every rank runs the SPMD hot path on its shard(s) of a table sharded by
+trajectory id, and checks its slice against the unsharded CPU oracle:
+sampled ids (bit-exact), IS weights (1e-6 rel), collected rows -- including
+rows of peer shards read over NVLink (DEVICE columns) and rows of other
+ranks' host shards read zero-copy over this GPU's PCIe (HOST columns) -- and
+the keys after collective priority updates.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+import paper_2310_05205_b200 as gear  # noqa: E402
+
+OS = {gear.GEAR_FIFO: oracle.FIFO, gear.GEAR_LIFO: oracle.LIFO, gear.GEAR_UNIFORM: oracle.UNIFORM,
+      gear.GEAR_WEIGHTED: oracle.WEIGHTED, gear.GEAR_PRIORITIZED: oracle.PRIORITIZED}
+
+
+def run_case(comm, W, rank, R, placements, removal, Cs=700, B=40, steps=3):
+    dt = [gear.GEAR_F32, gear.GEAR_U8, gear.GEAR_I32]
+    shapes = [(5,), (3,), ()]
+    cols = [gear.Column(f"c{i}", dt[i % 3], shapes[i % 3], p) for i, p in enumerate(placements)]
+    S = W * R
+    N = S * Cs
+    t = gear.Table(N, 4, cols, comm, shards_per_rank=R, removal=removal, max_batch=1024)
+    o = oracle.Table(Cs, S, removal=removal)
+    rb = t.row_bytes
+    content = np.full(N, -1, np.int64)
+    prio_all = synth.priorities(2 * N, seed=9, zero_frac=0.1)
+    rng = np.random.default_rng(5)
+    plan = []                                   # (shard, n) inserts, same on every rank
+    for s in range(S):
+        k = 0
+        while k < int(Cs * 1.25):
+            b = int(rng.integers(1, 400))
+            b = min(b, int(Cs * 1.25) - k)
+            plan.append((s, k, b))
+            k += b
+    for s, k, b in plan:
+        traj = np.arange(s * 2 * Cs + k, s * 2 * Cs + k + b)
+        p = prio_all[s * 2 * Cs + k: s * 2 * Cs + k + b]
+        st, oidx = o.insert(s, p)
+        content[oidx.astype(np.int64)] = traj
+        if s // R == rank:
+            rows = [torch.from_numpy(synth.row_bytes_of(c, traj, rb[c])).cuda() for c in range(len(cols))]
+            out = np.zeros(b, np.uint64)
+            t.insert(s, rows, p, out)
+            assert np.array_equal(out, oidx), "insert slots differ"
+    torch.cuda.synchronize()
+    dist.barrier()
+    key, seq, gen = t.read_state()
+    lo, hi = rank * R * Cs, (rank + 1) * R * Cs
+    assert np.array_equal(key, o.key[lo:hi]) and np.array_equal(seq, o.seq[lo:hi])
+    assert np.array_equal(gen, o.gen[lo:hi])
+
+    for step in range(steps):
+        for strat in (gear.GEAR_UNIFORM, gear.GEAR_WEIGHTED, gear.GEAR_PRIORITIZED, gear.GEAR_FIFO,
+                      gear.GEAR_LIFO):
+            seed = synth.SAMPLE_SEED_BASE + 100 * step + strat
+            idx = torch.empty(B, dtype=torch.int64, device="cuda")
+            w = torch.empty(B, dtype=torch.float32, device="cuda")
+            pr = torch.empty(B, dtype=torch.float64, device="cuda")
+            t.sample(strat, B, seed, 0.4, idx, w, pr)
+            torch.cuda.synchronize()
+            st, oi, ow, op = o.sample(OS[strat], W, rank, B, seed, 0.4)
+            assert st == 0, st
+            gi = idx.cpu().numpy().view(np.uint64)
+            assert np.array_equal(gi, oi), f"strategy {strat}: ids differ at {np.nonzero(gi != oi)[0][:8]}"
+            np.testing.assert_allclose(w.cpu().numpy(), ow, rtol=1e-6)
+            assert np.array_equal(pr.cpu().numpy(), op)
+            outs = [torch.empty((B, r), dtype=torch.uint8, device="cuda") for r in rb]
+            t.collect(idx, list(range(len(cols))), outs)
+            torch.cuda.synchronize()
+            for c in range(len(cols)):
+                want = synth.row_bytes_of(c, content[oi.astype(np.int64)], rb[c])
+                assert np.array_equal(outs[c].cpu().numpy(), want), f"collect column {c}"
+            err, _ = t.sync()
+            assert err == 0, err
+        # collective update: every rank updates its own sampled ids
+        newp = np.random.default_rng(1000 * step + rank).lognormal(0, 1, B)
+        newp[:3] = 0.0
+        gear.gear_update_priorities(t.handle, B, idx, torch.from_numpy(newp).cuda(), gear.GEAR_F64)
+        torch.cuda.synchronize()
+        lists = [None] * W
+        dist.all_gather_object(lists, (gi, newp))
+        for r in range(W):                             # (rank, position) order
+            o.update(lists[r][0], lists[r][1])
+        key, _, _ = t.read_state()
+        assert np.array_equal(key, o.key[lo:hi]), "keys after the collective update"
+    t.close()
+
+
+def main():
+    W = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ["RANK"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = gear.comm_from_torch_distributed(local)
+    D, H = gear.GEAR_DEVICE, gear.GEAR_HOST
+    cases = [(1, [D, D, D], 0), (2, [D, D, D], 1), (1, [H, H, H], 0), (2, [D, H, D], 0)]
+    for R, pl, removal in cases:
+        run_case(comm, W, rank, R, pl, removal)
+        dist.barrier()
+        if rank == 0:
+            print(f"case R={R} placements={pl} removal={removal}: ok", flush=True)
+    gear.gear_comm_destroy(comm)
+    dist.destroy_process_group()
+    print(f"rank {rank}: all multi-GPU parity cases ok", flush=True)
+
+
+if __name__ == "__main__":
+    main()
