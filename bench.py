@@ -172,47 +172,83 @@ def run_gpu(args):
         h_idx = torch.empty(B, dtype=torch.int64, pin_memory=True)
         h_w = torch.empty(B, dtype=torch.float32, pin_memory=True)
         h_prio = [torch.from_numpy(synth.priorities(B, seed=1000 + k)).pin_memory() for k in range(16)]
-    ev_c0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev_c1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    # Second stream and idx double buffer for the pipelined step.
+    cstream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        idx2 = [idx, torch.empty(B, dtype=torch.int64, device="cuda")]
+    ev_sampled = [torch.cuda.Event() for _ in range(2)]
+    ev_collected = [torch.cuda.Event() for _ in range(2)]
 
-    def step(i, timed):
-        seed = synth.SAMPLE_SEED_BASE + i
-        gear.gear_sample(t.handle, strategy, B, seed, cfg.beta, idx, w, None, None, stream)
-        if timed:
-            ev_c0[i].record(stream)
+    def step_serial(i, ev):
+        """sample -> collect -> update, all on one stream."""
+        gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + i, cfg.beta, idx, w,
+                         None, None, stream)
+        if ev:
+            ev[0][i].record(stream)
         gear.gear_collect(t.handle, B, idx, col_ids, outs, stream)
-        if timed:
-            ev_c1[i].record(stream)
+        if ev:
+            ev[1][i].record(stream)
         if cfg.update:
             gear.gear_update_priorities(t.handle, B, idx, pool[i % 16], gear.GEAR_F64, None, stream)
 
+    def step_pipe(i, ev):
+        """The same three calls; selection (sample + update, which share the
+        keys) stays in order on `stream`, collection runs on `cstream`, so
+        collect(i) overlaps update(i) and sample(i+1).  idx is double
+        buffered: sample(i+2) waits until collect(i) has read idx[i%2]."""
+        b = i % 2
+        if i >= 2:
+            stream.wait_event(ev_collected[b])
+        gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + i, cfg.beta, idx2[b], w,
+                         None, None, stream)
+        ev_sampled[b].record(stream)
+        if cfg.update:
+            gear.gear_update_priorities(t.handle, B, idx2[b], pool[i % 16], gear.GEAR_F64, None,
+                                        stream)
+        cstream.wait_event(ev_sampled[b])
+        if ev:
+            ev[0][i].record(cstream)
+        gear.gear_collect(t.handle, B, idx2[b], col_ids, outs, cstream)
+        if ev:
+            ev[1][i].record(cstream)
+        ev_collected[b].record(cstream)
+
     def barrier():
         stream.synchronize()
+        cstream.synchronize()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
 
-    for i in range(args.warmup):
-        step(i, False)
-    barrier()
-    err, _ = t.sync()
-    assert err == 0, f"device error bits {err} during warm-up"
-    clocks = ClockSampler(local)
-    clocks.start()
-    l0 = gear.gear_kernel_launches()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record(stream)
-    for i in range(args.steps):
-        step(i, True)
-    e1.record(stream)
-    barrier()
-    launches = gear.gear_kernel_launches() - l0
-    clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    coll_ms = [a.elapsed_time(b) for a, b in zip(ev_c0, ev_c1)]
-    err, _ = t.sync()
-    assert err == 0, f"device error bits {err} in the timed region"
+    def timed(step_fn):
+        for i in range(args.warmup):
+            step_fn(i, None)
+        barrier()
+        err, _ = t.sync()
+        assert err == 0, f"device error bits {err} during warm-up"
+        ev = ([torch.cuda.Event(enable_timing=True) for _ in range(args.steps)],
+              [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)])
+        clocks = ClockSampler(local)
+        clocks.start()
+        l0 = gear.gear_kernel_launches()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        cstream.wait_event(e0)
+        for i in range(args.steps):
+            step_fn(i, ev)
+        stream.wait_stream(cstream)
+        e1.record(stream)
+        barrier()
+        launches = gear.gear_kernel_launches() - l0
+        clk = clocks.stop()
+        err, _ = t.sync()
+        assert err == 0, f"device error bits {err} in the timed region"
+        coll = float(np.mean([a.elapsed_time(b) for a, b in zip(*ev)]))
+        return e0.elapsed_time(e1), coll, launches, clk
+
+    ms, coll_ms_p, launches, clk = timed(step_pipe)
+    ms_serial, coll_ms_s, _, clk_s = timed(step_serial)
 
     # end-to-end through the C-ABI with HOST buffers: the step's priority update
     # (ids + f64 priorities) comes from pinned host memory, and the sampled ids
@@ -235,10 +271,10 @@ def run_gpu(args):
     barrier()
     e2e_ms = e2.elapsed_time(e3)
 
-    times = torch.tensor([ms, e2e_ms, float(np.mean(coll_ms))], device="cuda")
+    times = torch.tensor([ms, e2e_ms, coll_ms_p, ms_serial, coll_ms_s], device="cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
-    ms, e2e_ms, coll_avg = (float(x) for x in times.cpu())
+    ms, e2e_ms, coll_avg, ms_serial, coll_serial = (float(x) for x in times.cpu())
 
     traj = world * B * args.steps
     value = traj / (ms / 1e3)
@@ -283,6 +319,10 @@ def run_gpu(args):
                    "parallelism": f"dp{world} (table sharded by trajectory id, 1 shard per GPU)",
                    **({"note": cap_note} if cap_note else {})},
         "collect_gbps": payload / (coll_avg / 1e3) / 1e9,
+        "step": "pipelined: collect(i) on a 2nd stream overlaps update(i) + sample(i+1)",
+        "serial": {"value": traj / (ms_serial / 1e3), "ms_per_step": ms_serial / args.steps,
+                   "collect_avg_ms": coll_serial,
+                   "note": "sample -> collect -> update on one stream, same K steps"},
         "roofline": roof,
         "e2e": {"value": traj / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": (16 * B if cfg.update else 0),
                 "d2h_bytes_per_step": 12 * B},

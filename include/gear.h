@@ -243,6 +243,24 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
  * be NULL.  Returns STATE if any bit was set, else OK. */
 gear_status gear_table_sync(gear_table* t, uint32_t* dev_errors, uint64_t* n_stale);
 
+/* Tuning knobs of the collect kernel (not collective, no device work):
+ *   "collect_impl": 1 = rows >= 4 KB with 16-byte alignment move by TMA bulk
+ *                   copies through shared memory (default), 0 = every row
+ *                   by warp-wide 16-byte LSU copies;
+ *   "lsu_chunk":    bytes per warp task of the LSU path (multiple of 512);
+ *   "tma_chunk":    bytes per TMA stage (multiple of 16, 4096..32768;
+ *                   default 16384);
+ *   "tma_ctas_per_sm": TMA CTAs per SM (default 2), "tma_stages": stages per
+ *                   CTA (2, 3, 4, 6, 8; default 3); ctas * stages * tma_chunk
+ *                   must stay <= 220 KB (set the smaller knob first);
+ *   "update_fused": 1 = priority updates of <= 8192 entries (all ranks) run
+ *                   tag + apply in one single-CTA launch (default), 0 = two
+ *                   grid-wide launches.
+ * Initial values also come from the environment (GEAR_COLLECT_IMPL=lsu|tma,
+ * GEAR_COLLECT_CHUNK, GEAR_TMA_CHUNK).  INVALID_ARG for an unknown key or
+ * value. */
+gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value);
+
 /* Read back this rank's slot state (device -> host, synchronous), for tests
  * and checkpoints: keys u64[R*C_s], seq u64[R*C_s], gen u32[R*C_s]; any
  * pointer may be NULL. */

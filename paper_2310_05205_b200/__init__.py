@@ -101,6 +101,7 @@ SIGNATURES = {
     "gear_collect": ([_P, _u32, _P, _u32, _P, _P, _P], _i32),
     "gear_table_sync": ([_P, _P, _P], _i32),
     "gear_read_state": ([_P, _P, _P, _P], _i32),
+    "gear_table_set_tuning": ([_P, ctypes.c_char_p, ctypes.c_int64], _i32),
 }
 
 _lib = None
@@ -285,6 +286,10 @@ def gear_read_state(t: int):
     gen = np.zeros(n, np.uint32)
     _check("gear_read_state", load().gear_read_state(t, _ptr(key), _ptr(seq), _ptr(gen)))
     return key, seq, gen
+
+
+def gear_table_set_tuning(t: int, key: str, value: int):
+    _check("gear_table_set_tuning", load().gear_table_set_tuning(t, key.encode(), value))
 
 
 class Table:

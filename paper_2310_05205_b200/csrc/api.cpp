@@ -186,6 +186,10 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   if (d->ncols == 0 || d->ncols > (uint32_t)kMaxCols || d->cols == nullptr)
     return set_error(GEAR_ERR_INVALID_ARG, "ncols must be 1..%d", kMaxCols);
   if (const char* e = getenv("GEAR_COLLECT_CHUNK")) t->chunk_bytes = (uint32_t)atoi(e);
+  if (const char* e = getenv("GEAR_TMA_CHUNK")) t->tma_chunk = (uint32_t)atoi(e);
+  if (const char* e = getenv("GEAR_COLLECT_IMPL")) t->collect_impl = strcmp(e, "lsu") == 0 ? 0 : 1;
+  if (t->tma_chunk < 4096 || t->tma_chunk % 16 || t->tma_chunk > 32768)
+    return set_error(GEAR_ERR_INVALID_ARG, "GEAR_TMA_CHUNK must be a multiple of 16 in [4096, 32768]");
   if (t->chunk_bytes < 512 || t->chunk_bytes % 512)
     return set_error(GEAR_ERR_INVALID_ARG, "GEAR_COLLECT_CHUNK must be a multiple of 512");
 
@@ -625,21 +629,35 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
     }
     if (gen) GEAR_TRY(stage_in(gen, n, t->upd_gen, s, &d_gen));
   }
-  GEAR_CUDA(launch_update_quantize(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N, t->F,
-                                   t->qmax, t->upd_local, t->err, s));
-  const UpdRec* recs = t->upd_local;
-  uint32_t m = n;
-  if (t->W > 1) {
-    GEAR_TRY(allgather_bytes(t->comm, t->upd_local, t->upd_all, (size_t)n * sizeof(UpdRec), s));
-    recs = t->upd_all;
-    m = n * t->W;
-  }
   t->epoch += 1;
   const uint64_t local_begin = (uint64_t)t->rank * t->Clocal;
-  GEAR_CUDA(launch_update_tag(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->epoch,
-                              t->n_stale, t->err, s));
-  GEAR_CUDA(launch_update_apply(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->epoch,
-                                t->key, s));
+  const bool fused = t->update_fused && (uint64_t)n * t->W <= update_fused_max();
+  if (t->W == 1 && fused) {
+    // one launch: quantise, tag, block barrier, apply
+    GEAR_CUDA(launch_update_fused(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, nullptr, n, t->N,
+                                  t->F, t->qmax, local_begin, t->Clocal, t->gen, t->tag, t->epoch,
+                                  t->n_stale, t->err, t->key, s));
+  } else {
+    GEAR_CUDA(launch_update_quantize(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N, t->F,
+                                     t->qmax, t->upd_local, t->err, s));
+    const UpdRec* recs = t->upd_local;
+    uint32_t m = n;
+    if (t->W > 1) {
+      GEAR_TRY(allgather_bytes(t->comm, t->upd_local, t->upd_all, (size_t)n * sizeof(UpdRec), s));
+      recs = t->upd_all;
+      m = n * t->W;
+    }
+    if (fused) {
+      GEAR_CUDA(launch_update_fused(nullptr, nullptr, 0, nullptr, recs, m, t->N, t->F, t->qmax,
+                                    local_begin, t->Clocal, t->gen, t->tag, t->epoch, t->n_stale,
+                                    t->err, t->key, s));
+    } else {
+      GEAR_CUDA(launch_update_tag(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->epoch,
+                                  t->n_stale, t->err, s));
+      GEAR_CUDA(launch_update_apply(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->epoch,
+                                    t->key, s));
+    }
+  }
   t->dirty = true;
   return GEAR_OK;
 }
@@ -754,9 +772,9 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
   cp.n_global = t->N;
   cp.ncols = ncols;
   cp.n = n;
-  cp.chunk_bytes = t->chunk_bytes;
   cp.err = t->err;
-  uint64_t chunks = 0;
+  cp.tma_ctas_per_sm = (uint32_t)t->tma_ctas;
+  cp.tma_stages = (uint32_t)t->tma_stages;
   for (uint32_t c = 0; c < ncols; ++c) {
     if (col_ids[c] >= t->cols.size()) return set_error(GEAR_ERR_INVALID_ARG, "bad column id %u", col_ids[c]);
     if (out[c] == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "out[%u] is NULL", c);
@@ -764,17 +782,27 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
     CollectCol& cc = cp.col[c];
     cc.out = (uint8_t*)out[c];
     cc.rb = cs.rb;
-    cc.chunks_per_row = (uint32_t)((cs.rb + t->chunk_bytes - 1) / t->chunk_bytes);
-    cc.chunk_begin = chunks;
     uintptr_t align_or = (uintptr_t)out[c];
     for (uint32_t r = 0; r < t->W; ++r) {
       cc.src[r] = cs.view[r];
       align_or |= (uintptr_t)cs.view[r];
     }
-    cc.vec = vec_width(cs.rb, t->chunk_bytes, {align_or});
-    chunks += (uint64_t)n * cc.chunks_per_row;
+    cc.vec = vec_width(cs.rb, 512, {align_or});
+    // Rows of >= 4 KB with 16-byte alignment go to the TMA bulk-copy path.
+    cc.tma = (t->collect_impl == 1 && cc.vec == 16 && cs.rb >= 4096) ? 1u : 0u;
+    cc.chunk = cc.tma ? t->tma_chunk : t->chunk_bytes;
+    if (cc.vec < 16 && cc.chunk % cc.vec) cc.chunk = t->chunk_bytes;
+    cc.chunks_per_row = (uint32_t)((cs.rb + cc.chunk - 1) / cc.chunk);
+    if (cc.tma) {
+      cc.chunk_begin = cp.tma_total;
+      cp.tma_total += (uint64_t)n * cc.chunks_per_row;
+      cp.tma_cols[cp.n_tma++] = (uint8_t)c;
+    } else {
+      cc.chunk_begin = cp.lsu_total;
+      cp.lsu_total += (uint64_t)n * cc.chunks_per_row;
+      cp.lsu_cols[cp.n_lsu++] = (uint8_t)c;
+    }
   }
-  cp.total_chunks = chunks;
   GEAR_CUDA(launch_collect(cp, s));
   return GEAR_OK;
 }
@@ -793,6 +821,32 @@ gear_status gear_table_sync(gear_table* t, uint32_t* dev_errors, uint64_t* n_sta
   if (dev_errors) *dev_errors = e;
   if (n_stale) *n_stale = ns;
   if (e) return set_error(GEAR_ERR_STATE, "device error bits 0x%x", e);
+  return GEAR_OK;
+}
+
+gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value) {
+  clear_error();
+  GEAR_TRY(check_table(t));
+  if (key == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "key is NULL");
+  if (!strcmp(key, "collect_impl") && (value == 0 || value == 1)) {
+    t->collect_impl = (int)value;
+  } else if (!strcmp(key, "lsu_chunk") && value >= 512 && value % 512 == 0 && value <= (1 << 20)) {
+    t->chunk_bytes = (uint32_t)value;
+  } else if (!strcmp(key, "update_fused") && (value == 0 || value == 1)) {
+    t->update_fused = (int)value;
+  } else if (!strcmp(key, "tma_ctas_per_sm") && value >= 1 && value <= 8 &&
+             (uint64_t)value * t->tma_stages * t->tma_chunk <= (220u << 10)) {
+    t->tma_ctas = (int)value;
+  } else if (!strcmp(key, "tma_stages") &&
+             (value == 2 || value == 3 || value == 4 || value == 6 || value == 8) &&
+             (uint64_t)value * t->tma_ctas * t->tma_chunk <= (220u << 10)) {
+    t->tma_stages = (int)value;
+  } else if (!strcmp(key, "tma_chunk") && value >= 4096 && value % 16 == 0 && value <= 32768 &&
+             (uint64_t)value * t->tma_ctas * t->tma_stages <= (220u << 10)) {
+    t->tma_chunk = (uint32_t)value;
+  } else {
+    return set_error(GEAR_ERR_INVALID_ARG, "bad tuning %s = %lld", key, (long long)value);
+  }
   return GEAR_OK;
 }
 

@@ -67,9 +67,11 @@ struct CollectCol {
   uint8_t* out;                       // [n][rb] output batch
   const uint8_t* src[kMaxRanks];      // device-accessible base of each rank's rows
   uint64_t rb;                        // row bytes
-  uint64_t chunk_begin;               // first global chunk id of this column
+  uint64_t chunk_begin;               // first task id of this column in its task space
   uint32_t chunks_per_row;
-  uint32_t vec;                       // vector width in bytes: 16, 8, 4 or 1
+  uint32_t chunk;                     // bytes per task of this column
+  uint32_t vec;                       // LSU vector width in bytes: 16, 8, 4, 2 or 1
+  uint32_t tma;                       // 1: moved by TMA bulk copies (16-B aligned rows)
 };
 
 struct CollectParams {
@@ -77,10 +79,16 @@ struct CollectParams {
   const uint64_t* idx;                // [n] global ids (device)
   uint64_t rows_per_rank;             // R * C_s
   uint64_t n_global;                  // N
-  uint64_t total_chunks;
+  uint64_t lsu_total;                 // tasks of the LSU (warp-copy) space
+  uint64_t tma_total;                 // tasks of the TMA bulk-copy space
+  uint8_t lsu_cols[kMaxCols];
+  uint8_t tma_cols[kMaxCols];
+  uint32_t n_lsu;
+  uint32_t n_tma;
+  uint32_t tma_ctas_per_sm;           // CTAs of the TMA kernel per SM
+  uint32_t tma_stages;                // 2, 3, 4, 6 or 8 shared-memory stages per CTA
   uint32_t ncols;
   uint32_t n;
-  uint32_t chunk_bytes;               // bytes per warp task
   uint32_t* err;
 };
 
@@ -154,6 +162,17 @@ cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_beg
 cudaError_t launch_update_apply(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                                 uint64_t local_rows, const uint32_t* gen,
                                 const unsigned long long* tag, uint32_t epoch, uint64_t* key,
+                                cudaStream_t s);
+
+// Single-launch update for m <= update_fused_max() entries (one CTA): raw
+// W = 1 inputs when idx != nullptr, else all-gathered records.
+uint32_t update_fused_max();
+cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_is_f64,
+                                const uint32_t* gen_in, const UpdRec* recs, uint32_t m,
+                                uint64_t n_global, uint32_t frac_bits, uint64_t q_max,
+                                uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
+                                unsigned long long* tag, uint32_t epoch,
+                                unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                 cudaStream_t s);
 
 // K5: collect (gather) and the insert-side scatter.

@@ -75,17 +75,29 @@ __device__ __forceinline__ void copy_dispatch(uint32_t vec, uint8_t* dst, const 
   }
 }
 
-__global__ void __launch_bounds__(kThreads) collect_kernel(const __grid_constant__ CollectParams p) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t task = warp0; task < p.total_chunks; task += nwarps) {
-    uint32_t c = 0;
-    while (c + 1 < p.ncols && task >= p.col[c + 1].chunk_begin) ++c;
+// Decode task `task` of a task space (columns `cols[0..ncols)` in order of
+// chunk_begin) into (column, row j, chunk k).
+__device__ __forceinline__ void decode_task(const CollectParams& p, const uint8_t* cols,
+                                            uint32_t ncols, uint64_t task, uint32_t* c_out,
+                                            uint64_t* j_out, uint64_t* k_out) {
+  uint32_t ci = 0;
+  while (ci + 1 < ncols && task >= p.col[cols[ci + 1]].chunk_begin) ++ci;
+  const uint32_t c = cols[ci];
+  const uint64_t rel = task - p.col[c].chunk_begin;
+  const uint64_t j = rel / p.col[c].chunks_per_row;
+  *c_out = c;
+  *j_out = j;
+  *k_out = rel - j * p.col[c].chunks_per_row;
+}
+
+// Warps [w_first, w_first + w_count) of every CTA walk the LSU task space.
+__device__ __forceinline__ void collect_lsu(const CollectParams& p, uint64_t warp0,
+                                            uint64_t nwarps, int lane) {
+  for (uint64_t task = warp0; task < p.lsu_total; task += nwarps) {
+    uint32_t c;
+    uint64_t j, k;
+    decode_task(p, p.lsu_cols, p.n_lsu, task, &c, &j, &k);
     const CollectCol& col = p.col[c];
-    const uint64_t rel = task - col.chunk_begin;
-    const uint64_t j = rel / col.chunks_per_row;
-    const uint64_t k = rel - j * col.chunks_per_row;
     const uint64_t g = __ldg(p.idx + j);
     if (g >= p.n_global) {
       if (lane == 0 && k == 0) atomicOr(p.err, kErrIndexRange);
@@ -93,12 +105,123 @@ __global__ void __launch_bounds__(kThreads) collect_kernel(const __grid_constant
     }
     const uint64_t owner = g / p.rows_per_rank;
     const uint64_t local = g - owner * p.rows_per_rank;
-    const uint64_t off = k * (uint64_t)p.chunk_bytes;
+    const uint64_t off = k * (uint64_t)col.chunk;
     const uint64_t rem = col.rb - off;
-    const uint64_t bytes = rem < p.chunk_bytes ? rem : p.chunk_bytes;
+    const uint64_t bytes = rem < col.chunk ? rem : col.chunk;
     copy_dispatch(col.vec, col.out + j * col.rb + off, col.src[owner] + local * col.rb + off,
                   bytes, lane);
   }
+}
+
+__global__ void __launch_bounds__(kThreads) collect_kernel(const __grid_constant__ CollectParams p) {
+  const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  collect_lsu(p, warp0, (uint64_t)gridDim.x * kWarps, threadIdx.x & 31);
+}
+
+// ---- TMA bulk-copy variant -------------------------------------------------
+// One CTA per SM.  Lane 0 of warp 0 runs a kStages-deep ring of shared-memory
+// stages: cp.async.bulk global->shared completes on the stage's mbarrier,
+// then cp.async.bulk shared->global writes the stage to the batch and a
+// bulk async-group tracks when the stage may be refilled.  A CTA keeps up to
+// kStages * stage bytes in flight with no register cost, independent of the
+// source (local HBM, a peer's HBM over NVLink, or mapped host memory).  The
+// other warps copy the columns whose rows are not 16-byte aligned.
+constexpr int kTmaThreads = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Issue the bulk load of TMA task `task` into stage `s` (mbarrier bars[s]).
+// Returns the bytes moved (0 for an invalid id: the barrier is still armed).
+__device__ __forceinline__ uint32_t tma_issue_load(const CollectParams& p, uint64_t task,
+                                                   uint32_t stage_addr, uint32_t bar,
+                                                   uint8_t** dst) {
+  uint32_t c;
+  uint64_t j, k;
+  decode_task(p, p.tma_cols, p.n_tma, task, &c, &j, &k);
+  const CollectCol& col = p.col[c];
+  const uint64_t g = __ldg(p.idx + j);
+  if (g >= p.n_global) {
+    if (k == 0) atomicOr(p.err, kErrIndexRange);
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+    return 0;
+  }
+  const uint64_t owner = g / p.rows_per_rank;
+  const uint64_t local = g - owner * p.rows_per_rank;
+  const uint64_t off = k * (uint64_t)col.chunk;
+  const uint64_t rem = col.rb - off;
+  const uint32_t bytes = (uint32_t)(rem < col.chunk ? rem : col.chunk);
+  *dst = col.out + j * col.rb + off;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          stage_addr),
+      "l"(col.src[owner] + local * col.rb + off), "r"(bytes), "r"(bar)
+      : "memory");
+  return bytes;
+}
+
+// Pipeline of the issuing lane, over its tasks n = 0, 1, ... (task id
+// blockIdx.x + n * gridDim.x):  loads of tasks n+1 .. n+kStages-1 are in
+// flight while task n is stored; the stage of task n-1 is refilled (task
+// n-1+kStages) once its store has finished reading shared memory
+// (wait_group.read 1: only the store of task n may still be reading).
+template <int kStages>
+__global__ void __launch_bounds__(kTmaThreads)
+    collect_tma_kernel(const __grid_constant__ CollectParams p, uint32_t stage_bytes) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bars[kStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp != 0) {
+    const uint64_t w0 = (uint64_t)blockIdx.x * (kTmaThreads / 32 - 1) + (warp - 1);
+    collect_lsu(p, w0, (uint64_t)gridDim.x * (kTmaThreads / 32 - 1), lane);
+    return;
+  }
+  if (lane != 0) return;
+  for (int s = 0; s < kStages; ++s)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[s])) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  const uint64_t first = blockIdx.x, step = gridDim.x;
+  const uint64_t ntask = p.tma_total > first ? (p.tma_total - first + step - 1) / step : 0;
+  const uint32_t base = smem_u32(smem);
+  uint8_t* dst[kStages] = {};
+  uint32_t nbytes[kStages] = {};
+  uint32_t phase = 0;
+  for (uint64_t n = 0; n < ntask && n < (uint64_t)kStages; ++n)
+    nbytes[n] = tma_issue_load(p, first + n * step, base + (uint32_t)n * stage_bytes,
+                               smem_u32(&bars[n]), &dst[n]);
+  for (uint64_t n = 0; n < ntask; ++n) {
+    const int s = (int)(n % kStages);
+    while (!mbar_try_wait(smem_u32(&bars[s]), (phase >> s) & 1u)) {
+    }
+    phase ^= 1u << s;
+    if (nbytes[s])
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst[s]),
+                   "r"(base + (uint32_t)s * stage_bytes), "r"(nbytes[s])
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (n >= 1 && n - 1 + kStages < ntask) {
+      const int sp = (int)((n - 1) % kStages);
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      nbytes[sp] = tma_issue_load(p, first + (n - 1 + kStages) * step,
+                                  base + (uint32_t)sp * stage_bytes, smem_u32(&bars[sp]), &dst[sp]);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant__ ScatterParams p) {
@@ -153,11 +276,42 @@ int grid_for(K kernel, uint64_t tasks) {
 
 }  // namespace
 
-cudaError_t launch_collect(const CollectParams& p, cudaStream_t s) {
-  if (p.total_chunks == 0) return cudaSuccess;
+// kStages stages of tma_chunk bytes per CTA, ctas CTAs per SM (192 KB of
+// shared memory per SM either way).
+template <int kStages>
+cudaError_t launch_tma(const CollectParams& p, int ctas, cudaStream_t s) {
+  const uint32_t stage_bytes = p.col[p.tma_cols[0]].chunk;
+  const size_t smem = (size_t)kStages * stage_bytes;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(collect_tma_kernel<kStages>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   count_launch();
-  collect_kernel<<<grid_for(collect_kernel, p.total_chunks), kThreads, 0, s>>>(p);
+  collect_tma_kernel<kStages><<<sms * ctas, kTmaThreads, smem, s>>>(p, stage_bytes);
   return cudaGetLastError();
+}
+
+cudaError_t launch_collect(const CollectParams& p, cudaStream_t s) {
+  if (p.lsu_total + p.tma_total == 0) return cudaSuccess;
+  if (p.tma_total == 0) {
+    count_launch();
+    collect_kernel<<<grid_for(collect_kernel, p.lsu_total), kThreads, 0, s>>>(p);
+    return cudaGetLastError();
+  }
+  const int ctas = (int)p.tma_ctas_per_sm;
+  switch (p.tma_stages) {
+    case 2: return launch_tma<2>(p, ctas, s);
+    case 3: return launch_tma<3>(p, ctas, s);
+    case 4: return launch_tma<4>(p, ctas, s);
+    case 6: return launch_tma<6>(p, ctas, s);
+    default: return launch_tma<8>(p, ctas, s);
+  }
 }
 
 cudaError_t launch_scatter(const ScatterParams& p, cudaStream_t s) {

@@ -90,7 +90,85 @@ __global__ void __launch_bounds__(kThreads)
     key[local] = r.q;
 }
 
+// Single-CTA variant for up to kFusedMax entries: tag pass, block barrier,
+// apply pass in one launch.  With `idx != nullptr` the entries are the raw
+// (W = 1) inputs and are quantised in place; otherwise `recs` holds the
+// all-gathered records of every rank.
+constexpr int kFusedThreads = 1024;
+constexpr uint32_t kFusedMax = 8192;
+constexpr int kFusedPer = kFusedMax / kFusedThreads;
+
+__global__ void __launch_bounds__(kFusedThreads)
+    fused_kernel(const uint64_t* __restrict__ idx, const void* __restrict__ prio, int prio_is_f64,
+                 const uint32_t* __restrict__ gen_in, const UpdRec* __restrict__ recs, uint32_t m,
+                 uint64_t n_global, uint32_t frac_bits, uint64_t q_max, uint64_t local_begin,
+                 uint64_t local_rows, const uint32_t* __restrict__ gen, unsigned long long* tag,
+                 uint32_t epoch, unsigned long long* n_stale, uint32_t* err, uint64_t* key) {
+  UpdRec r[kFusedPer];
+  bool mine[kFusedPer];
+  uint64_t loc[kFusedPer];
+  uint32_t e = 0, stale = 0;
+#pragma unroll
+  for (int u = 0; u < kFusedPer; ++u) {
+    const uint32_t k = threadIdx.x + u * kFusedThreads;
+    mine[u] = false;
+    if (k >= m) continue;
+    if (idx) {
+      r[u].idx = idx[k];
+      r[u].gen = gen_in ? gen_in[k] : 0u;
+      r[u].flags = gen_in ? 2u : 0u;
+      const double p = prio_is_f64 ? static_cast<const double*>(prio)[k]
+                                   : (double)static_cast<const float*>(prio)[k];
+      if (r[u].idx == kIdxNone) {
+      } else if (r[u].idx >= n_global) {
+        e |= kErrIndexRange;
+      } else if (!quantize(p, frac_bits, q_max, &r[u].q)) {
+        e |= kErrBadPriority;
+      } else {
+        r[u].flags |= 1u;
+      }
+    } else {
+      r[u] = recs[k];
+    }
+    bool st;
+    mine[u] = owned_and_fresh(r[u], local_begin, local_rows, gen, &loc[u], &st);
+    stale += st ? 1u : 0u;
+    if (mine[u])
+      atomicMax(tag + loc[u], ((unsigned long long)epoch << 32) | (unsigned long long)(k + 1));
+  }
+  if (stale) {
+    atomicAdd(n_stale, (unsigned long long)stale);
+    e |= kErrStale;
+  }
+  if (e) atomicOr(err, e);
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kFusedPer; ++u) {
+    const uint32_t k = threadIdx.x + u * kFusedThreads;
+    if (mine[u] && __ldcg(tag + loc[u]) ==
+                       (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1)))
+      key[loc[u]] = r[u].q;
+  }
+}
+
 }  // namespace
+
+uint32_t update_fused_max() { return kFusedMax; }
+
+cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_is_f64,
+                                const uint32_t* gen_in, const UpdRec* recs, uint32_t m,
+                                uint64_t n_global, uint32_t frac_bits, uint64_t q_max,
+                                uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
+                                unsigned long long* tag, uint32_t epoch,
+                                unsigned long long* n_stale, uint32_t* err, uint64_t* key,
+                                cudaStream_t s) {
+  if (m == 0) return cudaSuccess;
+  count_launch();
+  fused_kernel<<<1, kFusedThreads, 0, s>>>(idx, prio, prio_is_f64, gen_in, recs, m, n_global,
+                                           frac_bits, q_max, local_begin, local_rows, gen, tag,
+                                           epoch, n_stale, err, key);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_update_quantize(const uint64_t* idx, const void* prio, int prio_is_f64,
                                    const uint32_t* gen, uint32_t n, uint64_t n_global,

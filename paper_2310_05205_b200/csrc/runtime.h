@@ -153,5 +153,10 @@ struct gear_table {
   uint8_t* d_rows = nullptr;        // staging for pageable row sources
   size_t d_rows_bytes = 0;
   cudaEvent_t staging_ev = nullptr;
-  uint32_t chunk_bytes = 8192;      // collect warp-task size
+  uint32_t chunk_bytes = 8192;      // collect warp-task size (LSU path)
+  uint32_t tma_chunk = 16384;       // collect TMA stage size
+  int update_fused = 1;             // single-CTA tag+apply update when it fits
+  int tma_ctas = 2;                 // TMA collect CTAs per SM
+  int tma_stages = 3;               // shared-memory stages per TMA CTA
+  int collect_impl = 1;             // 1: TMA bulk copies for large aligned rows, 0: LSU only
 };

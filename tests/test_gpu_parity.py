@@ -89,9 +89,13 @@ def test_zero_weight_and_empty(torch_cuda):
     P.close()
 
 
-def test_update_errors_duplicates_and_generations(torch_cuda):
+@pytest.mark.parametrize("fused", [0, 1])
+def test_update_errors_duplicates_and_generations(torch_cuda, fused):
+    """Both update paths: the single-CTA fused launch and the two grid-wide
+    tag/apply launches."""
     cols = [synth.ColSpec("x", "u8", (8,))]
     P = _pair(capacity=256, seq_len=1, colspecs=cols, R=2)
+    G.gear_table_set_tuning(P.t.handle, "update_fused", fused)
     P.insert(0, np.ones(100))
     P.insert(1, np.ones(128))
     rng = np.random.default_rng(11)
@@ -232,4 +236,28 @@ def test_deterministic_across_repeats_and_beta(torch_cuda):
     qmin = key.min()
     assert np.array_equal(b[1], np.array([np.float32(int(qmin) / int(k)) for k in key]))
     P.check_sample(G.GEAR_PRIORITIZED, 512, 3, 1.0)
+    P.close()
+
+
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("placement", ["device", "host"])
+def test_collect_large_rows_tma_and_lsu(torch_cuda, impl, placement):
+    """Rows >= 4 KB with 16-byte alignment take the TMA bulk-copy path
+    (impl 1), the rest the warp-LSU path; ragged last chunks, duplicate ids,
+    three shards, both placements, several chunk sizes."""
+    cols = [synth.ColSpec("big", "u8", (5008,)), synth.ColSpec("tok", "i32", (256,)),
+            synth.ColSpec("odd", "u8", (7,)), synth.ColSpec("f", "f32", (3,))]
+    P = _pair(capacity=3 * 97, seq_len=9, colspecs=cols, R=3, placement=placement)
+    assert P.rb == [45072, 9216, 63, 108]
+    P.fill(synth.priorities(3 * 97, seed=8))
+    rng = np.random.default_rng(impl)
+    G.gear_table_set_tuning(P.t.handle, "collect_impl", impl)
+    for tma_chunk, lsu_chunk in ((32768, 8192), (4096, 512), (16384, 1024)):
+        G.gear_table_set_tuning(P.t.handle, "tma_chunk", tma_chunk)
+        G.gear_table_set_tuning(P.t.handle, "lsu_chunk", lsu_chunk)
+        idx = rng.integers(0, 3 * 97, size=300).astype(np.uint64)
+        P.check_collect(idx)
+        P.check_collect(idx[:1], col_ids=[1, 0])
+    with pytest.raises(G.GearError):
+        G.gear_table_set_tuning(P.t.handle, "tma_chunk", 100)
     P.close()
