@@ -31,6 +31,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep stdout to the one JSON line
 
 METRIC = "sampled+collected trajectories/sec and collect GB/s vs HBM/PCIe roofline, 1/2/4/8 B200"
 UNIT = "trajectories/s"
@@ -156,6 +157,8 @@ def run_gpu(args):
     stream = torch.cuda.Stream()
     t, prio_all = build_table(cfg, comm, world, rank, capacity, stream)
     strategy = gear.STRATEGIES[cfg.strategy]
+    if args.assign == "owner":
+        strategy |= gear.GEAR_SAMPLE_OWNER_AFFINE
     B = cfg.batch
     ncols = len(t.row_bytes)
     col_ids = list(range(ncols))
@@ -280,29 +283,31 @@ def run_gpu(args):
     value = traj / (ms / 1e3)
     hbm_peak, hbm_src = _peaks()
     # Algorithmic bytes of one collect launch: every
-    # payload byte is read once from its source and written once to HBM.
-    if world == 1 and host_bytes == 0:
-        alg = 2 * payload
-        roof = {"bound": "hbm", "achieved": alg / (coll_avg / 1e3) / 1e9, "peak": hbm_peak,
-                "unit": "GB/s", "peak_source": hbm_src}
-    elif host_bytes and dev_bytes == 0:
-        roof = {"bound": "pcie", "achieved": payload / (coll_avg / 1e3) / 1e9, "peak": PCIE_H2D_GBS,
-                "unit": "GB/s", "peak_source": "probe: pinned H2D cudaMemcpy (profiles/r01_probe_2gpu.jsonl)"}
-    else:
-        # remote fraction (W-1)/W of the payload crosses NVLink into this GPU
-        remote = dev_bytes * (world - 1) / world
-        t_nvl = remote / (NVLINK_PEER_GBS * 1e9)
-        t_hbm = 2 * dev_bytes / (hbm_peak * 1e9)
-        t_pcie = host_bytes / (PCIE_H2D_GBS * 1e9)
-        bound = max((t_nvl, "nvlink"), (t_hbm, "hbm"), (t_pcie, "pcie"))
-        roof = {"bound": bound[1], "achieved": None, "peak": None, "unit": "GB/s",
-                "ideal_ms": bound[0] * 1e3}
-        roof["frac"] = bound[0] * 1e3 / coll_avg
-    if roof.get("achieved") is not None:
-        roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["kernel"] = "collect_kernel"
+    # payload byte is read once from its source (local HBM, a peer's HBM over
+    # NVLink, or host memory over this GPU's PCIe) and written once to local
+    # HBM.  The remote fraction is measured on the step's sampled ids.
+    Cl = capacity // world
+    own = (idx2[(args.steps - 1) % 2].cpu().numpy().astype(np.uint64) // np.uint64(Cl))
+    f_remote = torch.tensor([float(np.mean(own != rank))], device="cuda")
+    if world > 1:
+        dist.all_reduce(f_remote, op=dist.ReduceOp.MAX)
+    f_remote = float(f_remote.item())
+    remote = dev_bytes * f_remote
+    t_ideal = {"hbm": (2 * dev_bytes - remote) / (hbm_peak * 1e9),
+               "nvlink": remote / (NVLINK_PEER_GBS * 1e9),
+               "pcie": host_bytes / (PCIE_H2D_GBS * 1e9)}
+    bound = max(t_ideal, key=t_ideal.get)
+    alg = {"hbm": 2 * dev_bytes - remote, "nvlink": remote, "pcie": host_bytes}[bound]
+    peak = {"hbm": hbm_peak, "nvlink": NVLINK_PEER_GBS, "pcie": PCIE_H2D_GBS}[bound]
+    roof = {"bound": bound, "achieved": alg / (coll_avg / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+            "peak_source": {"hbm": hbm_src,
+                            "nvlink": "probe: cudaMemcpyPeer pull (profiles/r01_probe_2gpu.jsonl)",
+                            "pcie": "probe: pinned H2D cudaMemcpy (profiles/r01_probe_2gpu.jsonl)"}[bound]}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["kernel"] = "collect_tma_kernel" if max(t.row_bytes) >= 4096 else "collect_kernel"
     roof["avg_launch_ms"] = coll_avg
-    roof["algorithmic_bytes_per_launch"] = 2 * payload if roof["bound"] == "hbm" else payload
+    roof["algorithmic_bytes_per_launch"] = alg
+    roof["remote_fraction"] = f_remote
     roof["traffic"] = args.traffic
 
     line = {
@@ -317,6 +322,7 @@ def run_gpu(args):
                    "l2": "inputs larger than L2: random rows of a %.1f GB table, %.0f MB batch per rank"
                          % (capacity * row_total / 1e9, payload / 1e6),
                    "parallelism": f"dp{world} (table sharded by trajectory id, 1 shard per GPU)",
+                   "assignment": args.assign,
                    **({"note": cap_note} if cap_note else {})},
         "collect_gbps": payload / (coll_avg / 1e3) / 1e9,
         "step": "pipelined: collect(i) on a 2nd stream overlaps update(i) + sample(i+1)",
@@ -423,6 +429,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--assign", default="owner", choices=["owner", "contiguous"],
+                    help="owner-affine (DESIGN.md Q19) or contiguous rank slices of the global batch")
     ap.add_argument("--impl", default="gear", choices=["gear", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

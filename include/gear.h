@@ -94,6 +94,16 @@ typedef enum {
   GEAR_PRIORITIZED = 4
 } gear_strategy;
 
+/* Flag OR-ed into the strategy of gear_sample: owner-affine assignment of
+ * the same global batch (Q19; data locality, "the
+ * majority of the trajectories collected by the servers reside in local
+ * memory").  Instead of the contiguous positions [r*B, (r+1)*B), rank r keeps
+ * up to B entries of the global batch that its own shards own (in global
+ * order); the surplus of over-full owners, in global order, fills the
+ * under-full ranks in rank order.  Same W*B entries, same distribution, so
+ * each rank mostly collects rows from its own HBM instead of over NVLink. */
+#define GEAR_SAMPLE_OWNER_AFFINE 0x100
+
 /* Victim choice when a shard is full. */
 typedef enum { GEAR_REMOVE_FIFO = 0, GEAR_REMOVE_LIFO = 1 } gear_removal;
 

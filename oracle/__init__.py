@@ -63,6 +63,8 @@ def lib():
         L.gor_inverse.restype = u64
         L.gor_sample.argtypes = [i32, P, P, u64, u32, u32, u32, u32, u64, f64, P, P, P]
         L.gor_sample.restype = i32
+        L.gor_sample_owner_affine.argtypes = [i32, P, P, u64, u32, u32, u32, u32, u64, f64, P, P, P]
+        L.gor_sample_owner_affine.restype = i32
         L.gor_update.argtypes = [P, P, u64, u32, u32, P, P, P, P]
         L.gor_update.restype = i32
         L.gor_translate.argtypes = [u64, u64, P, P]
@@ -132,6 +134,19 @@ def sample(strategy: int, key: np.ndarray, seq: np.ndarray | None, shard_cap: in
     return st, idx, w, p
 
 
+def sample_owner_affine(strategy: int, key: np.ndarray, seq: np.ndarray | None, shard_cap: int,
+                        n_shards: int, n_ranks: int, rank: int, B: int, seed: int, beta: float = 0.0):
+    """Reading Q19: the same global batch, assigned to ranks by owner."""
+    key = np.ascontiguousarray(key, dtype=np.uint64)
+    seq = np.zeros_like(key) if seq is None else np.ascontiguousarray(seq, dtype=np.uint64)
+    idx = np.zeros(B, dtype=np.uint64)
+    w = np.zeros(B, dtype=np.float32)
+    p = np.zeros(B, dtype=np.float64)
+    st = lib().gor_sample_owner_affine(strategy, _p(key), _p(seq), shard_cap, n_shards, n_ranks,
+                                       rank, B, seed, float(beta), _p(idx), _p(w), _p(p))
+    return st, idx, w, p
+
+
 def update(key: np.ndarray, gen: np.ndarray, frac_bits: int, idx, p, gen_in=None):
     """In-place on key.  Returns (status bitmask, n_stale)."""
     assert key.dtype == np.uint64 and gen.dtype == np.uint32
@@ -197,6 +212,6 @@ class Table:
     def update(self, idx, p, gen_in=None):
         return update(self.key, self.gen, self.F, idx, p, gen_in)
 
-    def sample(self, strategy, n_ranks, rank, B, seed, beta=0.0):
-        return sample(strategy, self.key, self.seq, self.cap, self.S, n_ranks, rank, B,
-                      seed, beta)
+    def sample(self, strategy, n_ranks, rank, B, seed, beta=0.0, owner_affine=False):
+        fn = sample_owner_affine if owner_affine else sample
+        return fn(strategy, self.key, self.seq, self.cap, self.S, n_ranks, rank, B, seed, beta)

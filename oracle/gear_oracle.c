@@ -201,6 +201,54 @@ int gor_sample(int strategy, const uint64_t* key, const uint64_t* seq,
   return GOR_OK;
 }
 
+/* Q19: owner-affine assignment of the global batch (see gear_oracle.h). */
+int gor_sample_owner_affine(int strategy, const uint64_t* key, const uint64_t* seq,
+                            uint64_t shard_cap, uint32_t n_shards, uint32_t n_ranks,
+                            uint32_t rank, uint32_t B, uint64_t seed, double beta,
+                            uint64_t* out_idx, float* out_w, double* out_p) {
+  if (n_ranks == 0 || rank >= n_ranks || n_shards % n_ranks) return GOR_INVALID;
+  if (B == 0) return GOR_OK;
+  uint64_t K = (uint64_t)n_ranks * B;
+  uint64_t* g = (uint64_t*)malloc(sizeof(uint64_t) * K);
+  double* p = (double*)malloc(sizeof(double) * K);
+  /* the global batch, in global order */
+  int st = gor_sample(strategy, key, seq, shard_cap, n_shards, 1, 0, (uint32_t)K, seed, beta,
+                      g, NULL, p);
+  if (st != GOR_OK) { free(g); free(p); return st; }
+  uint32_t R = n_shards / n_ranks;
+  uint64_t* count = (uint64_t*)calloc(n_ranks, sizeof(uint64_t));
+  for (uint64_t j = 0; j < K; ++j) count[(g[j] / shard_cap) / R] += 1;
+  uint64_t offset = 0;           /* overflow entries taken by ranks before `rank` */
+  for (uint32_t r = 0; r < rank; ++r) offset += count[r] < B ? B - count[r] : 0;
+  uint64_t need = count[rank] < B ? B - count[rank] : 0;
+  uint64_t* seen = (uint64_t*)calloc(n_ranks, sizeof(uint64_t));
+  uint64_t nown = 0, nover = 0, ov = 0;
+  uint64_t* own = (uint64_t*)malloc(sizeof(uint64_t) * B);
+  uint64_t* over = (uint64_t*)malloc(sizeof(uint64_t) * B);
+  for (uint64_t j = 0; j < K; ++j) {
+    uint32_t o = (uint32_t)((g[j] / shard_cap) / R);
+    uint64_t pos = seen[o]++;    /* position of j among its owner's entries */
+    if (pos < B) {
+      if (o == rank) own[nown++] = j;
+    } else {
+      if (ov >= offset && ov < offset + need) over[nover++] = j;
+      ++ov;
+    }
+  }
+  uint32_t b = 0;
+  for (uint64_t k = 0; k < nown; ++k, ++b) out_idx[b] = g[own[k]], out_p ? out_p[b] = p[own[k]] : 0;
+  for (uint64_t k = 0; k < nover; ++k, ++b) out_idx[b] = g[over[k]], out_p ? out_p[b] = p[over[k]] : 0;
+  if (out_w) {
+    uint64_t qmin = UINT64_MAX;
+    for (uint32_t k = 0; k < B; ++k) if (key[out_idx[k]] < qmin) qmin = key[out_idx[k]];
+    for (uint32_t k = 0; k < B; ++k)
+      out_w[k] = strategy == GOR_PRIORITIZED ? (float)pow((double)qmin / (double)key[out_idx[k]], beta)
+                                             : 1.0f;
+  }
+  free(g); free(p); free(count); free(seen); free(own); free(over);
+  return GOR_OK;
+}
+
 /* Q11: apply the list in order; the last valid writer of a slot wins. */
 int gor_update(uint64_t* key, const uint32_t* gen, uint64_t n_global,
                uint32_t frac_bits, uint32_t n, const uint64_t* idx, const double* p,

@@ -79,6 +79,22 @@ int gor_sample(int strategy, const uint64_t* key, const uint64_t* seq,
                uint32_t B, uint64_t seed, double beta,
                uint64_t* out_idx, float* out_w, double* out_p);
 
+/* Owner-affine assignment of the same global batch (reading Q19; data
+ * locality, "the majority of the trajectories collected by the
+ * servers reside in local memory").  The global batch of n_ranks*B entries
+ * (draws j = 0.. for UNIFORM/WEIGHTED/PRIORITIZED, merged order for
+ * FIFO/LIFO) is computed exactly as gor_sample with one rank; entry j is
+ * owned by rank (g_j / shard_cap) / (n_shards / n_ranks).  Rank r keeps its
+ * own entries in j order, at most B of them; the entries beyond B of
+ * over-full owners form an overflow list in j order, and under-full ranks
+ * take consecutive runs of it in rank order (rank r takes
+ * max(0, B - count_r) entries after those of ranks < r).  The slice is own
+ * entries then overflow entries; IS weights use q_min over that slice. */
+int gor_sample_owner_affine(int strategy, const uint64_t* key, const uint64_t* seq,
+                            uint64_t shard_cap, uint32_t n_shards, uint32_t n_ranks,
+                            uint32_t rank, uint32_t B, uint64_t seed, double beta,
+                            uint64_t* out_idx, float* out_w, double* out_p);
+
 /* Priority update, applied as the concatenation of every rank's list in
  * (rank, position) order, so the last writer wins (Q11).  Entries with an
  * out-of-range id, an invalid priority, a never-inserted slot (gen == 0) or

@@ -45,6 +45,7 @@ GEAR_U8, GEAR_I32, GEAR_I64, GEAR_F32, GEAR_F64, GEAR_BF16 = range(6)
 GEAR_DEVICE, GEAR_HOST = 0, 1
 GEAR_FIFO, GEAR_LIFO, GEAR_UNIFORM, GEAR_WEIGHTED, GEAR_PRIORITIZED = range(5)
 GEAR_REMOVE_FIFO, GEAR_REMOVE_LIFO = 0, 1
+GEAR_SAMPLE_OWNER_AFFINE = 0x100
 
 STRATEGIES = {"fifo": GEAR_FIFO, "lifo": GEAR_LIFO, "uniform": GEAR_UNIFORM,
               "weighted": GEAR_WEIGHTED, "prioritized": GEAR_PRIORITIZED}

@@ -143,6 +143,8 @@ void destroy_table(gear_table* t) {
   dfree(t->q_scratch); dfree(t->qmin_slot); dfree(t->done_ctr);
   dfree(t->tmp_idx); dfree(t->tmp_w); dfree(t->tmp_p); dfree(t->tmp_gen);
   dfree(t->cand_local); dfree(t->cand_all);
+  dfree(t->draw_list); dfree(t->pos_scratch); dfree(t->ov_scratch);
+  dfree(t->glob_shard); dfree(t->glob_slot);
   dfree(t->upd_local); dfree(t->upd_all); dfree(t->upd_idx); dfree(t->upd_prio); dfree(t->upd_gen);
   dfree(t->n_stale); dfree(t->err);
   dfree(t->col_idx.p);
@@ -350,6 +352,11 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_TRY(dalloc(&t->tmp_w, MB));
   GEAR_TRY(dalloc(&t->tmp_p, MB));
   GEAR_TRY(dalloc(&t->tmp_gen, MB));
+  GEAR_TRY(dalloc(&t->draw_list, MB));
+  GEAR_TRY(dalloc(&t->pos_scratch, K));
+  GEAR_TRY(dalloc(&t->ov_scratch, K));
+  GEAR_TRY(dalloc(&t->glob_shard, K));
+  GEAR_TRY(dalloc(&t->glob_slot, K));
   GEAR_TRY(dalloc(&t->cand_local, t->R * K));
   GEAR_TRY(dalloc(&t->cand_all, t->S * K));
   GEAR_TRY(dalloc(&t->upd_local, MB));
@@ -396,6 +403,22 @@ uint32_t vec_width(uint64_t rb, uint32_t chunk, std::initializer_list<uintptr_t>
     if (ok) return v;
   }
   return 1;
+}
+
+AssignParams assign_params(gear_table* t, uint32_t B, uint64_t seed) {
+  AssignParams ap{};
+  ap.n_shards = t->S;
+  ap.shards_per_rank = t->R;
+  ap.W = t->W;
+  ap.rank = t->rank;
+  ap.B = B;
+  ap.seed = seed;
+  ap.shard_cap = t->Cs;
+  ap.draw_list = t->draw_list;
+  ap.pos_scratch = t->pos_scratch;
+  ap.ov_scratch = t->ov_scratch;
+  ap.gen_ptrs = t->d_gen_ptrs;
+  return ap;
 }
 
 gear_status check_table(const gear_table* t) {
@@ -669,6 +692,8 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
   GEAR_TRY(check_table(t));
   GEAR_CUDA(cudaSetDevice(t->device));
   cudaStream_t s = (cudaStream_t)stream;
+  const bool affine = ((uint32_t)strategy & GEAR_SAMPLE_OWNER_AFFINE) != 0;
+  strategy = (gear_strategy)((uint32_t)strategy & ~(uint32_t)GEAR_SAMPLE_OWNER_AFFINE);
   if (strategy < GEAR_FIFO || strategy > GEAR_PRIORITIZED)
     return set_error(GEAR_ERR_INVALID_ARG, "bad strategy %d", (int)strategy);
   if (B > t->max_batch) return set_error(GEAR_ERR_INVALID_ARG, "B %u > max_batch %u", B, t->max_batch);
@@ -699,7 +724,20 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     GEAR_TRY(allgather_bytes(t->comm, t->fifo_totals_local, t->fifo_totals_all,
                              t->R * sizeof(ShardTotals), s));
     GEAR_CUDA(launch_fifo_merge(t->cand_all, t->fifo_totals_all, t->S, K, lifo, t->Cs, t->rank,
-                                B, t->d_gen_ptrs, t->R, d_idx, d_w, d_p, d_gen, t->err, s));
+                                B, t->d_gen_ptrs, t->R, d_idx, d_w, d_p, d_gen, t->err,
+                                affine ? t->glob_shard : nullptr, affine ? t->glob_slot : nullptr,
+                                s));
+    if (affine) {
+      AssignParams ap = assign_params(t, B, seed);
+      ap.fifo_totals = t->fifo_totals_all;
+      ap.glob_shard = t->glob_shard;
+      ap.glob_slot = t->glob_slot;
+      ap.out_idx = d_idx;
+      ap.out_w = d_w;
+      ap.out_p = d_p;
+      ap.out_gen = d_gen;
+      GEAR_CUDA(launch_assign(ap, s));
+    }
   } else {
     const int mode = strategy == GEAR_UNIFORM ? 1 : 0;
     if (t->dirty || t->cdf_mode != mode) {
@@ -737,6 +775,12 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     sp.qmin_slot = t->qmin_slot;
     sp.done_ctr = t->done_ctr;
     sp.err = t->err;
+    if (affine) {
+      AssignParams ap = assign_params(t, B, seed);
+      ap.totals = t->cdf_totals_all;
+      GEAR_CUDA(launch_assign(ap, s));
+      sp.draw_list = t->draw_list;
+    }
     GEAR_CUDA(launch_sample(sp, s));
   }
   if (h_idx) GEAR_CUDA(cudaMemcpyAsync(out_idx, d_idx, B * 8ull, cudaMemcpyDeviceToHost, s));

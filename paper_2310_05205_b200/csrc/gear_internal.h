@@ -127,10 +127,34 @@ struct SampleParams {
   float* out_w;
   double* out_p;
   uint32_t* out_gen;
+  const uint32_t* draw_list;          // [B] draw numbers j of the slice, or null: rank*B + b
   uint64_t* q_scratch;                // [B]
   unsigned long long* qmin_slot;      // reset to ~0 by the last block
   uint32_t* done_ctr;                 // reset to 0 by the last block
   uint32_t* err;
+};
+
+// Owner-affine assignment of the global batch (kernels/assign.cu).
+struct AssignParams {
+  const ShardTotals* totals;        // draws: CDF totals [S] (null for FIFO/LIFO)
+  const ShardTotals* fifo_totals;   // FIFO/LIFO: candidate counts [S] (null for draws)
+  const uint32_t* glob_shard;       // FIFO/LIFO merged global list [K] (null for draws)
+  const uint32_t* glob_slot;
+  uint32_t n_shards;
+  uint32_t shards_per_rank;
+  uint32_t W;
+  uint32_t rank;
+  uint32_t B;
+  uint64_t seed;
+  uint64_t shard_cap;
+  uint32_t* draw_list;              // [B] out: global entry j of each slice position
+  uint32_t* pos_scratch;            // [K]
+  uint32_t* ov_scratch;             // [K]
+  uint64_t* out_idx;                // FIFO/LIFO outputs (written by the assign kernel)
+  float* out_w;
+  double* out_p;
+  uint32_t* out_gen;
+  const uint32_t* const* gen_ptrs;
 };
 
 // ---- kernel launchers (kernels/*.cu) --------------------------------------
@@ -192,10 +216,14 @@ cudaError_t launch_fifo_local(const uint64_t* key, const uint64_t* seq, const ui
                               const FifoRings& rings, uint64_t shard_cap,
                               uint32_t n_shards_local, uint32_t first_shard, uint32_t K,
                               int lifo, Cand* cand_out, ShardTotals* totals_out, cudaStream_t s);
+// glob_shard != null: write the whole merged list (glob_shard/glob_slot[K])
+// for the owner-affine assignment instead of this rank's slice.
 cudaError_t launch_fifo_merge(const Cand* cand_all, const ShardTotals* totals_all,
                               uint32_t n_shards, uint32_t K, int lifo, uint64_t shard_cap,
                               uint32_t rank, uint32_t B, const uint32_t* const* gen_ptrs,
                               uint32_t shards_per_rank, uint64_t* out_idx, float* out_w,
-                              double* out_p, uint32_t* out_gen, uint32_t* err, cudaStream_t s);
+                              double* out_p, uint32_t* out_gen, uint32_t* err,
+                              uint32_t* glob_shard, uint32_t* glob_slot, cudaStream_t s);
+cudaError_t launch_assign(const AssignParams& p, cudaStream_t s);
 
 }  // namespace gear

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kMergeThreads)
                       uint32_t S, uint32_t K, int lifo, uint64_t shard_cap, uint32_t rank,
                       uint32_t B, const uint32_t* const* gen_ptrs, uint32_t shards_per_rank,
                       uint64_t* out_idx, float* out_w, double* out_p, uint32_t* out_gen,
-                      uint32_t* err) {
+                      uint32_t* err, uint32_t* glob_shard, uint32_t* glob_slot) {
   const uint64_t t = (uint64_t)blockIdx.x * kMergeThreads + threadIdx.x;
   uint64_t avail = 0;
   for (uint32_t s = 0; s < S; ++s) avail += totals[s].aux;
@@ -123,6 +123,13 @@ __global__ void __launch_bounds__(kMergeThreads)
     if (s2 == s) continue;
     pos += count_before(cand_all + (uint64_t)s2 * K, (uint32_t)totals[s2].aux, s2, me.seq, s,
                         lifo);
+  }
+  if (glob_shard) {  // whole merged list for the owner-affine assignment
+    if (pos < K) {
+      glob_shard[pos] = me.shard;
+      glob_slot[pos] = me.slot;
+    }
+    return;
   }
   const uint64_t lo = (uint64_t)rank * B;
   if (pos < lo || pos >= lo + B) return;
@@ -153,14 +160,16 @@ cudaError_t launch_fifo_merge(const Cand* cand_all, const ShardTotals* totals_al
                               uint32_t n_shards, uint32_t K, int lifo, uint64_t shard_cap,
                               uint32_t rank, uint32_t B, const uint32_t* const* gen_ptrs,
                               uint32_t shards_per_rank, uint64_t* out_idx, float* out_w,
-                              double* out_p, uint32_t* out_gen, uint32_t* err, cudaStream_t s) {
+                              double* out_p, uint32_t* out_gen, uint32_t* err,
+                              uint32_t* glob_shard, uint32_t* glob_slot, cudaStream_t s) {
   const uint64_t n = (uint64_t)n_shards * K;
   const uint64_t threads = n > B ? n : B;
   const uint32_t grid = (uint32_t)((threads + kMergeThreads - 1) / kMergeThreads);
   count_launch();
   fifo_merge_kernel<<<grid, kMergeThreads, 0, s>>>(cand_all, totals_all, n_shards, K, lifo,
                                                    shard_cap, rank, B, gen_ptrs, shards_per_rank,
-                                                   out_idx, out_w, out_p, out_gen, err);
+                                                   out_idx, out_w, out_p, out_gen, err,
+                                                   glob_shard, glob_slot);
   return cudaGetLastError();
 }
 

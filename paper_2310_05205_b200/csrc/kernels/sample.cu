@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
 
   uint64_t my_q = ~0ull;
   if (b < p.B) {
-    const uint64_t j = (uint64_t)p.rank * p.B + b;
+    const uint64_t j = p.draw_list ? (uint64_t)p.draw_list[b] : (uint64_t)p.rank * p.B + b;
     uint64_t g = kIdxNone, q = 0;
     if (T > 0) {
       const uint64_t r = draw_bits(p.seed, j);

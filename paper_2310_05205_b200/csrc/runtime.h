@@ -126,6 +126,11 @@ struct gear_table {
   float* tmp_w = nullptr;
   double* tmp_p = nullptr;
   uint32_t* tmp_gen = nullptr;
+  uint32_t* draw_list = nullptr;     // [max_batch] owner-affine slice -> draw number
+  uint32_t* pos_scratch = nullptr;   // [W*max_batch]
+  uint32_t* ov_scratch = nullptr;    // [W*max_batch]
+  uint32_t* glob_shard = nullptr;    // [W*max_batch] merged FIFO/LIFO list
+  uint32_t* glob_slot = nullptr;
   gear::Cand* cand_local = nullptr;  // [R * W*max_batch]
   gear::Cand* cand_all = nullptr;    // [S * W*max_batch]
 

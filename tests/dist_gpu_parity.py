@@ -88,6 +88,20 @@ def run_case(comm, W, rank, R, placements, removal, Cs=700, B=40, steps=3):
                 assert np.array_equal(outs[c].cpu().numpy(), want), f"collect column {c}"
             err, _ = t.sync()
             assert err == 0, err
+            # owner-affine assignment of the same global batch (reading Q19)
+            ia = torch.empty(B, dtype=torch.int64, device="cuda")
+            wa = torch.empty(B, dtype=torch.float32, device="cuda")
+            t.sample(strat | gear.GEAR_SAMPLE_OWNER_AFFINE, B, seed, 0.4, ia, wa)
+            torch.cuda.synchronize()
+            st, oa, owa, _ = o.sample(OS[strat], W, rank, B, seed, 0.4, owner_affine=True)
+            ga = ia.cpu().numpy().view(np.uint64)
+            assert st == 0 and np.array_equal(ga, oa), f"strategy {strat}: owner-affine ids differ"
+            np.testing.assert_allclose(wa.cpu().numpy(), owa, rtol=1e-6)
+            t.collect(ia, list(range(len(cols))), outs)
+            torch.cuda.synchronize()
+            for c in range(len(cols)):
+                want = synth.row_bytes_of(c, content[oa.astype(np.int64)], rb[c])
+                assert np.array_equal(outs[c].cpu().numpy(), want), f"affine collect column {c}"
         # collective update: every rank updates its own sampled ids
         newp = np.random.default_rng(1000 * step + rank).lognormal(0, 1, B)
         newp[:3] = 0.0

@@ -225,6 +225,21 @@ def test_host_buffers_through_abi(torch_cuda):
     P.close()
 
 
+def test_owner_affine_single_rank_is_identity(torch_cuda):
+    """With one rank every entry is local: the owner-affine slice equals the
+    contiguous one (the W>1 cases run in dist_gpu_parity.py)."""
+    P = _pair(capacity=C1.capacity, seq_len=C1.seq_len, colspecs=C1.cols, R=4)
+    P.fill(synth.priorities(C1.capacity, seed=6, zero_frac=0.1))
+    for strat in (G.GEAR_UNIFORM, G.GEAR_WEIGHTED, G.GEAR_PRIORITIZED, G.GEAR_FIFO, G.GEAR_LIFO):
+        a = P.sample_gpu(strat, 64, 17, 0.4)
+        b = P.sample_gpu(strat | G.GEAR_SAMPLE_OWNER_AFFINE, 64, 17, 0.4)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+        from gpu_harness import ORACLE_STRATEGY
+        st, oi, ow, _ = P.o.sample(ORACLE_STRATEGY[strat], 1, 0, 64, 17, 0.4, owner_affine=True)
+        assert st == 0 and np.array_equal(b[0], oi)
+    P.close()
+
+
 def test_deterministic_across_repeats_and_beta(torch_cuda):
     P = _pair(capacity=C1.capacity, seq_len=C1.seq_len, colspecs=C1.cols, R=4)
     P.fill(synth.priorities(C1.capacity, seed=5))

@@ -414,3 +414,37 @@ def test_translate_round_trip(oracle_mod):
         g = int(rng.integers(0, 1 << 62))
         s, i = oracle_mod.translate(g, cap)
         assert s * cap + i == g and 0 <= i < cap
+
+
+# --------------------------------------------------------------------------
+# Owner-affine assignment (reading Q19): properties, not the formula
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("strategy", [2, 3, 4, 0, 1])
+def test_owner_affine_partitions_the_global_batch(oracle_mod, strategy):
+    rng = np.random.default_rng(30 + strategy)
+    for W, R in ((1, 1), (2, 1), (4, 2), (8, 1), (3, 2)):
+        S, Cs, B = W * R, 50, 37
+        t = oracle_mod.Table(Cs, S)
+        for s in range(S):
+            t.insert(s, rng.lognormal(0, 1.5, Cs) * (rng.random(Cs) > 0.1) * (1 + 3 * (s % 2)))
+        K = W * B
+        st, glob, _, gp = t.sample(strategy, 1, 0, K, seed=99, beta=0.5)
+        assert st == 0
+        owners = (glob // np.uint64(Cs)) // np.uint64(R)
+        slices = []
+        for r in range(W):
+            st, idx, w, p = t.sample(strategy, W, r, B, 99, 0.5, owner_affine=True)
+            assert st == 0 and idx.size == B
+            own = int(np.sum(owners == r))
+            # the rank keeps min(B, own) of its own entries, first, in global order
+            k = min(B, own)
+            assert np.array_equal(idx[:k], glob[owners == r][:k])
+            assert np.all((idx[k:] // np.uint64(Cs)) // np.uint64(R) != r) or own >= B
+            if strategy == 4:
+                q = t.key[idx.astype(np.int64)]
+                assert np.all(w[q == q.min()] == 1.0) and np.all(w <= 1.0)
+            slices.append(idx)
+        # together the ranks receive exactly the global batch (as a multiset)
+        assert sorted(np.concatenate(slices).tolist()) == sorted(glob.tolist())
+        if W == 1:
+            assert np.array_equal(slices[0], glob)
