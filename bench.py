@@ -94,17 +94,19 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- workload
 def scaled_capacity(cfg, n_ranks: int) -> tuple[int, str]:
-    """Host-resident tables are scaled to fit 60% of this box's RAM."""
+    """Host-resident tables are scaled to fit this box's RAM: 60% at N=1,
+    40% at N>1 (every rank registers every rank's shared host shard)."""
     import synth
     host_rb = sum(synth.row_bytes(cfg, c) for c in cfg.cols if c.placement == "host")
     N = cfg.capacity
     note = ""
     if host_rb:
         mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
-        fit = int(0.6 * mem) // host_rb
+        frac = 0.6 if n_ranks == 1 else 0.4
+        fit = int(frac * mem) // host_rb
         if fit < N:
             N = max(n_ranks * 1024, (fit // (n_ranks * 1024)) * n_ranks * 1024)
-            note = f"capacity scaled {cfg.capacity} -> {N} to fit 60% of {mem >> 30} GiB host RAM"
+            note = f"capacity scaled {cfg.capacity} -> {N} to fit {int(frac * 100)}% of {mem >> 30} GiB host RAM"
     N -= N % n_ranks
     return N, note
 
@@ -153,6 +155,10 @@ def run_gpu(args):
     gear.load()
     comm = gear.comm_from_torch_distributed(local) if world > 1 else None
     cfg = synth.CONFIGS[args.config]
+    if args.strategy:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, strategy=args.strategy,
+                                  update=cfg.update and args.strategy == "prioritized")
     capacity, cap_note = scaled_capacity(cfg, world)
     stream = torch.cuda.Stream()
     t, prio_all = build_table(cfg, comm, world, rank, capacity, stream)
@@ -429,6 +435,9 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--strategy", default=None,
+                    choices=["fifo", "lifo", "uniform", "weighted", "prioritized"],
+                    help="override the config's strategy")
     ap.add_argument("--assign", default="owner", choices=["owner", "contiguous"],
                     help="owner-affine (DESIGN.md Q19) or contiguous rank slices of the global batch")
     ap.add_argument("--impl", default="gear", choices=["gear", "reference"])

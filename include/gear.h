@@ -61,6 +61,7 @@ typedef int32_t gear_status;
 #define GEAR_DEVERR_BAD_PRIORITY 2u /* an update priority was NaN/inf/negative */
 #define GEAR_DEVERR_STALE 4u        /* an update hit a never-inserted slot or a stale generation */
 #define GEAR_DEVERR_EMPTY 8u        /* a sample found nothing (or < W*B for FIFO/LIFO) selectable */
+#define GEAR_DEVERR_TIMEOUT 16u     /* a peer-mailbox exchange waited > 4 s for a peer (SPMD broken) */
 
 /* Padding id: update entries with this id are ignored (lets ranks with fewer
  * updates pass the common n of a collective update). */
@@ -263,6 +264,10 @@ gear_status gear_table_sync(gear_table* t, uint32_t* dev_errors, uint64_t* n_sta
  *   "tma_ctas_per_sm": TMA CTAs per SM (default 2), "tma_stages": stages per
  *                   CTA (2, 3, 4, 6, 8; default 3); ctas * stages * tma_chunk
  *                   must stay <= 220 KB (set the smaller knob first);
+ *   "peer_xchg":    W > 1 only, same value on every rank: 1 = the per-step
+ *                   exchanges (shard totals, update records, FIFO/LIFO
+ *                   candidates) are NVLink stores into the peers' mailboxes
+ *                   inside the step's kernels (default), 0 = NCCL all-gathers;
  *   "update_fused": 1 = priority updates of <= 8192 entries (all ranks) run
  *                   tag + apply in one single-CTA launch (default), 0 = two
  *                   grid-wide launches.

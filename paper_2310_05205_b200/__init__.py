@@ -38,6 +38,7 @@ GEAR_DEVERR_INDEX_RANGE = 1
 GEAR_DEVERR_BAD_PRIORITY = 2
 GEAR_DEVERR_STALE = 4
 GEAR_DEVERR_EMPTY = 8
+GEAR_DEVERR_TIMEOUT = 16
 GEAR_IDX_NONE = 0xFFFFFFFFFFFFFFFF
 
 # dtypes / placements / strategies / removal (gear.h enums)

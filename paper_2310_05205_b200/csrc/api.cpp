@@ -133,6 +133,8 @@ void destroy_table(gear_table* t) {
     if (c.placement == GEAR_DEVICE && c.local) cudaFree(c.local);
   }
   for (void* p : t->ipc_opened) cudaIpcCloseMemHandle(p);
+  for (void* p : t->mbox_opened) cudaIpcCloseMemHandle(p);
+  dfree(t->mbox);
   dfree(t->key); dfree(t->seq); dfree(t->gen); dfree(t->tag); dfree(t->ord);
   for (int i = 0; i < 2; ++i) {
     dfree(t->cdf[i]); dfree(t->scan_status[i]); dfree(t->scan_ticket[i]);
@@ -341,6 +343,23 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_CUDA(cudaMemcpy(t->d_cdf_ptrs, cdf_ptrs.data(), 2 * t->S * sizeof(void*), cudaMemcpyHostToDevice));
   GEAR_CUDA(cudaMemcpy(t->d_gen_ptrs, gen_ptrs.data(), t->W * sizeof(void*), cudaMemcpyHostToDevice));
 
+  // Peer mailboxes for the per-step exchanges (W > 1), mapped by every rank.
+  if (t->W > 1) {
+    const MboxLayout L = mbox_layout(t->W, t->S, t->max_batch);
+    GEAR_TRY(dalloc(&t->mbox, L.bytes));
+    GEAR_CUDA(cudaMemset(t->mbox, 0, L.bytes));
+    void* views[kMaxRanks] = {};
+    GEAR_TRY(exchange_ipc(t, t->mbox, views, t->mbox_opened));
+    for (uint32_t r = 0; r < t->W; ++r) t->mb.base[r] = (uint8_t*)views[r];
+    t->mb.W = t->W;
+    t->mb.rank = t->rank;
+    t->mb.S = t->S;
+    t->mb.R = t->R;
+    t->mb.MB = t->max_batch;
+    GEAR_CUDA(cudaDeviceSynchronize());
+    GEAR_TRY(barrier(comm));  // every mailbox is zeroed before anyone writes
+  }
+
   // Scratch.
   const uint64_t MB = t->max_batch, K = (uint64_t)t->W * MB;
   GEAR_TRY(dalloc(&t->q_scratch, MB));
@@ -418,6 +437,7 @@ AssignParams assign_params(gear_table* t, uint32_t B, uint64_t seed) {
   ap.pos_scratch = t->pos_scratch;
   ap.ov_scratch = t->ov_scratch;
   ap.gen_ptrs = t->d_gen_ptrs;
+  ap.err = t->err;
   return ap;
 }
 
@@ -660,6 +680,14 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
     GEAR_CUDA(launch_update_fused(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, nullptr, n, t->N,
                                   t->F, t->qmax, local_begin, t->Clocal, t->gen, t->tag, t->epoch,
                                   t->n_stale, t->err, t->key, s));
+  } else if (t->W > 1 && fused && t->peer_xchg) {
+    // one launch: quantise, push records to every peer over NVLink, wait for
+    // every rank's records, tag, barrier, apply
+    Mbox mb = t->mb;
+    mb.epoch = ++t->ep_upd;
+    GEAR_CUDA(launch_update_xchg(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N, t->F,
+                                 t->qmax, mb, local_begin, t->Clocal, t->gen, t->tag, t->epoch,
+                                 t->n_stale, t->err, t->key, s));
   } else {
     GEAR_CUDA(launch_update_quantize(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N, t->F,
                                      t->qmax, t->upd_local, t->err, s));
@@ -718,18 +746,32 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
       rings.len[ls] = t->rings[ls].len;
     }
     const int lifo = strategy == GEAR_LIFO;
+    const bool xchg = t->W > 1 && t->peer_xchg;
+    Mbox mb = t->mb;
+    const ShardTotals* fifo_totals = t->fifo_totals_all;
+    if (xchg) {
+      // candidates go straight into every peer's mailbox from the local kernel
+      mb.epoch = ++t->ep_fifo;
+      const MboxLayout L = mbox_layout(t->W, t->S, t->max_batch);
+      fifo_totals = reinterpret_cast<const ShardTotals*>(t->mb.base[t->rank] + L.ccnt) +
+                    (mb.epoch & 1) * t->S;
+    }
     GEAR_CUDA(launch_fifo_local(t->key, t->seq, t->ord, rings, t->Cs, t->R, t->rank * t->R, K,
-                                lifo, t->cand_local, t->fifo_totals_local, s));
-    GEAR_TRY(allgather_bytes(t->comm, t->cand_local, t->cand_all, (size_t)t->R * K * sizeof(Cand), s));
-    GEAR_TRY(allgather_bytes(t->comm, t->fifo_totals_local, t->fifo_totals_all,
-                             t->R * sizeof(ShardTotals), s));
+                                lifo, t->cand_local, t->fifo_totals_local, xchg ? &mb : nullptr,
+                                s));
+    if (!xchg) {
+      GEAR_TRY(allgather_bytes(t->comm, t->cand_local, t->cand_all,
+                               (size_t)t->R * K * sizeof(Cand), s));
+      GEAR_TRY(allgather_bytes(t->comm, t->fifo_totals_local, t->fifo_totals_all,
+                               t->R * sizeof(ShardTotals), s));
+    }
     GEAR_CUDA(launch_fifo_merge(t->cand_all, t->fifo_totals_all, t->S, K, lifo, t->Cs, t->rank,
                                 B, t->d_gen_ptrs, t->R, d_idx, d_w, d_p, d_gen, t->err,
                                 affine ? t->glob_shard : nullptr, affine ? t->glob_slot : nullptr,
-                                s));
+                                xchg ? &mb : nullptr, s));
     if (affine) {
       AssignParams ap = assign_params(t, B, seed);
-      ap.fifo_totals = t->fifo_totals_all;
+      ap.fifo_totals = fifo_totals;
       ap.glob_shard = t->glob_shard;
       ap.glob_slot = t->glob_slot;
       ap.out_idx = d_idx;
@@ -751,12 +793,28 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
       t->cdf_mode = mode;
       t->dirty = false;
     }
-    // Every step publishes the totals; the all-gather is also the barrier
-    // that makes every shard's CDF visible before anyone searches it.
-    GEAR_TRY(allgather_bytes(t->comm, t->cdf_totals_local, t->cdf_totals_all,
-                             t->R * sizeof(ShardTotals), s));
+    // Every step publishes the totals; the exchange is also the barrier that
+    // makes every shard's CDF visible before anyone searches it.  W > 1: the
+    // first kernel of the step (assign or sample) pushes this rank's totals
+    // into every peer's mailbox over NVLink and waits for all of them;
+    // otherwise an NCCL all-gather (or a copy at W = 1).
+    const bool xchg = t->W > 1 && t->peer_xchg;
+    Mbox mb = t->mb;
+    const ShardTotals* totals_all = t->cdf_totals_all;
+    if (xchg) {
+      mb.epoch = ++t->ep_totals;
+      const MboxLayout L = mbox_layout(t->W, t->S, t->max_batch);
+      totals_all = reinterpret_cast<const ShardTotals*>(t->mb.base[t->rank] + L.totals) +
+                   (mb.epoch & 1) * t->S;
+    } else {
+      GEAR_TRY(allgather_bytes(t->comm, t->cdf_totals_local, t->cdf_totals_all,
+                               t->R * sizeof(ShardTotals), s));
+    }
     SampleParams sp{};
-    sp.totals = t->cdf_totals_all;
+    sp.totals = totals_all;
+    sp.totals_local = t->cdf_totals_local;
+    sp.mbox = mb;
+    sp.xchg = xchg && !affine;
     sp.cdf_ptrs = t->d_cdf_ptrs;
     sp.gen_ptrs = t->d_gen_ptrs;
     sp.shard_cap = t->Cs;
@@ -777,7 +835,10 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     sp.err = t->err;
     if (affine) {
       AssignParams ap = assign_params(t, B, seed);
-      ap.totals = t->cdf_totals_all;
+      ap.totals = totals_all;
+      ap.totals_local = t->cdf_totals_local;
+      ap.mbox = mb;
+      ap.xchg = xchg;
       GEAR_CUDA(launch_assign(ap, s));
       sp.draw_list = t->draw_list;
     }
@@ -876,6 +937,8 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     t->collect_impl = (int)value;
   } else if (!strcmp(key, "lsu_chunk") && value >= 512 && value % 512 == 0 && value <= (1 << 20)) {
     t->chunk_bytes = (uint32_t)value;
+  } else if (!strcmp(key, "peer_xchg") && (value == 0 || value == 1)) {
+    t->peer_xchg = (int)value;  // must be set identically on every rank
   } else if (!strcmp(key, "update_fused") && (value == 0 || value == 1)) {
     t->update_fused = (int)value;
   } else if (!strcmp(key, "tma_ctas_per_sm") && value >= 1 && value <= 8 &&

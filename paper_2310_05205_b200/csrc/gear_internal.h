@@ -20,6 +20,8 @@ constexpr uint32_t kErrBadPriority = 2u;
 constexpr uint32_t kErrStale = 4u;
 constexpr uint32_t kErrEmpty = 8u;
 
+constexpr uint32_t kErrTimeout = 16u;
+
 // Strategy codes (mirror gear_strategy).
 constexpr int kFifo = 0, kLifo = 1, kUniform = 2, kWeighted = 3, kPrioritized = 4;
 
@@ -61,6 +63,45 @@ struct Cand {
   uint64_t seq;
   uint32_t shard;
   uint32_t slot;  // shard-local slot
+};
+
+// Peer mailboxes (W > 1).  Every rank owns one device allocation that all
+// peers map through CUDA IPC and write over NVLink; the small per-step
+// exchanges (shard totals, update records, FIFO/LIFO candidates) are remote
+// stores + a release flag carrying the exchange's epoch, consumed in place by
+// the next kernel -- no NCCL launch on the step.  Two buffers (epoch & 1)
+// alternate: a peer can only be one exchange ahead.
+struct MboxLayout {
+  uint64_t totals;  // ShardTotals [2][S]
+  uint64_t tflag;   // u64 [2][W]
+  uint64_t upd;     // UpdRec [2][W][MB]
+  uint64_t uflag;   // u64 [2][W]
+  uint64_t cand;    // Cand [2][S][K], K = W*MB
+  uint64_t ccnt;    // ShardTotals [2][S] (aux = candidate count)
+  uint64_t cflag;   // u64 [2][S]
+  uint64_t bytes;
+};
+
+__host__ __device__ inline MboxLayout mbox_layout(uint32_t W, uint32_t S, uint32_t MB) {
+  MboxLayout l;
+  const uint64_t K = (uint64_t)W * MB;
+  uint64_t o = 0;
+  l.totals = o; o += 2ull * S * sizeof(ShardTotals);
+  l.tflag = o;  o += 2ull * W * 8;
+  l.upd = o;    o += 2ull * W * MB * sizeof(UpdRec);
+  l.uflag = o;  o += 2ull * W * 8;
+  l.cand = o;   o += 2ull * S * K * sizeof(Cand);
+  l.ccnt = o;   o += 2ull * S * sizeof(ShardTotals);
+  l.cflag = o;  o += 2ull * S * 8;
+  l.bytes = (o + 255) & ~255ull;
+  return l;
+}
+
+// Kernel-parameter view of every rank's mailbox.
+struct Mbox {
+  uint8_t* base[kMaxRanks];  // base[rank] is this rank's own mailbox
+  uint32_t W, rank, S, R, MB;
+  uint64_t epoch;            // this exchange's epoch (>= 1), buffer = epoch & 1
 };
 
 struct CollectCol {
@@ -112,7 +153,10 @@ struct ScatterParams {
 };
 
 struct SampleParams {
-  const ShardTotals* totals;          // [S]
+  const ShardTotals* totals;          // [S] (ignored when xchg: taken from the mailbox)
+  const ShardTotals* totals_local;    // [R] this rank's totals (xchg)
+  Mbox mbox;
+  int xchg;                           // 1: exchange the totals through the mailboxes first
   const uint64_t* const* cdf_ptrs;    // [2*S]: parity p of shard s at [p*S + s]
   const uint32_t* const* gen_ptrs;    // [W]: each rank's gen array
   uint64_t shard_cap;                 // C_s
@@ -137,6 +181,9 @@ struct SampleParams {
 // Owner-affine assignment of the global batch (kernels/assign.cu).
 struct AssignParams {
   const ShardTotals* totals;        // draws: CDF totals [S] (null for FIFO/LIFO)
+  const ShardTotals* totals_local;  // draws with xchg: this rank's [R] totals
+  Mbox mbox;
+  int xchg;                         // 1: exchange the totals through the mailboxes first
   const ShardTotals* fifo_totals;   // FIFO/LIFO: candidate counts [S] (null for draws)
   const uint32_t* glob_shard;       // FIFO/LIFO merged global list [K] (null for draws)
   const uint32_t* glob_slot;
@@ -155,6 +202,7 @@ struct AssignParams {
   double* out_p;
   uint32_t* out_gen;
   const uint32_t* const* gen_ptrs;
+  uint32_t* err;
 };
 
 // ---- kernel launchers (kernels/*.cu) --------------------------------------
@@ -199,6 +247,16 @@ cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_
                                 unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                 cudaStream_t s);
 
+// W > 1 collective update through the peer mailboxes, one launch (n*W <=
+// update_fused_max()).
+cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_is_f64,
+                               const uint32_t* gen_in, uint32_t n, uint64_t n_global,
+                               uint32_t frac_bits, uint64_t q_max, const Mbox& mb,
+                               uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
+                               unsigned long long* tag, uint32_t epoch,
+                               unsigned long long* n_stale, uint32_t* err, uint64_t* key,
+                               cudaStream_t s);
+
 // K5: collect (gather) and the insert-side scatter.
 cudaError_t launch_collect(const CollectParams& p, cudaStream_t s);
 cudaError_t launch_scatter(const ScatterParams& p, cudaStream_t s);
@@ -215,7 +273,8 @@ struct FifoRings {
 cudaError_t launch_fifo_local(const uint64_t* key, const uint64_t* seq, const uint32_t* ord,
                               const FifoRings& rings, uint64_t shard_cap,
                               uint32_t n_shards_local, uint32_t first_shard, uint32_t K,
-                              int lifo, Cand* cand_out, ShardTotals* totals_out, cudaStream_t s);
+                              int lifo, Cand* cand_out, ShardTotals* totals_out,
+                              const Mbox* mbox, cudaStream_t s);
 // glob_shard != null: write the whole merged list (glob_shard/glob_slot[K])
 // for the owner-affine assignment instead of this rank's slice.
 cudaError_t launch_fifo_merge(const Cand* cand_all, const ShardTotals* totals_all,
@@ -223,7 +282,8 @@ cudaError_t launch_fifo_merge(const Cand* cand_all, const ShardTotals* totals_al
                               uint32_t rank, uint32_t B, const uint32_t* const* gen_ptrs,
                               uint32_t shards_per_rank, uint64_t* out_idx, float* out_w,
                               double* out_p, uint32_t* out_gen, uint32_t* err,
-                              uint32_t* glob_shard, uint32_t* glob_slot, cudaStream_t s);
+                              uint32_t* glob_shard, uint32_t* glob_slot, const Mbox* mbox,
+                              cudaStream_t s);
 cudaError_t launch_assign(const AssignParams& p, cudaStream_t s);
 
 }  // namespace gear

@@ -14,7 +14,7 @@
 //
 // One CTA of 1024 threads; K = W*B <= 8*4096 entries are walked in chunks of
 // 1024 with a per-owner ballot scan (W <= 8 owners).
-#include "common.cuh"
+#include "mbox.cuh"
 
 namespace gear {
 
@@ -32,9 +32,14 @@ __global__ void __launch_bounds__(kThreads) assign_kernel(const __grid_constant_
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t W = p.W, B = p.B, K = W * B;
   const uint32_t S = p.n_shards;
+  // W > 1 draws: exchange the shard totals through the peer mailboxes here;
+  // the sample kernel that follows reads them from this rank's mailbox.
+  const ShardTotals* totals =
+      p.xchg ? mbox_exchange_totals(p.mbox, p.totals_local, p.err) : p.totals;
   if (tid < 32) {
     uint64_t Ts = 0;
-    if ((uint32_t)lane < S && p.totals) Ts = p.totals[lane].total_and_parity & ((1ull << 62) - 1);
+    if ((uint32_t)lane < S && totals)
+      Ts = __ldcg(&totals[lane].total_and_parity) & ((1ull << 62) - 1);
     const uint64_t G = warp_incl_scan_u64(Ts, lane);
     if ((uint32_t)lane < S) s_G[lane] = G;
     if (lane == 31) s_T = G;

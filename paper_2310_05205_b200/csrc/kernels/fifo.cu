@@ -12,7 +12,7 @@
 // is its position in its own (sorted) list plus, for every other list, the
 // number of entries that order before it under (seq, shard) -- a binary
 // search per list.  Rank r keeps positions [r*B, (r+1)*B).
-#include "common.cuh"
+#include "mbox.cuh"
 
 namespace gear {
 
@@ -25,7 +25,8 @@ __global__ void __launch_bounds__(kLocalThreads)
     fifo_local_kernel(const uint64_t* __restrict__ key, const uint64_t* __restrict__ seq,
                       const uint32_t* __restrict__ ord, const __grid_constant__ FifoRings rings,
                       uint64_t shard_cap, uint32_t first_shard, uint32_t K, int lifo,
-                      Cand* __restrict__ cand_out, ShardTotals* __restrict__ totals_out) {
+                      Cand* __restrict__ cand_out, ShardTotals* __restrict__ totals_out,
+                      const __grid_constant__ Mbox m, int xchg) {
   __shared__ uint32_t s_warp[kLocalThreads / 32];
   __shared__ uint32_t s_count;
   const uint32_t ls = blockIdx.x;
@@ -75,6 +76,29 @@ __global__ void __launch_bounds__(kLocalThreads)
     t.aux = s_count < K ? s_count : K;
     totals_out[ls] = t;
   }
+  if (!xchg) return;
+  // W > 1: push this shard's candidates and count into every peer's mailbox
+  // over NVLink, then release the shard's flag there (mbox.cuh).
+  __syncthreads();
+  const MboxLayout L = mbox_layout(m.W, m.S, m.MB);
+  const uint32_t b = mbox_buf(m), shard = first_shard + ls;
+  const uint32_t n = s_count < K ? s_count : K;
+  for (uint32_t r = 0; r < m.W; ++r) {
+    Cand* dst = mbox_at<Cand>(m, r, L.cand) + ((uint64_t)b * m.S + shard) * K;
+    for (uint32_t i = tid; i < n; i += kLocalThreads) dst[i] = out[i];
+    if (tid == 0) {
+      ShardTotals t;
+      t.total_and_parity = 0;
+      t.aux = n;
+      mbox_at<ShardTotals>(m, r, L.ccnt)[b * m.S + shard] = t;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    for (uint32_t r = 0; r < m.W; ++r)
+      st_release_sys_u64(mbox_at<uint64_t>(m, r, L.cflag) + b * m.S + shard, m.epoch);
+  }
 }
 
 // Number of entries of the sorted list c[0..n) that order before (sq, s)
@@ -100,8 +124,18 @@ __global__ void __launch_bounds__(kMergeThreads)
                       uint32_t S, uint32_t K, int lifo, uint64_t shard_cap, uint32_t rank,
                       uint32_t B, const uint32_t* const* gen_ptrs, uint32_t shards_per_rank,
                       uint64_t* out_idx, float* out_w, double* out_p, uint32_t* out_gen,
-                      uint32_t* err, uint32_t* glob_shard, uint32_t* glob_slot) {
+                      uint32_t* err, uint32_t* glob_shard, uint32_t* glob_slot,
+                      const __grid_constant__ Mbox m, int xchg) {
   const uint64_t t = (uint64_t)blockIdx.x * kMergeThreads + threadIdx.x;
+  if (xchg) {  // candidates of all S shards arrive in this rank's mailbox
+    const MboxLayout L = mbox_layout(m.W, m.S, m.MB);
+    const uint32_t b = mbox_buf(m);
+    if (threadIdx.x == 0)
+      mbox_wait(mbox_at<uint64_t>(m, m.rank, L.cflag) + b * m.S, m.S, m.epoch, err);
+    __syncthreads();
+    cand_all = mbox_at<Cand>(m, m.rank, L.cand) + (uint64_t)b * m.S * K;
+    totals = mbox_at<ShardTotals>(m, m.rank, L.ccnt) + b * m.S;
+  }
   uint64_t avail = 0;
   for (uint32_t s = 0; s < S; ++s) avail += totals[s].aux;
   if (avail < K) {  // fewer than W*B selectable: EMPTY
@@ -149,10 +183,12 @@ __global__ void __launch_bounds__(kMergeThreads)
 cudaError_t launch_fifo_local(const uint64_t* key, const uint64_t* seq, const uint32_t* ord,
                               const FifoRings& rings, uint64_t shard_cap,
                               uint32_t n_shards_local, uint32_t first_shard, uint32_t K,
-                              int lifo, Cand* cand_out, ShardTotals* totals_out, cudaStream_t s) {
+                              int lifo, Cand* cand_out, ShardTotals* totals_out,
+                              const Mbox* mbox, cudaStream_t s) {
   count_launch();
   fifo_local_kernel<<<n_shards_local, kLocalThreads, 0, s>>>(
-      key, seq, ord, rings, shard_cap, first_shard, K, lifo, cand_out, totals_out);
+      key, seq, ord, rings, shard_cap, first_shard, K, lifo, cand_out, totals_out,
+      mbox ? *mbox : Mbox{}, mbox != nullptr);
   return cudaGetLastError();
 }
 
@@ -161,7 +197,8 @@ cudaError_t launch_fifo_merge(const Cand* cand_all, const ShardTotals* totals_al
                               uint32_t rank, uint32_t B, const uint32_t* const* gen_ptrs,
                               uint32_t shards_per_rank, uint64_t* out_idx, float* out_w,
                               double* out_p, uint32_t* out_gen, uint32_t* err,
-                              uint32_t* glob_shard, uint32_t* glob_slot, cudaStream_t s) {
+                              uint32_t* glob_shard, uint32_t* glob_slot, const Mbox* mbox,
+                              cudaStream_t s) {
   const uint64_t n = (uint64_t)n_shards * K;
   const uint64_t threads = n > B ? n : B;
   const uint32_t grid = (uint32_t)((threads + kMergeThreads - 1) / kMergeThreads);
@@ -169,7 +206,8 @@ cudaError_t launch_fifo_merge(const Cand* cand_all, const ShardTotals* totals_al
   fifo_merge_kernel<<<grid, kMergeThreads, 0, s>>>(cand_all, totals_all, n_shards, K, lifo,
                                                    shard_cap, rank, B, gen_ptrs, shards_per_rank,
                                                    out_idx, out_w, out_p, out_gen, err,
-                                                   glob_shard, glob_slot);
+                                                   glob_shard, glob_slot,
+                                                   mbox ? *mbox : Mbox{}, mbox != nullptr);
   return cudaGetLastError();
 }
 

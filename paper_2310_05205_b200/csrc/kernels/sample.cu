@@ -16,7 +16,7 @@
 // The IS weights (q_min/q)^beta need the min over the whole slice; the last
 // block to finish (threadfence + counter) computes them and re-arms the
 // counter and the min slot for the next launch.
-#include "common.cuh"
+#include "mbox.cuh"
 
 namespace gear {
 
@@ -60,12 +60,16 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
   const uint32_t b = blockIdx.x * kWarps + warp;
   const bool prioritized = p.strategy == kPrioritized;
 
+  // W > 1: every block publishes this rank's shard totals into every peer's
+  // mailbox over NVLink and waits for all peers' (mbox.cuh).
+  const ShardTotals* totals = p.xchg ? mbox_exchange_totals(p.mbox, p.totals_local, p.err)
+                                     : p.totals;
   // Shard totals -> exclusive offsets (S <= 32: one lane per shard).
   const uint32_t S = p.n_shards;
   uint64_t Ts = 0;
   uint32_t par = 0;
   if ((uint32_t)lane < S) {
-    const uint64_t tp = p.totals[lane].total_and_parity;
+    const uint64_t tp = __ldcg(&totals[lane].total_and_parity);
     Ts = tp & ((1ull << 62) - 1);
     par = (uint32_t)(tp >> 63);
   }

@@ -8,7 +8,7 @@
 // atomicMax(tag[slot], epoch<<32 | k+1) and an apply pass lets only the entry
 // whose tag survived write the key.  The epoch (one per update call) makes the
 // tags of earlier calls smaller, so the tag array never needs clearing.
-#include "common.cuh"
+#include "mbox.cuh"
 
 namespace gear {
 
@@ -151,9 +151,103 @@ __global__ void __launch_bounds__(kFusedThreads)
   }
 }
 
+// W > 1, W*n <= kFusedMax: one CTA quantises this rank's n entries, pushes
+// the records into every peer's mailbox over NVLink (mbox.cuh), waits for the
+// records of all W ranks, then runs the tag / barrier / apply passes over the
+// W*n records in (rank, position) order -- the whole collective update in one
+// launch, no NCCL call.
+__global__ void __launch_bounds__(kFusedThreads)
+    xchg_kernel(const uint64_t* __restrict__ idx, const void* __restrict__ prio, int prio_is_f64,
+                const uint32_t* __restrict__ gen_in, uint32_t n, uint64_t n_global,
+                uint32_t frac_bits, uint64_t q_max, const __grid_constant__ Mbox mb,
+                uint64_t local_begin, uint64_t local_rows, const uint32_t* __restrict__ gen,
+                unsigned long long* tag, uint32_t epoch, unsigned long long* n_stale,
+                uint32_t* err, uint64_t* key) {
+  const MboxLayout L = mbox_layout(mb.W, mb.S, mb.MB);
+  const uint32_t bsel = mbox_buf(mb);
+  uint32_t e = 0;
+  for (uint32_t k = threadIdx.x; k < n; k += kFusedThreads) {
+    UpdRec r;
+    r.idx = idx[k];
+    r.q = 0;
+    r.gen = gen_in ? gen_in[k] : 0u;
+    r.flags = gen_in ? 2u : 0u;
+    const double p = prio_is_f64 ? static_cast<const double*>(prio)[k]
+                                 : (double)static_cast<const float*>(prio)[k];
+    if (r.idx == kIdxNone) {
+    } else if (r.idx >= n_global) {
+      e |= kErrIndexRange;
+    } else if (!quantize(p, frac_bits, q_max, &r.q)) {
+      e |= kErrBadPriority;
+    } else {
+      r.flags |= 1u;
+    }
+    for (uint32_t dst = 0; dst < mb.W; ++dst)
+      mbox_at<UpdRec>(mb, dst, L.upd)[((uint64_t)bsel * mb.W + mb.rank) * mb.MB + k] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (uint32_t dst = 0; dst < mb.W; ++dst)
+      st_release_sys_u64(mbox_at<uint64_t>(mb, dst, L.uflag) + bsel * mb.W + mb.rank, mb.epoch);
+    mbox_wait(mbox_at<uint64_t>(mb, mb.rank, L.uflag) + bsel * mb.W, mb.W, mb.epoch, err);
+  }
+  __syncthreads();
+  const UpdRec* recs = mbox_at<UpdRec>(mb, mb.rank, L.upd) + (uint64_t)bsel * mb.W * mb.MB;
+  const uint32_t m = mb.W * n;
+  UpdRec r[kFusedPer];
+  bool mine[kFusedPer];
+  uint64_t loc[kFusedPer];
+  uint32_t stale = 0;
+#pragma unroll
+  for (int u = 0; u < kFusedPer; ++u) {
+    const uint32_t k = threadIdx.x + u * kFusedThreads;  // (rank, position) order
+    mine[u] = false;
+    if (k >= m) continue;
+    const uint32_t src = k / n, pos = k - src * n;
+    const UpdRec* rp = recs + (uint64_t)src * mb.MB + pos;
+    r[u].idx = __ldcg(&rp->idx);
+    r[u].q = __ldcg(&rp->q);
+    r[u].gen = __ldcg(&rp->gen);
+    r[u].flags = __ldcg(&rp->flags);
+    bool st;
+    mine[u] = owned_and_fresh(r[u], local_begin, local_rows, gen, &loc[u], &st);
+    stale += st ? 1u : 0u;
+    if (mine[u])
+      atomicMax(tag + loc[u], ((unsigned long long)epoch << 32) | (unsigned long long)(k + 1));
+  }
+  if (stale) {
+    atomicAdd(n_stale, (unsigned long long)stale);
+    e |= kErrStale;
+  }
+  if (e) atomicOr(err, e);
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kFusedPer; ++u) {
+    const uint32_t k = threadIdx.x + u * kFusedThreads;
+    if (mine[u] && __ldcg(tag + loc[u]) ==
+                       (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1)))
+      key[loc[u]] = r[u].q;
+  }
+}
+
 }  // namespace
 
 uint32_t update_fused_max() { return kFusedMax; }
+
+cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_is_f64,
+                               const uint32_t* gen_in, uint32_t n, uint64_t n_global,
+                               uint32_t frac_bits, uint64_t q_max, const Mbox& mb,
+                               uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
+                               unsigned long long* tag, uint32_t epoch,
+                               unsigned long long* n_stale, uint32_t* err, uint64_t* key,
+                               cudaStream_t s) {
+  count_launch();
+  xchg_kernel<<<1, kFusedThreads, 0, s>>>(idx, prio, prio_is_f64, gen_in, n, n_global, frac_bits,
+                                          q_max, mb, local_begin, local_rows, gen, tag, epoch,
+                                          n_stale, err, key);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_is_f64,
                                 const uint32_t* gen_in, const UpdRec* recs, uint32_t m,

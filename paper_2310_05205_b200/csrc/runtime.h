@@ -126,6 +126,14 @@ struct gear_table {
   float* tmp_w = nullptr;
   double* tmp_p = nullptr;
   uint32_t* tmp_gen = nullptr;
+  // peer mailboxes (W > 1): this rank's allocation, every rank's mapping, and
+  // one epoch counter per exchange kind (identical on all ranks: SPMD)
+  uint8_t* mbox = nullptr;
+  gear::Mbox mb{};
+  std::vector<void*> mbox_opened;
+  uint64_t ep_totals = 0, ep_upd = 0, ep_fifo = 0;
+  int peer_xchg = 1;                 // 1: mailbox exchanges, 0: NCCL all-gathers
+
   uint32_t* draw_list = nullptr;     // [max_batch] owner-affine slice -> draw number
   uint32_t* pos_scratch = nullptr;   // [W*max_batch]
   uint32_t* ov_scratch = nullptr;    // [W*max_batch]

@@ -28,13 +28,14 @@ OS = {gear.GEAR_FIFO: oracle.FIFO, gear.GEAR_LIFO: oracle.LIFO, gear.GEAR_UNIFOR
       gear.GEAR_WEIGHTED: oracle.WEIGHTED, gear.GEAR_PRIORITIZED: oracle.PRIORITIZED}
 
 
-def run_case(comm, W, rank, R, placements, removal, Cs=700, B=40, steps=3):
+def run_case(comm, W, rank, R, placements, removal, Cs=700, B=40, steps=3, xchg=1):
     dt = [gear.GEAR_F32, gear.GEAR_U8, gear.GEAR_I32]
     shapes = [(5,), (3,), ()]
     cols = [gear.Column(f"c{i}", dt[i % 3], shapes[i % 3], p) for i, p in enumerate(placements)]
     S = W * R
     N = S * Cs
     t = gear.Table(N, 4, cols, comm, shards_per_rank=R, removal=removal, max_batch=1024)
+    gear.gear_table_set_tuning(t.handle, "peer_xchg", xchg)
     o = oracle.Table(Cs, S, removal=removal)
     rb = t.row_bytes
     content = np.full(N, -1, np.int64)
@@ -124,12 +125,13 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     comm = gear.comm_from_torch_distributed(local)
     D, H = gear.GEAR_DEVICE, gear.GEAR_HOST
-    cases = [(1, [D, D, D], 0), (2, [D, D, D], 1), (1, [H, H, H], 0), (2, [D, H, D], 0)]
-    for R, pl, removal in cases:
-        run_case(comm, W, rank, R, pl, removal)
+    cases = [(1, [D, D, D], 0, 1), (2, [D, D, D], 1, 1), (1, [H, H, H], 0, 1),
+             (2, [D, H, D], 0, 1), (1, [D, D, D], 0, 0), (2, [D, H, D], 1, 0)]
+    for R, pl, removal, xchg in cases:
+        run_case(comm, W, rank, R, pl, removal, xchg=xchg)
         dist.barrier()
         if rank == 0:
-            print(f"case R={R} placements={pl} removal={removal}: ok", flush=True)
+            print(f"case R={R} placements={pl} removal={removal} peer_xchg={xchg}: ok", flush=True)
     gear.gear_comm_destroy(comm)
     dist.destroy_process_group()
     print(f"rank {rank}: all multi-GPU parity cases ok", flush=True)
