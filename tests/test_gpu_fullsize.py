@@ -22,12 +22,15 @@ def torch_cuda():
     return torch
 
 
-def _run_config(torch, name, steps=3, rows_checked=24):
+def _run_config(torch, name, steps=3, rows_checked=24, strategy=None):
+    import dataclasses
     import bench
     import oracle
     import synth
     import paper_2310_05205_b200 as gear
     cfg = synth.CONFIGS[name]
+    if strategy:
+        cfg = dataclasses.replace(cfg, strategy=strategy, update=False)
     capacity, note = bench.scaled_capacity(cfg, 1)
     stream = torch.cuda.Stream()
     t, prio_all = bench.build_table(cfg, None, 1, 0, capacity, stream)
@@ -37,7 +40,8 @@ def _run_config(torch, name, steps=3, rows_checked=24):
     assert np.array_equal(key, o.key)
     B = cfg.batch
     strat = gear.STRATEGIES[cfg.strategy]
-    ostrat = {"prioritized": oracle.PRIORITIZED, "weighted": oracle.WEIGHTED}[cfg.strategy]
+    ostrat = {"prioritized": oracle.PRIORITIZED, "weighted": oracle.WEIGHTED,
+              "fifo": oracle.FIFO, "lifo": oracle.LIFO}[cfg.strategy]
     idx = torch.empty(B, dtype=torch.int64, device="cuda")
     w = torch.empty(B, dtype=torch.float32, device="cuda")
     outs = [torch.empty((B, rb), dtype=torch.uint8, device="cuda") for rb in t.row_bytes]
@@ -79,3 +83,10 @@ def test_c3_full_size_host(torch_cuda):
 
 def test_c5_host_scaled(torch_cuda):
     _run_config(torch_cuda, "c5", steps=2)
+
+
+@pytest.mark.parametrize("strategy", ["fifo", "lifo"])
+def test_c4_mixed_fifo_lifo_scaled(torch_cuda, strategy):
+    """c4 (HBM + host columns), FIFO/LIFO over the whole table (N scaled to
+    the box's host RAM)."""
+    _run_config(torch_cuda, "c4", steps=2, strategy=strategy)

@@ -54,7 +54,35 @@ static float time_memcpy(void* d, const void* s, size_t bytes, cudaMemcpyKind k,
   return best;
 }
 
+// Sustained single-device loop for the concurrent probes:
+//   probe zc <dev> <seconds>   zero-copy kernel reads of 1 GiB pinned host memory
+//   probe h2d <dev> <seconds>  pinned cudaMemcpy H2D of 1 GiB
+static int sustained(const char* mode, int dev, double secs) {
+  CK(cudaSetDevice(dev));
+  size_t bytes = (size_t)1 << 30;
+  void *h, *d;
+  CK(cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(h, 1, bytes);
+  CK(cudaMalloc(&d, bytes));
+  void* hd; CK(cudaHostGetDevicePointer(&hd, h, 0));
+  cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
+  double moved = 0, ms_total = 0;
+  auto t0 = std::chrono::steady_clock::now();
+  while (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < secs) {
+    CK(cudaEventRecord(a));
+    if (mode[0] == 'z') copy_kernel<8><<<1184, 512>>>((const int4*)hd, (int4*)d, bytes / 16);
+    else CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice));
+    CK(cudaEventRecord(b)); CK(cudaEventSynchronize(b));
+    float ms; CK(cudaEventElapsedTime(&ms, a, b));
+    moved += bytes; ms_total += ms;
+  }
+  printf("{\"probe\":\"sustained_%s\",\"dev\":%d,\"GBps\":%.2f,\"seconds\":%.2f}\n", mode, dev,
+         moved / ms_total / 1e6, ms_total / 1e3);
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc >= 4) return sustained(argv[1], atoi(argv[2]), atof(argv[3]));
   int ndev = 0; CK(cudaGetDeviceCount(&ndev));
   printf("{\"probe\":\"devices\",\"n\":%d}\n", ndev);
   size_t bytes = (size_t)1 << 30;
