@@ -103,6 +103,7 @@ def scaled_capacity(cfg, n_ranks: int) -> tuple[int, str]:
     if host_rb:
         mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
         frac = 0.6 if n_ranks == 1 else 0.4
+        frac = float(os.environ.get("GEAR_BENCH_HOST_FRAC", frac))
         fit = int(frac * mem) // host_rb
         if fit < N:
             N = max(n_ranks * 1024, (fit // (n_ranks * 1024)) * n_ranks * 1024)

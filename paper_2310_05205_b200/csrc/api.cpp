@@ -255,7 +255,16 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
     } else {
       if (t->W == 1) {
         void* p = nullptr;
-        GEAR_TRY(map_host("", true, cs.bytes_local, &p));
+        // GEAR_HOST_SHM=1: use a shared-memory object even at W = 1 (to
+        // compare page backing with the W > 1 path)
+        std::string nm;
+        if (const char* e = getenv("GEAR_HOST_SHM"); e && e[0] == '1') {
+          char b[96];
+          snprintf(b, sizeof(b), "/gear_w1_%d_c%u", (int)getpid(), c);
+          nm = b;
+        }
+        GEAR_TRY(map_host(nm, true, cs.bytes_local, &p));
+        if (!nm.empty()) shm_unlink(nm.c_str());
         cs.host_maps.emplace_back(p, cs.bytes_local);
         cs.local = (uint8_t*)p;
         void* dp = nullptr;
