@@ -260,9 +260,12 @@ def run_gpu(args):
     ms, coll_ms_p, launches, clk = timed(step_pipe)
     ms_serial, coll_ms_s, _, clk_s = timed(step_serial)
 
-    # end-to-end through the C-ABI with HOST buffers: the step's priority update
-    # (ids + f64 priorities) comes from pinned host memory, and the sampled ids
-    # and weights go back to pinned host memory, read by the host every step.
+    # End-to-end through the C-ABI with HOST buffers, one stream: the step's
+    # priority update reads ids + f64 priorities from pinned host memory (H2D
+    # inside gear_update_priorities), gear_sample writes the ids and IS weights
+    # to pinned host memory (D2H inside the call), gear_collect reads the ids
+    # from that host buffer (H2D inside the call) and writes the batch to HBM,
+    # and the host waits for the step before issuing the next one.
     barrier()
     h_idx.copy_(idx.cpu())
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -270,16 +273,15 @@ def run_gpu(args):
     for i in range(args.steps):
         if cfg.update:
             gear.gear_update_priorities(t.handle, B, h_idx, h_prio[i % 16], gear.GEAR_F64, None, stream)
-        gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + 7919 + i, cfg.beta, idx, w,
+        gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + 7919 + i, cfg.beta, h_idx, h_w,
                          None, None, stream)
-        gear.gear_collect(t.handle, B, idx, col_ids, outs, stream)
-        with torch.cuda.stream(stream):
-            h_idx.copy_(idx, non_blocking=True)
-            h_w.copy_(w, non_blocking=True)
+        gear.gear_collect(t.handle, B, h_idx, col_ids, outs, stream)
         stream.synchronize()     # the host consumes the ids before the next step
     e3.record(stream)
     barrier()
     e2e_ms = e2.elapsed_time(e3)
+    e2e_h2d = (16 * B if cfg.update else 0) + 8 * B
+    e2e_d2h = 12 * B
 
     times = torch.tensor([ms, e2e_ms, coll_ms_p, ms_serial, coll_ms_s], device="cuda")
     if world > 1:
@@ -337,8 +339,9 @@ def run_gpu(args):
                    "collect_avg_ms": coll_serial,
                    "note": "sample -> collect -> update on one stream, same K steps"},
         "roofline": roof,
-        "e2e": {"value": traj / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": (16 * B if cfg.update else 0),
-                "d2h_bytes_per_step": 12 * B},
+        "e2e": {"value": traj / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": e2e_h2d,
+                "d2h_bytes_per_step": e2e_d2h,
+                "path": "C-ABI with pinned host ids/priorities/weights; batch in HBM; host sync per step"},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
