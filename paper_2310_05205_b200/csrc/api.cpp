@@ -768,13 +768,18 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     GEAR_CUDA(launch_fifo_local(t->key, t->seq, t->ord, rings, t->Cs, t->R, t->rank * t->R, K,
                                 lifo, t->cand_local, t->fifo_totals_local, xchg ? &mb : nullptr,
                                 s));
-    if (!xchg) {
+    const Cand* cand_all = t->cand_all;
+    const ShardTotals* merge_totals = t->fifo_totals_all;
+    if (t->W == 1) {  // the local lists are all the lists
+      cand_all = t->cand_local;
+      merge_totals = fifo_totals = t->fifo_totals_local;
+    } else if (!xchg) {
       GEAR_TRY(allgather_bytes(t->comm, t->cand_local, t->cand_all,
                                (size_t)t->R * K * sizeof(Cand), s));
       GEAR_TRY(allgather_bytes(t->comm, t->fifo_totals_local, t->fifo_totals_all,
                                t->R * sizeof(ShardTotals), s));
     }
-    GEAR_CUDA(launch_fifo_merge(t->cand_all, t->fifo_totals_all, t->S, K, lifo, t->Cs, t->rank,
+    GEAR_CUDA(launch_fifo_merge(cand_all, merge_totals, t->S, K, lifo, t->Cs, t->rank,
                                 B, t->d_gen_ptrs, t->R, d_idx, d_w, d_p, d_gen, t->err,
                                 affine ? t->glob_shard : nullptr, affine ? t->glob_slot : nullptr,
                                 xchg ? &mb : nullptr, s));
@@ -815,6 +820,8 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
       const MboxLayout L = mbox_layout(t->W, t->S, t->max_batch);
       totals_all = reinterpret_cast<const ShardTotals*>(t->mb.base[t->rank] + L.totals) +
                    (mb.epoch & 1) * t->S;
+    } else if (t->W == 1) {
+      totals_all = t->cdf_totals_local;  // R local shards are all the shards
     } else {
       GEAR_TRY(allgather_bytes(t->comm, t->cdf_totals_local, t->cdf_totals_all,
                                t->R * sizeof(ShardTotals), s));
