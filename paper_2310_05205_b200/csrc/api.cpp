@@ -799,10 +799,9 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     if (t->dirty || t->cdf_mode != mode) {
       // Rebuild into the other buffer: peers may still search the current one.
       t->cdf_parity ^= 1;
-      const int l = (int)(t->scan_launches & 1);
       GEAR_CUDA(launch_scan(t->key, t->cdf[t->cdf_parity], t->Cs, t->R, mode, t->cdf_parity,
-                            t->cdf_totals_local, t->scan_status[l], t->scan_status[l ^ 1],
-                            t->scan_ticket[l], t->scan_ticket[l ^ 1], s));
+                            t->cdf_totals_local, t->scan_status[0], t->scan_ticket[0],
+                            t->scan_ticket[1], s));
       t->scan_launches += 1;
       t->cdf_mode = mode;
       t->dirty = false;

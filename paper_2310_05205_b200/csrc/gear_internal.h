@@ -213,10 +213,12 @@ void count_launch(uint64_t n = 1);
 // K1: per-shard inclusive u64 scan with decoupled look-back.  Writes cdf for
 // `n_shards_local` contiguous shards of `shard_cap` keys and their totals.
 // indicator != 0 scans [key > 0] instead of key.
+// status [tiles], ticket and done counter start at 0 and are left at 0 by the
+// kernel itself (the last tile re-arms them), so launches can be replayed.
 cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf, uint64_t shard_cap,
                         uint32_t n_shards_local, int indicator, uint32_t parity,
-                        ShardTotals* totals_out, uint64_t* status_cur, uint64_t* status_next,
-                        uint32_t* ticket_cur, uint32_t* ticket_next, cudaStream_t s);
+                        ShardTotals* totals_out, uint64_t* status, uint32_t* ticket,
+                        uint32_t* done, cudaStream_t s);
 uint32_t scan_tiles_per_shard(uint64_t shard_cap);
 
 // K2/K3/K7: draw + warp-cooperative search + IS weights.

@@ -12,8 +12,12 @@
 // store and need no fence.  Integer addition is associative, so the result is
 // bit-identical to a sequential sum whatever the tiling.
 //
-// Two status arrays and two tickets alternate between launches; each launch
-// clears the other pair for the next one, so no memset launch is needed.
+// Memory path: the tile is moved HBM -> shared memory with coalesced 16-byte
+// loads and back with coalesced 16-byte stores; threads own 16 consecutive
+// keys in a padded shared layout (one u64 of padding per 16, conflict-free
+// per half-warp).  The last tile to finish (done counter) clears the status
+// words, the ticket and the counter, so every launch starts from the same
+// state and the launch can be replayed from a CUDA graph.
 #include "common.cuh"
 
 namespace gear {
@@ -27,48 +31,54 @@ constexpr uint64_t kFlagA = 1ull << 62;
 constexpr uint64_t kFlagP = 2ull << 62;
 constexpr uint64_t kValMask = (1ull << 62) - 1;
 
+__device__ __forceinline__ int pad(int e) { return e + (e >> 4); }
+
 template <bool kIndicator>
 __global__ void __launch_bounds__(kThreads) scan_kernel(
     const uint64_t* __restrict__ key, uint64_t* __restrict__ cdf, uint64_t shard_cap,
     uint32_t tiles_per_shard, uint32_t n_tiles, uint32_t parity, ShardTotals* totals,
-    uint64_t* status, uint64_t* status_next, uint32_t* ticket, uint32_t* ticket_next) {
+    uint64_t* status, uint32_t* ticket, uint32_t* done) {
+  __shared__ uint64_t s_k[kTile + kTile / 16];
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_warp[kThreads / 32];
   __shared__ uint64_t s_excl;
+  __shared__ bool s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   if (tid == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const uint32_t t = s_tile;
-  // Clear this tile's slot of the next launch's status pair.
-  if (tid == 0) {
-    status_next[t] = 0;
-    if (t == 0) *ticket_next = 0;
-  }
   const uint32_t shard = t / tiles_per_shard;
   const uint32_t tt = t - shard * tiles_per_shard;
-  const uint64_t shard_base = (uint64_t)shard * shard_cap;
-  const uint64_t tile_begin = (uint64_t)tt * kTile;
-  const uint64_t my_begin = tile_begin + (uint64_t)tid * kItems;  // within shard
+  const uint64_t tile_begin = (uint64_t)tt * kTile;                   // within shard
+  const uint64_t gbase = (uint64_t)shard * shard_cap + tile_begin;    // within key[]
+  const uint32_t count = (uint32_t)min((uint64_t)kTile, shard_cap - tile_begin);
+  const bool vec = count == (uint32_t)kTile && (gbase & 1) == 0;
 
-  // Load kItems consecutive keys (16-byte vector loads when fully inside).
-  uint64_t v[kItems];
-  if (my_begin + kItems <= shard_cap && ((shard_base + my_begin) & 1) == 0) {
-    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(key + shard_base + my_begin);
+  // HBM -> shared, coalesced.
+  if (vec) {
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(key + gbase);
 #pragma unroll
-    for (int i = 0; i < kItems / 2; ++i) {
-      const ulonglong2 x = __ldg(src + i);
-      v[2 * i] = x.x;
-      v[2 * i + 1] = x.y;
+    for (int it = 0; it < kItems / 2; ++it) {
+      const int vi = it * kThreads + tid;
+      const ulonglong2 x = __ldg(src + vi);
+      const int p = pad(2 * vi);
+      s_k[p] = x.x;
+      s_k[p + 1] = x.y;
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < kItems; ++i)
-      v[i] = (my_begin + i < shard_cap) ? key[shard_base + my_begin + i] : 0ull;
+    for (int it = 0; it < kItems; ++it) {
+      const int e = it * kThreads + tid;
+      s_k[pad(e)] = (uint32_t)e < count ? key[gbase + e] : 0ull;
+    }
   }
-  if (kIndicator) {
+  __syncthreads();
+  uint64_t v[kItems];
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) v[i] = v[i] > 0 ? 1ull : 0ull;
+  for (int i = 0; i < kItems; ++i) {
+    const uint64_t x = s_k[tid * (kItems + 1) + i];
+    v[i] = kIndicator ? (x > 0 ? 1ull : 0ull) : x;
   }
   // Thread-local inclusive prefix.
 #pragma unroll
@@ -125,23 +135,44 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(
   }
   __syncthreads();
   const uint64_t base = s_excl + thread_excl;
-
-  // Store the CDF.
-  if (my_begin + kItems <= shard_cap && ((shard_base + my_begin) & 1) == 0) {
-    ulonglong2* dst = reinterpret_cast<ulonglong2*>(cdf + shard_base + my_begin);
 #pragma unroll
-    for (int i = 0; i < kItems / 2; ++i)
-      dst[i] = make_ulonglong2(base + v[2 * i], base + v[2 * i + 1]);
+  for (int i = 0; i < kItems; ++i) s_k[tid * (kItems + 1) + i] = base + v[i];
+  __syncthreads();
+
+  // shared -> HBM, coalesced.
+  if (vec) {
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(cdf + gbase);
+#pragma unroll
+    for (int it = 0; it < kItems / 2; ++it) {
+      const int vi = it * kThreads + tid;
+      const int p = pad(2 * vi);
+      dst[vi] = make_ulonglong2(s_k[p], s_k[p + 1]);
+    }
   } else {
 #pragma unroll
-    for (int i = 0; i < kItems; ++i)
-      if (my_begin + i < shard_cap) cdf[shard_base + my_begin + i] = base + v[i];
+    for (int it = 0; it < kItems; ++it) {
+      const int e = it * kThreads + tid;
+      if ((uint32_t)e < count) cdf[gbase + e] = s_k[pad(e)];
+    }
   }
   if (tt == tiles_per_shard - 1 && tid == 0) {
     ShardTotals r;
     r.total_and_parity = (s_excl + agg) | ((uint64_t)parity << 63);
     r.aux = 0;
     totals[shard] = r;
+  }
+  // The last tile to finish re-arms the status words, ticket and counter.
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == n_tiles - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    for (uint32_t i = tid; i < n_tiles; i += kThreads) status[i] = 0;
+    if (tid == 0) {
+      *ticket = 0;
+      *done = 0;
+    }
   }
 }
 
@@ -153,19 +184,17 @@ uint32_t scan_tiles_per_shard(uint64_t shard_cap) {
 
 cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf, uint64_t shard_cap,
                         uint32_t n_shards_local, int indicator, uint32_t parity,
-                        ShardTotals* totals_out, uint64_t* status_cur, uint64_t* status_next,
-                        uint32_t* ticket_cur, uint32_t* ticket_next, cudaStream_t s) {
+                        ShardTotals* totals_out, uint64_t* status, uint32_t* ticket,
+                        uint32_t* done, cudaStream_t s) {
   const uint32_t tps = scan_tiles_per_shard(shard_cap);
   const uint32_t n_tiles = tps * n_shards_local;
   count_launch();
   if (indicator)
     scan_kernel<true><<<n_tiles, kThreads, 0, s>>>(key, cdf, shard_cap, tps, n_tiles, parity,
-                                                   totals_out, status_cur, status_next,
-                                                   ticket_cur, ticket_next);
+                                                   totals_out, status, ticket, done);
   else
     scan_kernel<false><<<n_tiles, kThreads, 0, s>>>(key, cdf, shard_cap, tps, n_tiles, parity,
-                                                    totals_out, status_cur, status_next,
-                                                    ticket_cur, ticket_next);
+                                                    totals_out, status, ticket, done);
   return cudaGetLastError();
 }
 
