@@ -21,7 +21,7 @@ from typing import Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgear.so")
+LIB_PATH = os.environ.get("GEAR_LIB", os.path.join(_HERE, "libgear.so"))  # override: dev A/B builds
 
 # status codes (gear.h)
 GEAR_OK = 0

@@ -15,9 +15,9 @@
 // Memory path: the tile is moved HBM -> shared memory with coalesced 16-byte
 // loads and back with coalesced 16-byte stores; threads own 16 consecutive
 // keys in a padded shared layout (one u64 of padding per 16, conflict-free
-// per half-warp).  The last tile to finish (done counter) clears the status
-// words, the ticket and the counter, so every launch starts from the same
-// state and the launch can be replayed from a CUDA graph.
+// per half-warp).  The last tile to finish its look-back (done counter)
+// clears the status words, the ticket and the counter, so every launch starts
+// from the same state and the launch can be replayed from a CUDA graph.
 #include "common.cuh"
 
 namespace gear {
@@ -131,7 +131,15 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(
       }
       if (lane == 0) st_relaxed_u64(status + t, kFlagP | (excl + agg));
     }
-    if (lane == 0) s_excl = excl;
+    if (lane == 0) {
+      s_excl = excl;
+      // This tile no longer reads or writes status words: count it done.
+      // The fence only has to drain the status store above (the CDF stores
+      // come later), and the last tile to get here re-arms the status
+      // words, the ticket and the counter after its stores.
+      __threadfence();
+      s_last = atomicAdd(done, 1u) == n_tiles - 1;
+    }
   }
   __syncthreads();
   const uint64_t base = s_excl + thread_excl;
@@ -161,12 +169,6 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(
     r.aux = 0;
     totals[shard] = r;
   }
-  // The last tile to finish re-arms the status words, ticket and counter.
-  if (tid == 0) {
-    __threadfence();
-    s_last = atomicAdd(done, 1u) == n_tiles - 1;
-  }
-  __syncthreads();
   if (s_last) {
     for (uint32_t i = tid; i < n_tiles; i += kThreads) status[i] = 0;
     if (tid == 0) {
