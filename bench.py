@@ -257,8 +257,62 @@ def run_gpu(args):
         coll = float(np.mean([a.elapsed_time(b) for a, b in zip(*ev)]))
         return e0.elapsed_time(e1), coll, launches, clk
 
+    def timed_graph():
+        """The pipelined step captured once as a CUDA graph of S consecutive
+        steps (W = 1): the draw key comes from the table's device seed counter
+        and the update epoch is device-resident, so each replay performs S
+        new, different steps.  K/S replays are timed."""
+        S = next(d for d in (10, 8, 5, 4, 2, 1) if args.steps % d == 0)
+        gear.gear_table_set_tuning(t.handle, "device_seed", synth.SAMPLE_SEED_BASE + 100000)
+        gstrat = strategy | gear.GEAR_SAMPLE_DEVICE_SEED
+
+        def gstep(i):
+            b = i % 2
+            if i >= 2:
+                stream.wait_event(ev_collected[b])
+            gear.gear_sample(t.handle, gstrat, B, 0, cfg.beta, idx2[b], w, None, None, stream)
+            ev_sampled[b].record(stream)
+            if cfg.update:
+                gear.gear_update_priorities(t.handle, B, idx2[b], pool[i % 16], gear.GEAR_F64, None,
+                                            stream)
+            cstream.wait_event(ev_sampled[b])
+            gear.gear_collect(t.handle, B, idx2[b], col_ids, outs, cstream)
+            ev_collected[b].record(cstream)
+
+        for i in range(args.warmup):
+            gstep(i)
+        barrier()
+        g = torch.cuda.CUDAGraph()
+        l0 = gear.gear_kernel_launches()
+        with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+            for i in range(S):
+                gstep(i)
+            stream.wait_stream(cstream)
+        per_graph = gear.gear_kernel_launches() - l0
+        barrier()
+        g.replay()  # warm replay
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps // S):
+            g.replay()
+        e1.record(stream)
+        barrier()
+        err, _ = t.sync()
+        assert err == 0, f"device error bits {err} in the graph replays"
+        return e0.elapsed_time(e1), per_graph * (args.steps // S), S
+
     ms, coll_ms_p, launches, clk = timed(step_pipe)
     ms_serial, coll_ms_s, _, clk_s = timed(step_serial)
+    graph = None
+    if world == 1 and args.graph:
+        ms_g, launches_g, S_g = timed_graph()
+        graph = {"value": world * B * args.steps / (ms_g / 1e3), "ms_per_step": ms_g / args.steps,
+                 "steps_per_graph": S_g, "gpu_launches": launches_g}
+        if ms_g < ms:  # the graph-replayed pipelined step is the headline when faster
+            graph["eager_pipelined"] = {"value": world * B * args.steps / (ms / 1e3),
+                                        "ms_per_step": ms / args.steps}
+            ms, launches = ms_g, launches_g
 
     # End-to-end through the C-ABI with HOST buffers, one stream: the step's
     # priority update reads ids + f64 priorities from pinned host memory (H2D
@@ -334,7 +388,9 @@ def run_gpu(args):
                    "assignment": args.assign,
                    **({"note": cap_note} if cap_note else {})},
         "collect_gbps": payload / (coll_avg / 1e3) / 1e9,
-        "step": "pipelined: collect(i) on a 2nd stream overlaps update(i) + sample(i+1)",
+        "step": ("pipelined: collect(i) on a 2nd stream overlaps update(i) + sample(i+1)"
+                 + ("; CUDA-graph replay" if graph and "eager_pipelined" in graph else "")),
+        **({"graph": graph} if graph else {}),
         "serial": {"value": traj / (ms_serial / 1e3), "ms_per_step": ms_serial / args.steps,
                    "collect_avg_ms": coll_serial,
                    "note": "sample -> collect -> update on one stream, same K steps"},
@@ -442,6 +498,8 @@ def main():
     ap.add_argument("--strategy", default=None,
                     choices=["fifo", "lifo", "uniform", "weighted", "prioritized"],
                     help="override the config's strategy")
+    ap.add_argument("--graph", type=int, default=1,
+                    help="N=1: also time the pipelined step captured as a CUDA graph")
     ap.add_argument("--assign", default="owner", choices=["owner", "contiguous"],
                     help="owner-affine (DESIGN.md Q19) or contiguous rank slices of the global batch")
     ap.add_argument("--impl", default="gear", choices=["gear", "reference"])

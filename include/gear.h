@@ -105,6 +105,14 @@ typedef enum {
  * each rank mostly collects rows from its own HBM instead of over NVLink. */
 #define GEAR_SAMPLE_OWNER_AFFINE 0x100
 
+/* Flag OR-ed into the strategy of gear_sample: the draw key is the table's
+ * device-resident seed counter instead of the `seed` argument, and the call
+ * advances the counter on the device (set it with gear_table_set_tuning(t,
+ * "device_seed", value)).  Consecutive calls use value, value+1, ... even when
+ * the calls are captured once in a CUDA graph and replayed.  W = 1 only for
+ * graph replay: the W > 1 mailbox epochs are host-side. */
+#define GEAR_SAMPLE_DEVICE_SEED 0x200
+
 /* Victim choice when a shard is full. */
 typedef enum { GEAR_REMOVE_FIFO = 0, GEAR_REMOVE_LIFO = 1 } gear_removal;
 
@@ -264,6 +272,8 @@ gear_status gear_table_sync(gear_table* t, uint32_t* dev_errors, uint64_t* n_sta
  *   "tma_ctas_per_sm": TMA CTAs per SM (default 2), "tma_stages": stages per
  *                   CTA (2, 3, 4, 6, 8; default 3); ctas * stages * tma_chunk
  *                   must stay <= 220 KB (set the smaller knob first);
+ *   "device_seed":  set the device seed counter used by GEAR_SAMPLE_DEVICE_SEED
+ *                   (synchronises the device);
  *   "peer_xchg":    W > 1 only, same value on every rank: 1 = the per-step
  *                   exchanges (shard totals, update records, FIFO/LIFO
  *                   candidates) are NVLink stores into the peers' mailboxes

@@ -47,6 +47,7 @@ GEAR_DEVICE, GEAR_HOST = 0, 1
 GEAR_FIFO, GEAR_LIFO, GEAR_UNIFORM, GEAR_WEIGHTED, GEAR_PRIORITIZED = range(5)
 GEAR_REMOVE_FIFO, GEAR_REMOVE_LIFO = 0, 1
 GEAR_SAMPLE_OWNER_AFFINE = 0x100
+GEAR_SAMPLE_DEVICE_SEED = 0x200
 
 STRATEGIES = {"fifo": GEAR_FIFO, "lifo": GEAR_LIFO, "uniform": GEAR_UNIFORM,
               "weighted": GEAR_WEIGHTED, "prioritized": GEAR_PRIORITIZED}

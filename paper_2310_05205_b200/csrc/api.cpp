@@ -148,7 +148,7 @@ void destroy_table(gear_table* t) {
   dfree(t->draw_list); dfree(t->pos_scratch); dfree(t->ov_scratch);
   dfree(t->glob_shard); dfree(t->glob_slot);
   dfree(t->upd_local); dfree(t->upd_all); dfree(t->upd_idx); dfree(t->upd_prio); dfree(t->upd_gen);
-  dfree(t->n_stale); dfree(t->err);
+  dfree(t->n_stale); dfree(t->err); dfree(t->d_epoch); dfree(t->d_seed);
   dfree(t->col_idx.p);
   dfree(t->d_meta); dfree(t->d_ord); dfree(t->d_out); dfree(t->d_rows);
   if (t->h_meta) cudaFreeHost(t->h_meta);
@@ -392,6 +392,10 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_TRY(dalloc(&t->upd_idx, MB));
   GEAR_TRY(dalloc(&t->upd_prio, MB));
   GEAR_TRY(dalloc(&t->upd_gen, MB));
+  GEAR_TRY(dalloc(&t->d_epoch, 1));
+  GEAR_CUDA(cudaMemset(t->d_epoch, 0, 4));
+  GEAR_TRY(dalloc(&t->d_seed, 1));
+  GEAR_CUDA(cudaMemset(t->d_seed, 0, 8));
   GEAR_TRY(dalloc(&t->n_stale, 1));
   GEAR_TRY(dalloc(&t->err, 1));
   GEAR_CUDA(cudaMemset(t->n_stale, 0, 8));
@@ -681,13 +685,12 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
     }
     if (gen) GEAR_TRY(stage_in(gen, n, t->upd_gen, s, &d_gen));
   }
-  t->epoch += 1;
   const uint64_t local_begin = (uint64_t)t->rank * t->Clocal;
   const bool fused = t->update_fused && (uint64_t)n * t->W <= update_fused_max();
   if (t->W == 1 && fused) {
     // one launch: quantise, tag, block barrier, apply
     GEAR_CUDA(launch_update_fused(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, nullptr, n, t->N,
-                                  t->F, t->qmax, local_begin, t->Clocal, t->gen, t->tag, t->epoch,
+                                  t->F, t->qmax, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
                                   t->n_stale, t->err, t->key, s));
   } else if (t->W > 1 && fused && t->peer_xchg) {
     // one launch: quantise, push records to every peer over NVLink, wait for
@@ -695,7 +698,7 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
     Mbox mb = t->mb;
     mb.epoch = ++t->ep_upd;
     GEAR_CUDA(launch_update_xchg(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N, t->F,
-                                 t->qmax, mb, local_begin, t->Clocal, t->gen, t->tag, t->epoch,
+                                 t->qmax, mb, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
                                  t->n_stale, t->err, t->key, s));
   } else {
     GEAR_CUDA(launch_update_quantize(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N, t->F,
@@ -709,12 +712,12 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
     }
     if (fused) {
       GEAR_CUDA(launch_update_fused(nullptr, nullptr, 0, nullptr, recs, m, t->N, t->F, t->qmax,
-                                    local_begin, t->Clocal, t->gen, t->tag, t->epoch, t->n_stale,
+                                    local_begin, t->Clocal, t->gen, t->tag, t->d_epoch, t->n_stale,
                                     t->err, t->key, s));
     } else {
-      GEAR_CUDA(launch_update_tag(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->epoch,
+      GEAR_CUDA(launch_update_tag(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
                                   t->n_stale, t->err, s));
-      GEAR_CUDA(launch_update_apply(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->epoch,
+      GEAR_CUDA(launch_update_apply(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
                                     t->key, s));
     }
   }
@@ -730,7 +733,9 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
   GEAR_CUDA(cudaSetDevice(t->device));
   cudaStream_t s = (cudaStream_t)stream;
   const bool affine = ((uint32_t)strategy & GEAR_SAMPLE_OWNER_AFFINE) != 0;
-  strategy = (gear_strategy)((uint32_t)strategy & ~(uint32_t)GEAR_SAMPLE_OWNER_AFFINE);
+  const bool dseed = ((uint32_t)strategy & GEAR_SAMPLE_DEVICE_SEED) != 0;
+  strategy = (gear_strategy)((uint32_t)strategy &
+                             ~(uint32_t)(GEAR_SAMPLE_OWNER_AFFINE | GEAR_SAMPLE_DEVICE_SEED));
   if (strategy < GEAR_FIFO || strategy > GEAR_PRIORITIZED)
     return set_error(GEAR_ERR_INVALID_ARG, "bad strategy %d", (int)strategy);
   if (B > t->max_batch) return set_error(GEAR_ERR_INVALID_ARG, "B %u > max_batch %u", B, t->max_batch);
@@ -848,8 +853,10 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     sp.qmin_slot = t->qmin_slot;
     sp.done_ctr = t->done_ctr;
     sp.err = t->err;
+    sp.seed_dev = dseed ? t->d_seed : nullptr;
     if (affine) {
       AssignParams ap = assign_params(t, B, seed);
+      ap.seed_dev = sp.seed_dev;
       ap.totals = totals_all;
       ap.totals_local = t->cdf_totals_local;
       ap.mbox = mb;
@@ -952,6 +959,11 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     t->collect_impl = (int)value;
   } else if (!strcmp(key, "lsu_chunk") && value >= 512 && value % 512 == 0 && value <= (1 << 20)) {
     t->chunk_bytes = (uint32_t)value;
+  } else if (!strcmp(key, "device_seed")) {
+    const uint64_t v = (uint64_t)value;  // synchronous: not for use while capturing
+    GEAR_CUDA(cudaSetDevice(t->device));
+    GEAR_CUDA(cudaDeviceSynchronize());
+    GEAR_CUDA(cudaMemcpy(t->d_seed, &v, 8, cudaMemcpyHostToDevice));
   } else if (!strcmp(key, "peer_xchg") && (value == 0 || value == 1)) {
     t->peer_xchg = (int)value;  // must be set identically on every rank
   } else if (!strcmp(key, "update_fused") && (value == 0 || value == 1)) {

@@ -172,6 +172,7 @@ struct SampleParams {
   double* out_p;
   uint32_t* out_gen;
   const uint32_t* draw_list;          // [B] draw numbers j of the slice, or null: rank*B + b
+  uint64_t* seed_dev;                 // non-null: key = *seed_dev, advanced by the kernel
   uint64_t* q_scratch;                // [B]
   unsigned long long* qmin_slot;      // reset to ~0 by the last block
   uint32_t* done_ctr;                 // reset to 0 by the last block
@@ -193,6 +194,7 @@ struct AssignParams {
   uint32_t rank;
   uint32_t B;
   uint64_t seed;
+  const uint64_t* seed_dev;         // non-null: the key is *seed_dev (read only)
   uint64_t shard_cap;
   uint32_t* draw_list;              // [B] out: global entry j of each slice position
   uint32_t* pos_scratch;            // [K]
@@ -231,11 +233,11 @@ cudaError_t launch_update_quantize(const uint64_t* idx, const void* prio, int pr
                                    uint32_t* err, cudaStream_t s);
 cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                               uint64_t local_rows, const uint32_t* gen, unsigned long long* tag,
-                              uint32_t epoch, unsigned long long* n_stale, uint32_t* err,
+                              uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err,
                               cudaStream_t s);
 cudaError_t launch_update_apply(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                                 uint64_t local_rows, const uint32_t* gen,
-                                const unsigned long long* tag, uint32_t epoch, uint64_t* key,
+                                const unsigned long long* tag, uint32_t* epoch_dev, uint64_t* key,
                                 cudaStream_t s);
 
 // Single-launch update for m <= update_fused_max() entries (one CTA): raw
@@ -245,7 +247,7 @@ cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_
                                 const uint32_t* gen_in, const UpdRec* recs, uint32_t m,
                                 uint64_t n_global, uint32_t frac_bits, uint64_t q_max,
                                 uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
-                                unsigned long long* tag, uint32_t epoch,
+                                unsigned long long* tag, uint32_t* epoch_dev,
                                 unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                 cudaStream_t s);
 
@@ -255,7 +257,7 @@ cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_i
                                const uint32_t* gen_in, uint32_t n, uint64_t n_global,
                                uint32_t frac_bits, uint64_t q_max, const Mbox& mb,
                                uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
-                               unsigned long long* tag, uint32_t epoch,
+                               unsigned long long* tag, uint32_t* epoch_dev,
                                unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                cudaStream_t s);
 

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kThreads) assign_kernel(const __grid_constant_
   __syncthreads();
   if (s_bail) return;
   const uint64_t T = s_T;
+  const uint64_t seed = p.seed_dev ? *(volatile const uint64_t*)p.seed_dev : p.seed;
   if (!p.glob_shard && T == 0) {  // nothing selectable: the sample kernel latches EMPTY
     for (uint32_t b = tid; b < B; b += kThreads) p.draw_list[b] = p.rank * B + b;
     return;
@@ -69,7 +70,7 @@ __global__ void __launch_bounds__(kThreads) assign_kernel(const __grid_constant_
       if (p.glob_shard) {
         s = p.glob_shard[j];
       } else {
-        const uint64_t u = __umul64hi(draw_bits(p.seed, j), T);
+        const uint64_t u = __umul64hi(draw_bits(seed, j), T);
         s = 0;
         while (s + 1 < S && s_G[s] <= u) ++s;
       }

@@ -59,6 +59,9 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t b = blockIdx.x * kWarps + warp;
   const bool prioritized = p.strategy == kPrioritized;
+  // Device seed counter (graph-replayable draws): read here, advanced by the
+  // last block once every block has read it.
+  const uint64_t seed = p.seed_dev ? *(volatile const uint64_t*)p.seed_dev : p.seed;
 
   // W > 1: every block publishes this rank's shard totals into every peer's
   // mailbox over NVLink and waits for all peers' (mbox.cuh).
@@ -81,7 +84,7 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
     const uint64_t j = p.draw_list ? (uint64_t)p.draw_list[b] : (uint64_t)p.rank * p.B + b;
     uint64_t g = kIdxNone, q = 0;
     if (T > 0) {
-      const uint64_t r = draw_bits(p.seed, j);
+      const uint64_t r = draw_bits(seed, j);
       const uint64_t u = __umul64hi(r, T);
       const unsigned own = __ballot_sync(kFull, (uint32_t)lane < S && G > u);
       const int s = __ffs(own) - 1;
@@ -110,15 +113,17 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
     }
     my_q = T > 0 ? q : ~0ull;
   }
-  if (!prioritized || p.out_w == nullptr) return;
+  const bool need_w = prioritized && p.out_w != nullptr;
+  if (!need_w && !p.seed_dev) return;
 
-  // Slice-wide q_min, then the last block writes the weights.
+  // Slice-wide q_min, then the last block writes the weights (and advances
+  // the device seed counter).
   if (lane == 0) s_min[warp] = my_q;
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long m = ~0ull;
     for (int w = 0; w < kWarps; ++w) m = s_min[w] < m ? s_min[w] : m;
-    atomicMin(p.qmin_slot, m);
+    if (need_w) atomicMin(p.qmin_slot, m);
     __threadfence();
     const uint32_t done = atomicAdd(p.done_ctr, 1u);
     s_last = (done == gridDim.x - 1);
@@ -126,15 +131,18 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const unsigned long long qmin = *(volatile unsigned long long*)p.qmin_slot;
-  for (uint32_t k = threadIdx.x; k < p.B; k += kThreads) {
-    const uint64_t q = *(volatile uint64_t*)(p.q_scratch + k);
-    p.out_w[k] = (T > 0 && q > 0) ? (float)pow((double)qmin / (double)q, p.beta) : 0.0f;
+  if (need_w) {
+    const unsigned long long qmin = *(volatile unsigned long long*)p.qmin_slot;
+    for (uint32_t k = threadIdx.x; k < p.B; k += kThreads) {
+      const uint64_t q = *(volatile uint64_t*)(p.q_scratch + k);
+      p.out_w[k] = (T > 0 && q > 0) ? (float)pow((double)qmin / (double)q, p.beta) : 0.0f;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     *p.qmin_slot = ~0ull;
     *p.done_ctr = 0;
+    if (p.seed_dev) *p.seed_dev = seed + 1;
   }
 }
 

@@ -7,7 +7,9 @@
 // passes over the concatenated entry list: a tag pass does
 // atomicMax(tag[slot], epoch<<32 | k+1) and an apply pass lets only the entry
 // whose tag survived write the key.  The epoch (one per update call) makes the
-// tags of earlier calls smaller, so the tag array never needs clearing.
+// tags of earlier calls smaller, so the tag array never needs clearing; it
+// lives in device memory and the kernels advance it themselves, so an update
+// captured in a CUDA graph stays correct when the graph is replayed.
 #include "mbox.cuh"
 
 namespace gear {
@@ -62,7 +64,8 @@ __device__ __forceinline__ bool owned_and_fresh(const UpdRec& r, uint64_t local_
 __global__ void __launch_bounds__(kThreads)
     tag_kernel(const UpdRec* __restrict__ recs, uint32_t m, uint64_t local_begin,
                uint64_t local_rows, const uint32_t* __restrict__ gen, unsigned long long* tag,
-               uint32_t epoch, unsigned long long* n_stale, uint32_t* err) {
+               uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err) {
+  const uint32_t epoch = *epoch_dev + 1;
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   if (k >= m) return;
   const UpdRec r = recs[k];
@@ -79,7 +82,9 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     apply_kernel(const UpdRec* __restrict__ recs, uint32_t m, uint64_t local_begin,
                  uint64_t local_rows, const uint32_t* __restrict__ gen,
-                 const unsigned long long* __restrict__ tag, uint32_t epoch, uint64_t* key) {
+                 const unsigned long long* __restrict__ tag, const uint32_t* epoch_dev,
+                 uint64_t* key) {
+  const uint32_t epoch = *epoch_dev + 1;
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   if (k >= m) return;
   const UpdRec r = recs[k];
@@ -103,7 +108,8 @@ __global__ void __launch_bounds__(kFusedThreads)
                  const uint32_t* __restrict__ gen_in, const UpdRec* __restrict__ recs, uint32_t m,
                  uint64_t n_global, uint32_t frac_bits, uint64_t q_max, uint64_t local_begin,
                  uint64_t local_rows, const uint32_t* __restrict__ gen, unsigned long long* tag,
-                 uint32_t epoch, unsigned long long* n_stale, uint32_t* err, uint64_t* key) {
+                 uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err, uint64_t* key) {
+  const uint32_t epoch = *epoch_dev + 1;  // device-resident: graph-replayable
   UpdRec r[kFusedPer];
   bool mine[kFusedPer];
   uint64_t loc[kFusedPer];
@@ -149,6 +155,8 @@ __global__ void __launch_bounds__(kFusedThreads)
                        (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1)))
       key[loc[u]] = r[u].q;
   }
+  __syncthreads();  // every thread has read the epoch before it advances
+  if (threadIdx.x == 0) *epoch_dev = epoch;
 }
 
 // W > 1, W*n <= kFusedMax: one CTA quantises this rank's n entries, pushes
@@ -161,8 +169,9 @@ __global__ void __launch_bounds__(kFusedThreads)
                 const uint32_t* __restrict__ gen_in, uint32_t n, uint64_t n_global,
                 uint32_t frac_bits, uint64_t q_max, const __grid_constant__ Mbox mb,
                 uint64_t local_begin, uint64_t local_rows, const uint32_t* __restrict__ gen,
-                unsigned long long* tag, uint32_t epoch, unsigned long long* n_stale,
+                unsigned long long* tag, uint32_t* epoch_dev, unsigned long long* n_stale,
                 uint32_t* err, uint64_t* key) {
+  const uint32_t epoch = *epoch_dev + 1;  // device-resident tag epoch
   const MboxLayout L = mbox_layout(mb.W, mb.S, mb.MB);
   const uint32_t bsel = mbox_buf(mb);
   uint32_t e = 0;
@@ -229,7 +238,11 @@ __global__ void __launch_bounds__(kFusedThreads)
                        (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1)))
       key[loc[u]] = r[u].q;
   }
+  __syncthreads();  // every thread has read the epoch before it advances
+  if (threadIdx.x == 0) *epoch_dev = epoch;
 }
+
+__global__ void epoch_bump_kernel(uint32_t* epoch_dev) { *epoch_dev += 1; }
 
 }  // namespace
 
@@ -239,12 +252,12 @@ cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_i
                                const uint32_t* gen_in, uint32_t n, uint64_t n_global,
                                uint32_t frac_bits, uint64_t q_max, const Mbox& mb,
                                uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
-                               unsigned long long* tag, uint32_t epoch,
+                               unsigned long long* tag, uint32_t* epoch_dev,
                                unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                cudaStream_t s) {
   count_launch();
   xchg_kernel<<<1, kFusedThreads, 0, s>>>(idx, prio, prio_is_f64, gen_in, n, n_global, frac_bits,
-                                          q_max, mb, local_begin, local_rows, gen, tag, epoch,
+                                          q_max, mb, local_begin, local_rows, gen, tag, epoch_dev,
                                           n_stale, err, key);
   return cudaGetLastError();
 }
@@ -253,14 +266,14 @@ cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_
                                 const uint32_t* gen_in, const UpdRec* recs, uint32_t m,
                                 uint64_t n_global, uint32_t frac_bits, uint64_t q_max,
                                 uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
-                                unsigned long long* tag, uint32_t epoch,
+                                unsigned long long* tag, uint32_t* epoch_dev,
                                 unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                 cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   count_launch();
   fused_kernel<<<1, kFusedThreads, 0, s>>>(idx, prio, prio_is_f64, gen_in, recs, m, n_global,
                                            frac_bits, q_max, local_begin, local_rows, gen, tag,
-                                           epoch, n_stale, err, key);
+                                           epoch_dev, n_stale, err, key);
   return cudaGetLastError();
 }
 
@@ -277,23 +290,25 @@ cudaError_t launch_update_quantize(const uint64_t* idx, const void* prio, int pr
 
 cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                               uint64_t local_rows, const uint32_t* gen, unsigned long long* tag,
-                              uint32_t epoch, unsigned long long* n_stale, uint32_t* err,
+                              uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err,
                               cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   count_launch();
   tag_kernel<<<(m + kThreads - 1) / kThreads, kThreads, 0, s>>>(
-      recs, m, local_begin, local_rows, gen, tag, epoch, n_stale, err);
+      recs, m, local_begin, local_rows, gen, tag, epoch_dev, n_stale, err);
   return cudaGetLastError();
 }
 
 cudaError_t launch_update_apply(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                                 uint64_t local_rows, const uint32_t* gen,
-                                const unsigned long long* tag, uint32_t epoch, uint64_t* key,
+                                const unsigned long long* tag, uint32_t* epoch_dev, uint64_t* key,
                                 cudaStream_t s) {
   if (m == 0) return cudaSuccess;
-  count_launch();
+  count_launch(2);
   apply_kernel<<<(m + kThreads - 1) / kThreads, kThreads, 0, s>>>(recs, m, local_begin,
-                                                                  local_rows, gen, tag, epoch, key);
+                                                                  local_rows, gen, tag, epoch_dev,
+                                                                  key);
+  epoch_bump_kernel<<<1, 1, 0, s>>>(epoch_dev);  // after every apply block read it
   return cudaGetLastError();
 }
 

@@ -148,7 +148,8 @@ struct gear_table {
   uint64_t* upd_idx = nullptr;
   double* upd_prio = nullptr;
   uint32_t* upd_gen = nullptr;
-  uint32_t epoch = 0;
+  uint32_t* d_epoch = nullptr;      // update tag epoch (device-resident, advanced by the kernels)
+  uint64_t* d_seed = nullptr;       // device seed counter (gear_sample with GEAR_SAMPLE_DEVICE_SEED)
   unsigned long long* n_stale = nullptr;
   uint32_t* err = nullptr;
 
