@@ -290,13 +290,14 @@ def run_gpu(args):
             stream.wait_stream(cstream)
         per_graph = gear.gear_kernel_launches() - l0
         barrier()
-        g.replay()  # warm replay
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps // S):
-            g.replay()
-        e1.record(stream)
+        with torch.cuda.stream(stream):  # replay() launches on the current stream
+            g.replay()  # warm replay
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps // S):
+                g.replay()
+            e1.record(stream)
         barrier()
         err, _ = t.sync()
         assert err == 0, f"device error bits {err} in the graph replays"
@@ -307,6 +308,9 @@ def run_gpu(args):
     graph = None
     if world == 1 and args.graph:
         ms_g, launches_g, S_g = timed_graph()
+        # a replay that takes less than the collect launches it contains did
+        # not run them: refuse the number
+        assert ms_g >= 0.9 * coll_ms_p * args.steps, (ms_g, coll_ms_p)
         graph = {"value": world * B * args.steps / (ms_g / 1e3), "ms_per_step": ms_g / args.steps,
                  "steps_per_graph": S_g, "gpu_launches": launches_g}
         if ms_g < ms:  # the graph-replayed pipelined step is the headline when faster

@@ -56,7 +56,10 @@ __global__ void __launch_bounds__(kThreads) assign_kernel(const __grid_constant_
   __syncthreads();
   if (s_bail) return;
   const uint64_t T = s_T;
-  const uint64_t seed = p.seed_dev ? *(volatile const uint64_t*)p.seed_dev : p.seed;
+  // (an asm load under a branch: a plain conditional load from a possibly
+  // null pointer was hoisted by the compiler and faulted)
+  uint64_t seed = p.seed;
+  if (p.seed_dev != nullptr) seed = ld_relaxed_u64(p.seed_dev);
   if (!p.glob_shard && T == 0) {  // nothing selectable: the sample kernel latches EMPTY
     for (uint32_t b = tid; b < B; b += kThreads) p.draw_list[b] = p.rank * B + b;
     return;

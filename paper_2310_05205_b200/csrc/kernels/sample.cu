@@ -61,7 +61,8 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
   const bool prioritized = p.strategy == kPrioritized;
   // Device seed counter (graph-replayable draws): read here, advanced by the
   // last block once every block has read it.
-  const uint64_t seed = p.seed_dev ? *(volatile const uint64_t*)p.seed_dev : p.seed;
+  uint64_t seed = p.seed;
+  if (p.seed_dev != nullptr) seed = ld_relaxed_u64(p.seed_dev);  // asm: never hoisted
 
   // W > 1: every block publishes this rank's shard totals into every peer's
   // mailbox over NVLink and waits for all peers' (mbox.cuh).
