@@ -376,6 +376,10 @@ def run_gpu(args):
     roof["algorithmic_bytes_per_launch"] = alg
     roof["remote_fraction"] = f_remote
     roof["traffic"] = args.traffic
+    # The whole step against the same bound: the step's algorithmic bytes of
+    # the binding resource over the (headline) time per step.
+    roof["step_achieved"] = alg / (ms / args.steps / 1e3) / 1e9
+    roof["step_frac"] = roof["step_achieved"] / roof["peak"]
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
