@@ -732,7 +732,9 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
   GEAR_TRY(check_table(t));
   GEAR_CUDA(cudaSetDevice(t->device));
   cudaStream_t s = (cudaStream_t)stream;
-  const bool affine = ((uint32_t)strategy & GEAR_SAMPLE_OWNER_AFFINE) != 0;
+  // With one rank every entry is local: the owner-affine slice is the
+  // contiguous one, so the assignment kernel is skipped.
+  const bool affine = ((uint32_t)strategy & GEAR_SAMPLE_OWNER_AFFINE) != 0 && t->W > 1;
   const bool dseed = ((uint32_t)strategy & GEAR_SAMPLE_DEVICE_SEED) != 0;
   strategy = (gear_strategy)((uint32_t)strategy &
                              ~(uint32_t)(GEAR_SAMPLE_OWNER_AFFINE | GEAR_SAMPLE_DEVICE_SEED));
