@@ -259,9 +259,10 @@ def run_gpu(args):
 
     def timed_graph():
         """The pipelined step captured once as a CUDA graph of S consecutive
-        steps (W = 1): the draw key comes from the table's device seed counter
-        and the update epoch is device-resident, so each replay performs S
-        new, different steps.  K/S replays are timed."""
+        steps: the draw key comes from the table's device seed counter and the
+        update epoch, the peer-mailbox epochs and the CDF parity are
+        device-resident, so each replay performs S new, different (collective)
+        steps.  K/S replays are timed."""
         S = next(d for d in (10, 8, 5, 4, 2, 1) if args.steps % d == 0)
         gear.gear_table_set_tuning(t.handle, "device_seed", synth.SAMPLE_SEED_BASE + 100000)
         gstrat = strategy | gear.GEAR_SAMPLE_DEVICE_SEED
@@ -306,7 +307,7 @@ def run_gpu(args):
     ms, coll_ms_p, launches, clk = timed(step_pipe)
     ms_serial, coll_ms_s, _, clk_s = timed(step_serial)
     graph = None
-    if world == 1 and args.graph:
+    if args.graph:
         ms_g, launches_g, S_g = timed_graph()
         # a replay that takes less than the collect launches it contains did
         # not run them: refuse the number
@@ -507,7 +508,7 @@ def main():
                     choices=["fifo", "lifo", "uniform", "weighted", "prioritized"],
                     help="override the config's strategy")
     ap.add_argument("--graph", type=int, default=1,
-                    help="N=1: also time the pipelined step captured as a CUDA graph")
+                    help="also time the pipelined step captured as a CUDA graph")
     ap.add_argument("--assign", default="owner", choices=["owner", "contiguous"],
                     help="owner-affine (DESIGN.md Q19) or contiguous rank slices of the global batch")
     ap.add_argument("--impl", default="gear", choices=["gear", "reference"])

@@ -148,7 +148,7 @@ void destroy_table(gear_table* t) {
   dfree(t->draw_list); dfree(t->pos_scratch); dfree(t->ov_scratch);
   dfree(t->glob_shard); dfree(t->glob_slot);
   dfree(t->upd_local); dfree(t->upd_all); dfree(t->upd_idx); dfree(t->upd_prio); dfree(t->upd_gen);
-  dfree(t->n_stale); dfree(t->err); dfree(t->d_epoch); dfree(t->d_seed);
+  dfree(t->n_stale); dfree(t->err); dfree(t->d_epoch); dfree(t->d_seed); dfree(t->d_xep);
   dfree(t->col_idx.p);
   dfree(t->d_meta); dfree(t->d_ord); dfree(t->d_out); dfree(t->d_rows);
   if (t->h_meta) cudaFreeHost(t->h_meta);
@@ -392,6 +392,8 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_TRY(dalloc(&t->upd_idx, MB));
   GEAR_TRY(dalloc(&t->upd_prio, MB));
   GEAR_TRY(dalloc(&t->upd_gen, MB));
+  GEAR_TRY(dalloc(&t->d_xep, 4));
+  GEAR_CUDA(cudaMemset(t->d_xep, 0, 32));
   GEAR_TRY(dalloc(&t->d_epoch, 1));
   GEAR_CUDA(cudaMemset(t->d_epoch, 0, 4));
   GEAR_TRY(dalloc(&t->d_seed, 1));
@@ -696,7 +698,7 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
     // one launch: quantise, push records to every peer over NVLink, wait for
     // every rank's records, tag, barrier, apply
     Mbox mb = t->mb;
-    mb.epoch = ++t->ep_upd;
+    mb.epoch_dev = t->d_xep + 1;  // update-exchange epoch (advanced by the kernel)
     GEAR_CUDA(launch_update_xchg(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N, t->F,
                                  t->qmax, mb, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
                                  t->n_stale, t->err, t->key, s));
@@ -765,13 +767,9 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     const bool xchg = t->W > 1 && t->peer_xchg;
     Mbox mb = t->mb;
     const ShardTotals* fifo_totals = t->fifo_totals_all;
-    if (xchg) {
-      // candidates go straight into every peer's mailbox from the local kernel
-      mb.epoch = ++t->ep_fifo;
-      const MboxLayout L = mbox_layout(t->W, t->S, t->max_batch);
-      fifo_totals = reinterpret_cast<const ShardTotals*>(t->mb.base[t->rank] + L.ccnt) +
-                    (mb.epoch & 1) * t->S;
-    }
+    // candidates go straight into every peer's mailbox from the local kernel;
+    // the FIFO-exchange epoch advances after the merge (and assignment)
+    mb.epoch_dev = t->d_xep + 2;
     GEAR_CUDA(launch_fifo_local(t->key, t->seq, t->ord, rings, t->Cs, t->R, t->rank * t->R, K,
                                 lifo, t->cand_local, t->fifo_totals_local, xchg ? &mb : nullptr,
                                 s));
@@ -793,6 +791,8 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     if (affine) {
       AssignParams ap = assign_params(t, B, seed);
       ap.fifo_totals = fifo_totals;
+      ap.fifo_mbox = xchg;
+      ap.mbox = mb;
       ap.glob_shard = t->glob_shard;
       ap.glob_slot = t->glob_slot;
       ap.out_idx = d_idx;
@@ -801,12 +801,12 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
       ap.out_gen = d_gen;
       GEAR_CUDA(launch_assign(ap, s));
     }
+    if (xchg) GEAR_CUDA(launch_epoch_bump(t->d_xep + 2, s));
   } else {
     const int mode = strategy == GEAR_UNIFORM ? 1 : 0;
     if (t->dirty || t->cdf_mode != mode) {
-      // Rebuild into the other buffer: peers may still search the current one.
-      t->cdf_parity ^= 1;
-      GEAR_CUDA(launch_scan(t->key, t->cdf[t->cdf_parity], t->Cs, t->R, mode, t->cdf_parity,
+      // Rebuild into the buffer peers are not reading (device-resident parity).
+      GEAR_CUDA(launch_scan(t->key, t->cdf[0], t->cdf[1], t->Cs, t->R, mode, t->d_xep + 3,
                             t->cdf_totals_local, t->scan_status[0], t->scan_ticket[0],
                             t->scan_ticket[1], s));
       t->scan_launches += 1;
@@ -821,11 +821,9 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     const bool xchg = t->W > 1 && t->peer_xchg;
     Mbox mb = t->mb;
     const ShardTotals* totals_all = t->cdf_totals_all;
+    mb.epoch_dev = t->d_xep + 0;  // totals-exchange epoch (advanced by the kernels)
     if (xchg) {
-      mb.epoch = ++t->ep_totals;
-      const MboxLayout L = mbox_layout(t->W, t->S, t->max_batch);
-      totals_all = reinterpret_cast<const ShardTotals*>(t->mb.base[t->rank] + L.totals) +
-                   (mb.epoch & 1) * t->S;
+      totals_all = nullptr;  // the kernels find them in the mailbox
     } else if (t->W == 1) {
       totals_all = t->cdf_totals_local;  // R local shards are all the shards
     } else {
@@ -836,7 +834,8 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     sp.totals = totals_all;
     sp.totals_local = t->cdf_totals_local;
     sp.mbox = mb;
-    sp.xchg = xchg && !affine;
+    // 1: the sample kernel exchanges; 2: the assign kernel did, read the mailbox
+    sp.xchg = xchg ? (affine ? 2 : 1) : 0;
     sp.cdf_ptrs = t->d_cdf_ptrs;
     sp.gen_ptrs = t->d_gen_ptrs;
     sp.shard_cap = t->Cs;

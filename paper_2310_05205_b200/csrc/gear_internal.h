@@ -101,7 +101,9 @@ __host__ __device__ inline MboxLayout mbox_layout(uint32_t W, uint32_t S, uint32
 struct Mbox {
   uint8_t* base[kMaxRanks];  // base[rank] is this rank's own mailbox
   uint32_t W, rank, S, R, MB;
-  uint64_t epoch;            // this exchange's epoch (>= 1), buffer = epoch & 1
+  uint64_t* epoch_dev;       // this exchange kind's counter (device): the next
+                             // exchange is *epoch_dev + 1; the kernels advance it
+  uint64_t epoch;            // filled in-kernel from epoch_dev (buffer = epoch & 1)
 };
 
 struct CollectCol {
@@ -186,6 +188,7 @@ struct AssignParams {
   Mbox mbox;
   int xchg;                         // 1: exchange the totals through the mailboxes first
   const ShardTotals* fifo_totals;   // FIFO/LIFO: candidate counts [S] (null for draws)
+  int fifo_mbox;                    // 1: FIFO/LIFO counts are in the mailbox (fifo_totals unused)
   const uint32_t* glob_shard;       // FIFO/LIFO merged global list [K] (null for draws)
   const uint32_t* glob_slot;
   uint32_t n_shards;
@@ -217,8 +220,9 @@ void count_launch(uint64_t n = 1);
 // indicator != 0 scans [key > 0] instead of key.
 // status [tiles], ticket and done counter start at 0 and are left at 0 by the
 // kernel itself (the last tile re-arms them), so launches can be replayed.
-cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf, uint64_t shard_cap,
-                        uint32_t n_shards_local, int indicator, uint32_t parity,
+// Builds into cdf1 if the device parity *par_dev is 0, else cdf0, then flips it.
+cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf0, uint64_t* cdf1, uint64_t shard_cap,
+                        uint32_t n_shards_local, int indicator, uint64_t* par_dev,
                         ShardTotals* totals_out, uint64_t* status, uint32_t* ticket,
                         uint32_t* done, cudaStream_t s);
 uint32_t scan_tiles_per_shard(uint64_t shard_cap);
@@ -289,5 +293,7 @@ cudaError_t launch_fifo_merge(const Cand* cand_all, const ShardTotals* totals_al
                               uint32_t* glob_shard, uint32_t* glob_slot, const Mbox* mbox,
                               cudaStream_t s);
 cudaError_t launch_assign(const AssignParams& p, cudaStream_t s);
+// Advances a device-resident exchange epoch by one (FIFO/LIFO exchange).
+cudaError_t launch_epoch_bump(uint64_t* counter, cudaStream_t s);
 
 }  // namespace gear

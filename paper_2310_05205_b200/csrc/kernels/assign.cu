@@ -34,8 +34,19 @@ __global__ void __launch_bounds__(kThreads) assign_kernel(const __grid_constant_
   const uint32_t S = p.n_shards;
   // W > 1 draws: exchange the shard totals through the peer mailboxes here;
   // the sample kernel that follows reads them from this rank's mailbox.
-  const ShardTotals* totals =
-      p.xchg ? mbox_exchange_totals(p.mbox, p.totals_local, p.err) : p.totals;
+  const Mbox mm = (p.xchg || p.fifo_mbox) ? mbox_at_next_epoch(p.mbox) : p.mbox;
+  const ShardTotals* totals = p.totals;
+  if (p.xchg) {
+    totals = mbox_exchange_totals(mm, p.totals_local, p.err);  // ends with a barrier:
+    if (tid == 0) *p.mbox.epoch_dev = mm.epoch;                // every thread read it
+  }
+  // FIFO/LIFO through the mailboxes: the candidate counts of this exchange
+  // (the FIFO epoch advances after this kernel)
+  const ShardTotals* fifo_totals = p.fifo_totals;
+  if (p.fifo_mbox) {
+    const MboxLayout L = mbox_layout(mm.W, mm.S, mm.MB);
+    fifo_totals = mbox_at<ShardTotals>(mm, mm.rank, L.ccnt) + mbox_buf(mm) * mm.S;
+  }
   if (tid < 32) {
     uint64_t Ts = 0;
     if ((uint32_t)lane < S && totals)
@@ -47,9 +58,9 @@ __global__ void __launch_bounds__(kThreads) assign_kernel(const __grid_constant_
   if (tid <= (int)kMaxRanks) s_run[tid] = 0;
   if (tid == 0) {
     s_bail = 0;
-    if (p.fifo_totals) {  // FIFO/LIFO: fewer than K candidates -> EMPTY (merge wrote it)
+    if (fifo_totals) {  // FIFO/LIFO: fewer than K candidates -> EMPTY (merge wrote it)
       uint64_t avail = 0;
-      for (uint32_t s = 0; s < S; ++s) avail += p.fifo_totals[s].aux;
+      for (uint32_t s = 0; s < S; ++s) avail += __ldcg(&fifo_totals[s].aux);
       s_bail = avail < K;
     }
   }

@@ -26,7 +26,8 @@ __global__ void __launch_bounds__(kLocalThreads)
                       const uint32_t* __restrict__ ord, const __grid_constant__ FifoRings rings,
                       uint64_t shard_cap, uint32_t first_shard, uint32_t K, int lifo,
                       Cand* __restrict__ cand_out, ShardTotals* __restrict__ totals_out,
-                      const __grid_constant__ Mbox m, int xchg) {
+                      const __grid_constant__ Mbox m0, int xchg) {
+  const Mbox m = xchg ? mbox_at_next_epoch(m0) : m0;  // the FIFO epoch advances after the step
   __shared__ uint32_t s_warp[kLocalThreads / 32];
   __shared__ uint32_t s_count;
   const uint32_t ls = blockIdx.x;
@@ -125,7 +126,8 @@ __global__ void __launch_bounds__(kMergeThreads)
                       uint32_t B, const uint32_t* const* gen_ptrs, uint32_t shards_per_rank,
                       uint64_t* out_idx, float* out_w, double* out_p, uint32_t* out_gen,
                       uint32_t* err, uint32_t* glob_shard, uint32_t* glob_slot,
-                      const __grid_constant__ Mbox m, int xchg) {
+                      const __grid_constant__ Mbox m0, int xchg) {
+  const Mbox m = xchg ? mbox_at_next_epoch(m0) : m0;  // the FIFO epoch advances after the step
   const uint64_t t = (uint64_t)blockIdx.x * kMergeThreads + threadIdx.x;
   if (xchg) {  // candidates of all S shards arrive in this rank's mailbox
     const MboxLayout L = mbox_layout(m.W, m.S, m.MB);
@@ -208,6 +210,20 @@ cudaError_t launch_fifo_merge(const Cand* cand_all, const ShardTotals* totals_al
                                                    out_idx, out_w, out_p, out_gen, err,
                                                    glob_shard, glob_slot,
                                                    mbox ? *mbox : Mbox{}, mbox != nullptr);
+  return cudaGetLastError();
+}
+
+}  // namespace gear
+
+namespace gear {
+
+namespace {
+__global__ void epoch_bump_u64_kernel(uint64_t* p) { *p += 1; }
+}  // namespace
+
+cudaError_t launch_epoch_bump(uint64_t* counter, cudaStream_t s) {
+  count_launch();
+  epoch_bump_u64_kernel<<<1, 1, 0, s>>>(counter);
   return cudaGetLastError();
 }
 

@@ -48,6 +48,16 @@ __device__ __forceinline__ bool mbox_wait(const uint64_t* flags, uint32_t n, uin
 
 __device__ __forceinline__ uint32_t mbox_buf(const Mbox& m) { return (uint32_t)(m.epoch & 1); }
 
+// The epochs live in device memory so a captured step stays correct when a
+// CUDA graph replays it: a kernel that takes part in exchange e reads
+// e = *epoch_dev + 1 on entry, and exactly one party advances the counter
+// once every reader of this rank is done (see each kernel).
+__device__ __forceinline__ Mbox mbox_at_next_epoch(const Mbox& m) {
+  Mbox r = m;
+  r.epoch = ld_relaxed_u64(m.epoch_dev) + 1;
+  return r;
+}
+
 template <class T>
 __device__ __forceinline__ T* mbox_at(const Mbox& m, uint32_t r, uint64_t off) {
   return reinterpret_cast<T*>(m.base[r] + off);

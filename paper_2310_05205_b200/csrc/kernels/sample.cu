@@ -66,8 +66,16 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
 
   // W > 1: every block publishes this rank's shard totals into every peer's
   // mailbox over NVLink and waits for all peers' (mbox.cuh).
-  const ShardTotals* totals = p.xchg ? mbox_exchange_totals(p.mbox, p.totals_local, p.err)
-                                     : p.totals;
+  // xchg 2: the owner-affine assign kernel already exchanged them (and
+  // advanced the epoch): read this rank's mailbox at the current epoch.
+  const Mbox mm = p.xchg ? mbox_at_next_epoch(p.mbox) : p.mbox;
+  const ShardTotals* totals = p.totals;
+  if (p.xchg == 1) {
+    totals = mbox_exchange_totals(mm, p.totals_local, p.err);
+  } else if (p.xchg == 2) {
+    const MboxLayout L = mbox_layout(mm.W, mm.S, mm.MB);
+    totals = mbox_at<ShardTotals>(mm, mm.rank, L.totals) + ((mm.epoch - 1) & 1) * mm.S;
+  }
   // Shard totals -> exclusive offsets (S <= 32: one lane per shard).
   const uint32_t S = p.n_shards;
   uint64_t Ts = 0;
@@ -115,7 +123,8 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
     my_q = T > 0 ? q : ~0ull;
   }
   const bool need_w = prioritized && p.out_w != nullptr;
-  if (!need_w && !p.seed_dev) return;
+  const bool bump_epoch = p.xchg == 1;  // this kernel ran the exchange
+  if (!need_w && !p.seed_dev && !bump_epoch) return;
 
   // Slice-wide q_min, then the last block writes the weights (and advances
   // the device seed counter).
@@ -144,6 +153,7 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
     *p.qmin_slot = ~0ull;
     *p.done_ctr = 0;
     if (p.seed_dev) *p.seed_dev = seed + 1;
+    if (bump_epoch) *p.mbox.epoch_dev = mm.epoch;  // every block has read it
   }
 }
 

@@ -35,9 +35,14 @@ __device__ __forceinline__ int pad(int e) { return e + (e >> 4); }
 
 template <bool kIndicator>
 __global__ void __launch_bounds__(kThreads) scan_kernel(
-    const uint64_t* __restrict__ key, uint64_t* __restrict__ cdf, uint64_t shard_cap,
-    uint32_t tiles_per_shard, uint32_t n_tiles, uint32_t parity, ShardTotals* totals,
-    uint64_t* status, uint32_t* ticket, uint32_t* done) {
+    const uint64_t* __restrict__ key, uint64_t* __restrict__ cdf0, uint64_t* __restrict__ cdf1,
+    uint64_t shard_cap, uint32_t tiles_per_shard, uint32_t n_tiles, uint64_t* par_dev,
+    ShardTotals* totals, uint64_t* status, uint32_t* ticket, uint32_t* done) {
+  // The CDF is rebuilt into the buffer peers are NOT reading: the parity of
+  // the last build lives in device memory (graph-replayable) and is flipped
+  // by the last tile; the parity travels with the shard totals.
+  const uint32_t parity = (uint32_t)(ld_relaxed_u64(par_dev) & 1) ^ 1u;
+  uint64_t* __restrict__ cdf = parity ? cdf1 : cdf0;
   __shared__ uint64_t s_k[kTile + kTile / 16];
   __shared__ uint32_t s_tile;
   __shared__ uint64_t s_warp[kThreads / 32];
@@ -174,6 +179,7 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(
     if (tid == 0) {
       *ticket = 0;
       *done = 0;
+      *par_dev = parity;  // every tile read the old parity before counting done
     }
   }
 }
@@ -184,19 +190,19 @@ uint32_t scan_tiles_per_shard(uint64_t shard_cap) {
   return (uint32_t)((shard_cap + kTile - 1) / kTile);
 }
 
-cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf, uint64_t shard_cap,
-                        uint32_t n_shards_local, int indicator, uint32_t parity,
+cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf0, uint64_t* cdf1, uint64_t shard_cap,
+                        uint32_t n_shards_local, int indicator, uint64_t* par_dev,
                         ShardTotals* totals_out, uint64_t* status, uint32_t* ticket,
                         uint32_t* done, cudaStream_t s) {
   const uint32_t tps = scan_tiles_per_shard(shard_cap);
   const uint32_t n_tiles = tps * n_shards_local;
   count_launch();
   if (indicator)
-    scan_kernel<true><<<n_tiles, kThreads, 0, s>>>(key, cdf, shard_cap, tps, n_tiles, parity,
-                                                   totals_out, status, ticket, done);
+    scan_kernel<true><<<n_tiles, kThreads, 0, s>>>(key, cdf0, cdf1, shard_cap, tps, n_tiles,
+                                                   par_dev, totals_out, status, ticket, done);
   else
-    scan_kernel<false><<<n_tiles, kThreads, 0, s>>>(key, cdf, shard_cap, tps, n_tiles, parity,
-                                                    totals_out, status, ticket, done);
+    scan_kernel<false><<<n_tiles, kThreads, 0, s>>>(key, cdf0, cdf1, shard_cap, tps, n_tiles,
+                                                    par_dev, totals_out, status, ticket, done);
   return cudaGetLastError();
 }
 

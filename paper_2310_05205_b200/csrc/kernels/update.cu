@@ -167,11 +167,12 @@ __global__ void __launch_bounds__(kFusedThreads)
 __global__ void __launch_bounds__(kFusedThreads)
     xchg_kernel(const uint64_t* __restrict__ idx, const void* __restrict__ prio, int prio_is_f64,
                 const uint32_t* __restrict__ gen_in, uint32_t n, uint64_t n_global,
-                uint32_t frac_bits, uint64_t q_max, const __grid_constant__ Mbox mb,
+                uint32_t frac_bits, uint64_t q_max, const __grid_constant__ Mbox mb0,
                 uint64_t local_begin, uint64_t local_rows, const uint32_t* __restrict__ gen,
                 unsigned long long* tag, uint32_t* epoch_dev, unsigned long long* n_stale,
                 uint32_t* err, uint64_t* key) {
   const uint32_t epoch = *epoch_dev + 1;  // device-resident tag epoch
+  const Mbox mb = mbox_at_next_epoch(mb0);  // device-resident exchange epoch
   const MboxLayout L = mbox_layout(mb.W, mb.S, mb.MB);
   const uint32_t bsel = mbox_buf(mb);
   uint32_t e = 0;
@@ -239,7 +240,10 @@ __global__ void __launch_bounds__(kFusedThreads)
       key[loc[u]] = r[u].q;
   }
   __syncthreads();  // every thread has read the epoch before it advances
-  if (threadIdx.x == 0) *epoch_dev = epoch;
+  if (threadIdx.x == 0) {
+    *epoch_dev = epoch;
+    *mb0.epoch_dev = mb.epoch;
+  }
 }
 
 __global__ void epoch_bump_kernel(uint32_t* epoch_dev) { *epoch_dev += 1; }

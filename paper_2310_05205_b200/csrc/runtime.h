@@ -107,7 +107,6 @@ struct gear_table {
   uint64_t* scan_status[2] = {nullptr, nullptr};
   uint32_t* scan_ticket[2] = {nullptr, nullptr};
   uint64_t scan_launches = 0;
-  int cdf_parity = 1;     // parity of the last built buffer (first build -> 0)
   int cdf_mode = -1;      // -1 none, 0 weighted keys, 1 indicator
   bool dirty = true;
   gear::ShardTotals* cdf_totals_local = nullptr;  // [R]
@@ -131,7 +130,9 @@ struct gear_table {
   uint8_t* mbox = nullptr;
   gear::Mbox mb{};
   std::vector<void*> mbox_opened;
-  uint64_t ep_totals = 0, ep_upd = 0, ep_fifo = 0;
+  // device counters [4]: totals / update / FIFO exchange epochs, CDF parity
+  // (device-resident so that captured steps replay correctly)
+  uint64_t* d_xep = nullptr;
   int peer_xchg = 1;                 // 1: mailbox exchanges, 0: NCCL all-gathers
 
   uint32_t* draw_list = nullptr;     // [max_batch] owner-affine slice -> draw number

@@ -117,6 +117,81 @@ def run_case(comm, W, rank, R, placements, removal, Cs=700, B=40, steps=3, xchg=
     t.close()
 
 
+def run_graph_case(comm, W, rank, R=2, Cs=500, B=48, reps=4):
+    """Every rank captures sample(owner-affine, device seed) -> collect ->
+    update once as a CUDA graph and replays it: the mailbox epochs, the CDF
+    parity, the update epoch and the seed are device-resident, so each replay
+    is a new collective step and must match the oracle."""
+    cols = [gear.Column("a", gear.GEAR_F32, (6,)), gear.Column("b", gear.GEAR_U8, (5,))]
+    S = W * R
+    N = S * Cs
+    t = gear.Table(N, 2, cols, comm, shards_per_rank=R, max_batch=256)
+    o = oracle.Table(Cs, S)
+    prio_all = synth.priorities(N, seed=21, zero_frac=0.05)
+    for s in range(S):
+        st, oidx = o.insert(s, prio_all[s * Cs:(s + 1) * Cs])
+        if s // R == rank:
+            traj = np.arange(s * Cs, (s + 1) * Cs)
+            rows = [torch.from_numpy(synth.row_bytes_of(c, traj, t.row_bytes[c])).cuda() for c in range(2)]
+            t.insert(s, rows, prio_all[s * Cs:(s + 1) * Cs])
+    torch.cuda.synchronize()
+    dist.barrier()
+    seed0 = 777
+    gear.gear_table_set_tuning(t.handle, "device_seed", seed0)
+    idx = torch.empty(B, dtype=torch.int64, device="cuda")
+    w = torch.empty(B, dtype=torch.float32, device="cuda")
+    outs = [torch.empty((B, rb), dtype=torch.uint8, device="cuda") for rb in t.row_bytes]
+    newp = [np.random.default_rng(50 + r).lognormal(0, 1, B) for r in range(W)]
+    dnewp = torch.from_numpy(newp[rank]).cuda()
+    strat = gear.GEAR_PRIORITIZED | gear.GEAR_SAMPLE_OWNER_AFFINE | gear.GEAR_SAMPLE_DEVICE_SEED
+
+    def step():
+        gear.gear_sample(t.handle, strat, B, 0, 0.4, idx, w)
+        gear.gear_collect(t.handle, B, idx, [0, 1], outs)
+        gear.gear_update_priorities(t.handle, B, idx, dnewp, gear.GEAR_F64)
+
+    step()                                   # eager step (seed0), also warms up
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    sgraph = torch.cuda.Stream()
+    sgraph.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(sgraph):
+        with torch.cuda.graph(g, stream=sgraph, capture_error_mode="thread_local"):
+            step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    got = []
+    with torch.cuda.stream(sgraph):
+        for _ in range(reps):
+            g.replay()
+            sgraph.synchronize()
+            got.append((idx.cpu().numpy().view(np.uint64).copy(), w.cpu().numpy().copy(),
+                        [x.cpu().numpy().copy() for x in outs]))
+    err, _ = t.sync()
+    assert err == 0, err
+    content = np.arange(N)
+    for i in range(reps + 1):
+        seed = seed0 + i
+        lists = []
+        for r in range(W):
+            st, oi, ow, _ = o.sample(oracle.PRIORITIZED, W, r, B, seed, 0.4, owner_affine=True)
+            assert st == 0
+            lists.append(oi)
+            if r == rank and i >= 1:
+                gi, gw, gouts = got[i - 1]
+                assert np.array_equal(gi, oi), f"graph replay {i}: ids differ"
+                np.testing.assert_allclose(gw, ow, rtol=1e-6)
+                for c in range(2):
+                    want = synth.row_bytes_of(c, content[oi.astype(np.int64)], t.row_bytes[c])
+                    assert np.array_equal(gouts[c], want)
+        for r in range(W):
+            o.update(lists[r], newp[r])
+    key, _, _ = t.read_state()
+    lo, hi = rank * R * Cs, (rank + 1) * R * Cs
+    assert np.array_equal(key, o.key[lo:hi]), "keys after the replayed collective updates"
+    t.close()
+
+
 def main():
     W = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
@@ -132,6 +207,10 @@ def main():
         dist.barrier()
         if rank == 0:
             print(f"case R={R} placements={pl} removal={removal} peer_xchg={xchg}: ok", flush=True)
+    run_graph_case(comm, W, rank)
+    dist.barrier()
+    if rank == 0:
+        print("case graph replay (owner-affine, device seed): ok", flush=True)
     gear.gear_comm_destroy(comm)
     dist.destroy_process_group()
     print(f"rank {rank}: all multi-GPU parity cases ok", flush=True)
