@@ -86,13 +86,17 @@ typedef enum { GEAR_DEVICE = 0, GEAR_HOST = 1 } gear_placement;
  * oldest / newest selectable trajectories (decentralised);
  * UNIFORM/WEIGHTED/PRIORITIZED draw W*B ids with replacement from the CDF of
  * [key>0] / key (centralised).  PRIORITIZED also returns
- * importance-sampling weights (q_min/q)^beta over the rank's slice. */
+ * importance-sampling weights (q_min/q)^beta over the rank's slice.  TOPK
+ * (decentralised like FIFO) selects the W*B selectable
+ * trajectories with the largest priority keys, ties by the smaller global id,
+ * in that order (W*B <= 8192). */
 typedef enum {
   GEAR_FIFO = 0,
   GEAR_LIFO = 1,
   GEAR_UNIFORM = 2,
   GEAR_WEIGHTED = 3,
-  GEAR_PRIORITIZED = 4
+  GEAR_PRIORITIZED = 4,
+  GEAR_TOPK = 5
 } gear_strategy;
 
 /* Flag OR-ed into the strategy of gear_sample: owner-affine assignment of
@@ -109,8 +113,9 @@ typedef enum {
  * device-resident seed counter instead of the `seed` argument, and the call
  * advances the counter on the device (set it with gear_table_set_tuning(t,
  * "device_seed", value)).  Consecutive calls use value, value+1, ... even when
- * the calls are captured once in a CUDA graph and replayed.  W = 1 only for
- * graph replay: the W > 1 mailbox epochs are host-side. */
+ * the calls are captured once in a CUDA graph and replayed (every other
+ * per-call counter -- update epoch, mailbox epochs, CDF parity -- is
+ * device-resident too, so captured steps replay correctly at any W). */
 #define GEAR_SAMPLE_DEVICE_SEED 0x200
 
 /* Victim choice when a shard is full. */

@@ -22,7 +22,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gear_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-FIFO, LIFO, UNIFORM, WEIGHTED, PRIORITIZED = 0, 1, 2, 3, 4
+FIFO, LIFO, UNIFORM, WEIGHTED, PRIORITIZED, TOPK = 0, 1, 2, 3, 4, 5
 OK, BAD_PRIORITY, INDEX_RANGE, STALE, EMPTY, INVALID = 0, 1, 2, 4, 8, 16
 IDX_NONE = np.uint64(0xFFFFFFFFFFFFFFFF)
 

@@ -162,6 +162,32 @@ int gor_sample(int strategy, const uint64_t* key, const uint64_t* seq,
     return GOR_OK;
   }
 
+  if (strategy == GOR_TOPK) {
+    /* Q20: sort every selectable slot by (key descending, global id
+     * ascending) and take the first K; rank keeps [rank*B, rank*B+B).  The
+     * comparator negates the key through the `seq` field: sort ascending by
+     * (-key, g) written as (UINT64_MAX - key, g). */
+    gor_cand* c = (gor_cand*)malloc(sizeof(gor_cand) * (n ? n : 1));
+    uint64_t m = 0;
+    for (uint64_t g = 0; g < n; ++g) {
+      if (key[g] > 0) {
+        c[m].seq = UINT64_MAX - key[g];
+        c[m].shard = 0;      /* ties go by global id alone */
+        c[m].g = g;
+        ++m;
+      }
+    }
+    if (m < K) { free(c); return GOR_EMPTY; }
+    qsort(c, m, sizeof(gor_cand), gor_cand_cmp);
+    for (uint32_t b = 0; b < B; ++b) {
+      out_idx[b] = c[(uint64_t)rank * B + b].g;
+      if (out_w) out_w[b] = 1.0f;
+      if (out_p) out_p[b] = 1.0;
+    }
+    free(c);
+    return GOR_OK;
+  }
+
   if (strategy != GOR_UNIFORM && strategy != GOR_WEIGHTED && strategy != GOR_PRIORITIZED)
     return GOR_INVALID;
 

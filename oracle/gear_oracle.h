@@ -42,6 +42,10 @@ extern "C" {
 #define GOR_UNIFORM 2
 #define GOR_WEIGHTED 3
 #define GOR_PRIORITIZED 4
+/* TopK ("GEAR provides FIFO and TopK selection"; reading
+ * Q20): the n_ranks*B selectable slots with the largest keys, ties by the
+ * smaller global id, in that order. */
+#define GOR_TOPK 5
 
 /* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11 "Parallel random numbers:
  * as easy as 1, 2, 3"); the counter-based RNG of reading Q4, which supplies

@@ -44,13 +44,13 @@ GEAR_IDX_NONE = 0xFFFFFFFFFFFFFFFF
 # dtypes / placements / strategies / removal (gear.h enums)
 GEAR_U8, GEAR_I32, GEAR_I64, GEAR_F32, GEAR_F64, GEAR_BF16 = range(6)
 GEAR_DEVICE, GEAR_HOST = 0, 1
-GEAR_FIFO, GEAR_LIFO, GEAR_UNIFORM, GEAR_WEIGHTED, GEAR_PRIORITIZED = range(5)
+GEAR_FIFO, GEAR_LIFO, GEAR_UNIFORM, GEAR_WEIGHTED, GEAR_PRIORITIZED, GEAR_TOPK = range(6)
 GEAR_REMOVE_FIFO, GEAR_REMOVE_LIFO = 0, 1
 GEAR_SAMPLE_OWNER_AFFINE = 0x100
 GEAR_SAMPLE_DEVICE_SEED = 0x200
 
 STRATEGIES = {"fifo": GEAR_FIFO, "lifo": GEAR_LIFO, "uniform": GEAR_UNIFORM,
-              "weighted": GEAR_WEIGHTED, "prioritized": GEAR_PRIORITIZED}
+              "weighted": GEAR_WEIGHTED, "prioritized": GEAR_PRIORITIZED, "topk": GEAR_TOPK}
 DTYPES = {"u8": GEAR_U8, "i32": GEAR_I32, "i64": GEAR_I64, "f32": GEAR_F32, "f64": GEAR_F64,
           "bf16": GEAR_BF16}
 DTYPE_BYTES = {GEAR_U8: 1, GEAR_I32: 4, GEAR_I64: 8, GEAR_F32: 4, GEAR_F64: 8, GEAR_BF16: 2}

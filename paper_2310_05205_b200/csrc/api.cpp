@@ -740,7 +740,7 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
   const bool dseed = ((uint32_t)strategy & GEAR_SAMPLE_DEVICE_SEED) != 0;
   strategy = (gear_strategy)((uint32_t)strategy &
                              ~(uint32_t)(GEAR_SAMPLE_OWNER_AFFINE | GEAR_SAMPLE_DEVICE_SEED));
-  if (strategy < GEAR_FIFO || strategy > GEAR_PRIORITIZED)
+  if (strategy < GEAR_FIFO || strategy > GEAR_TOPK)
     return set_error(GEAR_ERR_INVALID_ARG, "bad strategy %d", (int)strategy);
   if (B > t->max_batch) return set_error(GEAR_ERR_INVALID_ARG, "B %u > max_batch %u", B, t->max_batch);
   if (B == 0) return GEAR_OK;
@@ -756,23 +756,30 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
   double* d_p = out_p ? (h_p ? t->tmp_p : out_p) : nullptr;
   uint32_t* d_gen = out_gen ? (h_gen ? t->tmp_gen : out_gen) : nullptr;
 
-  if (strategy == GEAR_FIFO || strategy == GEAR_LIFO) {
+  if (strategy == GEAR_FIFO || strategy == GEAR_LIFO || strategy == GEAR_TOPK) {
     const uint32_t K = t->W * B;
+    const bool topk = strategy == GEAR_TOPK;
+    if (topk && K > topk_max_k())
+      return set_error(GEAR_ERR_UNSUPPORTED, "TopK needs W*B <= %u (got %u)", topk_max_k(), K);
     FifoRings rings{};
     for (uint32_t ls = 0; ls < t->R; ++ls) {
       rings.head[ls] = t->rings[ls].head;
       rings.len[ls] = t->rings[ls].len;
     }
-    const int lifo = strategy == GEAR_LIFO;
+    const int lifo = topk ? 2 : (strategy == GEAR_LIFO ? 1 : 0);  // merge order
     const bool xchg = t->W > 1 && t->peer_xchg;
     Mbox mb = t->mb;
     const ShardTotals* fifo_totals = t->fifo_totals_all;
     // candidates go straight into every peer's mailbox from the local kernel;
     // the FIFO-exchange epoch advances after the merge (and assignment)
     mb.epoch_dev = t->d_xep + 2;
-    GEAR_CUDA(launch_fifo_local(t->key, t->seq, t->ord, rings, t->Cs, t->R, t->rank * t->R, K,
-                                lifo, t->cand_local, t->fifo_totals_local, xchg ? &mb : nullptr,
-                                s));
+    if (topk)
+      GEAR_CUDA(launch_topk_local(t->key, t->Cs, t->R, t->rank * t->R, K, t->cand_local,
+                                  t->fifo_totals_local, xchg ? &mb : nullptr, s));
+    else
+      GEAR_CUDA(launch_fifo_local(t->key, t->seq, t->ord, rings, t->Cs, t->R, t->rank * t->R, K,
+                                  lifo, t->cand_local, t->fifo_totals_local, xchg ? &mb : nullptr,
+                                  s));
     const Cand* cand_all = t->cand_all;
     const ShardTotals* merge_totals = t->fifo_totals_all;
     if (t->W == 1) {  // the local lists are all the lists

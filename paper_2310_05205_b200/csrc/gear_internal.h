@@ -293,6 +293,12 @@ cudaError_t launch_fifo_merge(const Cand* cand_all, const ShardTotals* totals_al
                               uint32_t* glob_shard, uint32_t* glob_slot, const Mbox* mbox,
                               cudaStream_t s);
 cudaError_t launch_assign(const AssignParams& p, cudaStream_t s);
+// TopK local selection (kernels/topk.cu): sorted top-K of each local shard;
+// merged by launch_fifo_merge with lifo == 2.  K <= topk_max_k().
+uint32_t topk_max_k();
+cudaError_t launch_topk_local(const uint64_t* key, uint64_t shard_cap, uint32_t n_shards_local,
+                              uint32_t first_shard, uint32_t K, Cand* cand_out,
+                              ShardTotals* totals_out, const Mbox* mbox, cudaStream_t s);
 // Advances a device-resident exchange epoch by one (FIFO/LIFO exchange).
 cudaError_t launch_epoch_bump(uint64_t* counter, cudaStream_t s);
 

@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(kLocalThreads)
 }
 
 // Number of entries of the sorted list c[0..n) that order before (sq, s)
-// under (seq, shard) -- ascending lists for FIFO, descending for LIFO.
+// under (seq, shard) -- ascending lists for FIFO, descending for LIFO, and
+// (key descending, shard ascending) for TopK (lifo == 2, topk.cu).
 __device__ __forceinline__ uint32_t count_before(const Cand* __restrict__ c, uint32_t n,
                                                  uint32_t list_shard, uint64_t sq, uint32_t s,
                                                  int lifo) {
@@ -112,8 +113,9 @@ __device__ __forceinline__ uint32_t count_before(const Cand* __restrict__ c, uin
     const uint32_t mid = (lo + hi) >> 1;
     const uint64_t e = c[mid].seq;
     bool b;
-    if (!lifo) b = e < sq || (e == sq && list_shard < s);
-    else b = e > sq || (e == sq && list_shard > s);
+    if (lifo == 0) b = e < sq || (e == sq && list_shard < s);        // FIFO
+    else if (lifo == 1) b = e > sq || (e == sq && list_shard > s);   // LIFO
+    else b = e > sq || (e == sq && list_shard < s);                  // TopK (seq = key)
     if (b) lo = mid + 1;
     else hi = mid;
   }

@@ -25,7 +25,8 @@ import synth  # noqa: E402
 import paper_2310_05205_b200 as gear  # noqa: E402
 
 OS = {gear.GEAR_FIFO: oracle.FIFO, gear.GEAR_LIFO: oracle.LIFO, gear.GEAR_UNIFORM: oracle.UNIFORM,
-      gear.GEAR_WEIGHTED: oracle.WEIGHTED, gear.GEAR_PRIORITIZED: oracle.PRIORITIZED}
+      gear.GEAR_WEIGHTED: oracle.WEIGHTED, gear.GEAR_PRIORITIZED: oracle.PRIORITIZED,
+      gear.GEAR_TOPK: oracle.TOPK}
 
 
 def run_case(comm, W, rank, R, placements, removal, Cs=700, B=40, steps=3, xchg=1):
@@ -68,7 +69,7 @@ def run_case(comm, W, rank, R, placements, removal, Cs=700, B=40, steps=3, xchg=
 
     for step in range(steps):
         for strat in (gear.GEAR_UNIFORM, gear.GEAR_WEIGHTED, gear.GEAR_PRIORITIZED, gear.GEAR_FIFO,
-                      gear.GEAR_LIFO):
+                      gear.GEAR_LIFO, gear.GEAR_TOPK):
             seed = synth.SAMPLE_SEED_BASE + 100 * step + strat
             idx = torch.empty(B, dtype=torch.int64, device="cuda")
             w = torch.empty(B, dtype=torch.float32, device="cuda")

@@ -11,7 +11,7 @@ import paper_2310_05205_b200 as gear
 DT = {"u8": gear.GEAR_U8, "i32": gear.GEAR_I32, "f32": gear.GEAR_F32}
 ORACLE_STRATEGY = {gear.GEAR_FIFO: oracle.FIFO, gear.GEAR_LIFO: oracle.LIFO,
                    gear.GEAR_UNIFORM: oracle.UNIFORM, gear.GEAR_WEIGHTED: oracle.WEIGHTED,
-                   gear.GEAR_PRIORITIZED: oracle.PRIORITIZED}
+                   gear.GEAR_PRIORITIZED: oracle.PRIORITIZED, gear.GEAR_TOPK: oracle.TOPK}
 
 
 class Pair:

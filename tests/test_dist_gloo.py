@@ -134,6 +134,29 @@ def _w_fifo_merge(rank, world, lifo):
     assert st == 0 and mine == [int(x) for x in want]
 
 
+def _w_topk_merge(rank, world):
+    """Decentralised TopK: each rank's shards offer their
+    local top-K by (key desc, id asc); the merge of the all-gathered lists
+    equals the oracle's global TopK."""
+    import oracle
+    R, Cs, B = 2, 80, 9
+    S, K = world * R, world * B
+    rng = np.random.default_rng(8)
+    key = rng.integers(0, 5, size=S * Cs).astype(np.uint64)     # heavy ties
+    cands = []
+    for s in range(rank * R, (rank + 1) * R):
+        g = np.arange(s * Cs, (s + 1) * Cs)
+        g = g[key[g] > 0]
+        top = sorted(g.tolist(), key=lambda x: (-int(key[x]), x))[:K]
+        cands += [(-int(key[x]), x) for x in top]
+    allc = [None] * world
+    dist.all_gather_object(allc, cands)
+    merged = sorted(c for cs in allc for c in cs)
+    mine = [g for _, g in merged[rank * B:(rank + 1) * B]]
+    st, want, _, _ = oracle.sample(oracle.TOPK, key, None, Cs, S, world, rank, B, 0)
+    assert st == 0 and mine == [int(x) for x in want]
+
+
 def _w_max_over_ranks(rank, world):
     ms = torch.tensor([1.0 + rank, 10.0 - rank])
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
@@ -151,6 +174,7 @@ def _w_misc(rank, world):
     _w_max_over_ranks(rank, world)
     for lifo in (0, 1):
         _w_fifo_merge(rank, world, lifo)
+    _w_topk_merge(rank, world)
 
 
 # ---------------------------------------------------------------- tests

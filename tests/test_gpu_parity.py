@@ -166,6 +166,35 @@ def test_fifo_lifo_with_ring_wrap(torch_cuda, removal, R):
     P.close()
 
 
+@pytest.mark.parametrize("R", [1, 3])
+def test_topk_with_ties(torch_cuda, R):
+    """TopK (Q20) on keys with many ties (priorities drawn
+    from 7 values) and zeros, several K including the all-selectable and the
+    EMPTY cases, a shard larger than one 1024-key chunk."""
+    cols = [synth.ColSpec("x", "u8", (4,))]
+    Cs = 2500
+    P = _pair(capacity=Cs * R, seq_len=1, colspecs=cols, R=R)
+    rng = np.random.default_rng(31)
+    vals = np.array([0.0, 0.25, 0.5, 1.0, 2.0, 3.0, 1e-3])
+    P.fill(vals[rng.integers(0, len(vals), size=Cs * R)])
+    sel = int((P.o.key > 0).sum())
+    for B in (1, 5, 64, 700, min(sel // 2, 4096)):
+        idx = P.check_sample(G.GEAR_TOPK, B, 0)
+        assert idx is not None
+        P.check_collect(idx)
+    ids = np.arange(0, Cs * R, 7, dtype=np.uint64)
+    P.update(ids, rng.lognormal(0, 1, ids.size))
+    P.check_sample(G.GEAR_TOPK, 333, 0)
+    # few selectable: all of them, then one more than there are -> EMPTY
+    P.update(np.arange(Cs * R, dtype=np.uint64)[:3000], np.zeros(3000))
+    left = int((P.o.key > 0).sum())
+    if left <= 4096:
+        assert P.check_sample(G.GEAR_TOPK, left, 0) is not None
+    if left + 1 <= 4096:
+        assert P.check_sample(G.GEAR_TOPK, left + 1, 0) is None
+    P.close()
+
+
 def test_insert_bad_priority_and_device_sources(torch_cuda):
     cols = [synth.ColSpec("a", "u8", (7,)), synth.ColSpec("b", "i32", (3,))]
     P = _pair(capacity=64, seq_len=3, colspecs=cols, R=2)

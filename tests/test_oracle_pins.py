@@ -448,3 +448,31 @@ def test_owner_affine_partitions_the_global_batch(oracle_mod, strategy):
         assert sorted(np.concatenate(slices).tolist()) == sorted(glob.tolist())
         if W == 1:
             assert np.array_equal(slices[0], glob)
+
+
+# --------------------------------------------------------------------------
+# TopK (reading Q20): brute force on small tables
+# --------------------------------------------------------------------------
+def test_topk_matches_brute_force(oracle_mod):
+    rng = np.random.default_rng(40)
+    for trial in range(60):
+        S = int(rng.integers(1, 5))
+        Cs = int(rng.integers(1, 40))
+        key = rng.integers(0, 6, size=S * Cs).astype(np.uint64)   # many ties
+        key[rng.random(S * Cs) < 0.2] = 0
+        sel = [g for g in range(S * Cs) if key[g] > 0]
+        brute = sorted(sel, key=lambda g: (-int(key[g]), g))
+        for W in (1, 2, 3):
+            B = int(rng.integers(1, 6))
+            if len(sel) < W * B:
+                st, *_ = oracle_mod.sample(oracle_mod.TOPK, key, None, Cs, S, W, 0, B, 0)
+                assert st == oracle_mod.EMPTY
+                continue
+            for r in range(W):
+                st, idx, w, p = oracle_mod.sample(oracle_mod.TOPK, key, None, Cs, S, W, r, B, 0)
+                assert st == 0
+                assert [int(x) for x in idx] == brute[r * B:(r + 1) * B]
+        if sel:
+            st, idx, _, _ = oracle_mod.sample(oracle_mod.TOPK, key, None, Cs, S, 1, 0, len(sel), 0)
+            ks = key[idx.astype(np.int64)]
+            assert np.all(ks[:-1] >= ks[1:])                      # non-increasing keys
