@@ -267,6 +267,17 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
  * be NULL.  Returns STATE if any bit was set, else OK. */
 gear_status gear_table_sync(gear_table* t, uint32_t* dev_errors, uint64_t* n_stale);
 
+/* Shard checkpoint ("GEAR allows for trajectory shards to
+ * be checkpointed on local SSDs").  gear_table_save writes this rank's R
+ * shards -- keys, seq, gen, insertion rings and every column's rows -- to
+ * `path` (one file per rank; pass a rank-specific path).  gear_table_load
+ * restores such a file into a table created with the same descriptor, world
+ * and rank (INVALID_ARG otherwise); the CDF is rebuilt by the next sample.
+ * Both synchronise the device and must not overlap other calls on the
+ * table; neither is collective. */
+gear_status gear_table_save(gear_table* t, const char* path);
+gear_status gear_table_load(gear_table* t, const char* path);
+
 /* Tuning knobs of the collect kernel (not collective, no device work):
  *   "collect_impl": 1 = rows >= 4 KB with 16-byte alignment move by TMA bulk
  *                   copies through shared memory (default), 0 = every row

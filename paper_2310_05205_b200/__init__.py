@@ -105,6 +105,8 @@ SIGNATURES = {
     "gear_table_sync": ([_P, _P, _P], _i32),
     "gear_read_state": ([_P, _P, _P, _P], _i32),
     "gear_table_set_tuning": ([_P, ctypes.c_char_p, ctypes.c_int64], _i32),
+    "gear_table_save": ([_P, ctypes.c_char_p], _i32),
+    "gear_table_load": ([_P, ctypes.c_char_p], _i32),
 }
 
 _lib = None
@@ -295,6 +297,14 @@ def gear_table_set_tuning(t: int, key: str, value: int):
     _check("gear_table_set_tuning", load().gear_table_set_tuning(t, key.encode(), value))
 
 
+def gear_table_save(t: int, path: str):
+    _check("gear_table_save", load().gear_table_save(t, str(path).encode()))
+
+
+def gear_table_load(t: int, path: str):
+    _check("gear_table_load", load().gear_table_load(t, str(path).encode()))
+
+
 class Table:
     """Thin owner of a gear_table handle (destroys it on close)."""
 
@@ -334,3 +344,9 @@ class Table:
 
     def read_state(self):
         return gear_read_state(self.handle)
+
+    def save(self, path):
+        gear_table_save(self.handle, path)
+
+    def load(self, path):
+        gear_table_load(self.handle, path)
