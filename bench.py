@@ -441,7 +441,7 @@ def cpu_baseline(cfg, capacity, prio_all, budget_s=15.0, max_steps=1000):
     for k0 in range(0, capacity, 1 << 20):
         o.insert(0, prio_all[k0:k0 + (1 << 20)])
     strat = {"prioritized": oracle.PRIORITIZED, "weighted": oracle.WEIGHTED, "uniform": oracle.UNIFORM,
-             "fifo": oracle.FIFO, "lifo": oracle.LIFO}[cfg.strategy]
+             "fifo": oracle.FIFO, "lifo": oracle.LIFO, "topk": oracle.TOPK}[cfg.strategy]
     steps = 0
     t0 = time.perf_counter()
     while True:
@@ -505,7 +505,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--strategy", default=None,
-                    choices=["fifo", "lifo", "uniform", "weighted", "prioritized"],
+                    choices=["fifo", "lifo", "uniform", "weighted", "prioritized", "topk"],
                     help="override the config's strategy")
     ap.add_argument("--graph", type=int, default=1,
                     help="also time the pipelined step captured as a CUDA graph")
