@@ -31,7 +31,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep stdout to the one JSON line
+os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep stdout to the one JSON line:
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # (WARN still prints the version line)
 
 METRIC = "sampled+collected trajectories/sec and collect GB/s vs HBM/PCIe roofline, 1/2/4/8 B200"
 UNIT = "trajectories/s"

@@ -145,6 +145,7 @@ void destroy_table(gear_table* t) {
   dfree(t->q_scratch); dfree(t->qmin_slot); dfree(t->done_ctr);
   dfree(t->tmp_idx); dfree(t->tmp_w); dfree(t->tmp_p); dfree(t->tmp_gen);
   dfree(t->cand_local); dfree(t->cand_all);
+  dfree(t->topk_state); dfree(t->topk_cnt); dfree(t->topk_tmp);
   dfree(t->draw_list); dfree(t->pos_scratch); dfree(t->ov_scratch);
   dfree(t->glob_shard); dfree(t->glob_slot);
   dfree(t->upd_local); dfree(t->upd_all); dfree(t->upd_idx); dfree(t->upd_prio); dfree(t->upd_gen);
@@ -387,6 +388,10 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_TRY(dalloc(&t->glob_slot, K));
   GEAR_TRY(dalloc(&t->cand_local, t->R * K));
   GEAR_TRY(dalloc(&t->cand_all, t->S * K));
+  GEAR_TRY(dalloc(&t->topk_tmp, t->R * K));
+  GEAR_TRY(dalloc(&t->topk_state, t->R));
+  GEAR_CUDA(cudaMemset(t->topk_state, 0, t->R * sizeof(TopkState)));
+  GEAR_TRY(dalloc(&t->topk_cnt, (size_t)t->R * kTopkMaxCtas * 2));
   GEAR_TRY(dalloc(&t->upd_local, MB));
   GEAR_TRY(dalloc(&t->upd_all, K));
   GEAR_TRY(dalloc(&t->upd_idx, MB));
@@ -774,8 +779,9 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     // the FIFO-exchange epoch advances after the merge (and assignment)
     mb.epoch_dev = t->d_xep + 2;
     if (topk)
-      GEAR_CUDA(launch_topk_local(t->key, t->Cs, t->R, t->rank * t->R, K, t->cand_local,
-                                  t->fifo_totals_local, xchg ? &mb : nullptr, s));
+      GEAR_CUDA(launch_topk_local(t->key, t->Cs, t->R, t->rank * t->R, K, t->topk_tmp, t->cand_local,
+                                  t->fifo_totals_local, t->topk_state, t->topk_cnt,
+                                  xchg ? &mb : nullptr, s));
     else
       GEAR_CUDA(launch_fifo_local(t->key, t->seq, t->ord, rings, t->Cs, t->R, t->rank * t->R, K,
                                   lifo, t->cand_local, t->fifo_totals_local, xchg ? &mb : nullptr,

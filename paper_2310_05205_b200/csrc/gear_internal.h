@@ -65,6 +65,22 @@ struct Cand {
   uint32_t slot;  // shard-local slot
 };
 
+// Per-shard state of the multi-CTA TopK radix select (kernels/topk.cu);
+// zero-initialised once, re-armed by the kernels themselves.
+constexpr uint32_t kTopkMaxCtas = 512;  // CTAs per shard
+struct TopkState {
+  unsigned long long max_key;  // stats: largest key
+  uint64_t prefix;             // select: key bits fixed so far (== T* when done)
+  uint64_t mask;
+  uint32_t n_sel;     // stats: selectable keys
+  uint32_t k_remain;  // keys still to take among those matching the prefix
+  int shift;          // next byte to resolve; < 0 when done
+  uint32_t all;       // n_sel <= K: take every selectable key
+  uint32_t ctr;       // last-CTA counter
+  uint32_t pad;
+  uint32_t hist[256];
+};
+
 // Peer mailboxes (W > 1).  Every rank owns one device allocation that all
 // peers map through CUDA IPC and write over NVLink; the small per-step
 // exchanges (shard totals, update records, FIFO/LIFO candidates) are remote
@@ -297,8 +313,9 @@ cudaError_t launch_assign(const AssignParams& p, cudaStream_t s);
 // merged by launch_fifo_merge with lifo == 2.  K <= topk_max_k().
 uint32_t topk_max_k();
 cudaError_t launch_topk_local(const uint64_t* key, uint64_t shard_cap, uint32_t n_shards_local,
-                              uint32_t first_shard, uint32_t K, Cand* cand_out,
-                              ShardTotals* totals_out, const Mbox* mbox, cudaStream_t s);
+                              uint32_t first_shard, uint32_t K, Cand* cand_tmp, Cand* cand_out,
+                              ShardTotals* totals_out, TopkState* state, uint32_t* cnt,
+                              const Mbox* mbox, cudaStream_t s);
 // Advances a device-resident exchange epoch by one (FIFO/LIFO exchange).
 cudaError_t launch_epoch_bump(uint64_t* counter, cudaStream_t s);
 

@@ -5,128 +5,265 @@
 // K = W*B selectable trajectories with the largest keys, ties by the smaller
 // global id, in that order.
 //
-// Local step, one CTA per local shard:
-//  1. count the selectable keys and their maximum (block reduction);
-//  2. if more than K are selectable, radix-select the K-th largest key: one
-//     256-bin shared-memory histogram pass per byte of the key, from the
-//     highest non-zero byte down, keeping only keys that match the prefix
-//     chosen so far -- this yields the threshold key T* and how many keys
-//     equal to T* are needed;
-//  3. compact, in slot order, the keys > T* and the first needed keys == T*
-//     (block ballot scan), into shared memory;
-//  4. bitonic-sort the <= K candidates by (key desc, slot asc) in shared
-//     memory and write them (with W > 1 also into every peer's mailbox).
+// Local step for each of the rank's R shards, spread over the whole GPU
+// (G CTAs per shard, each owning a contiguous slice of the shard's keys):
+//  1. stats: selectable count and maximum key (block reduce + atomics);
+//  2. radix select of the K-th largest key, one launch per key byte from the
+//     top: every CTA histograms the byte of the keys that match the prefix
+//     chosen so far into shared memory and adds it to the shard's global
+//     histogram; the last CTA of the shard (threadfence + counter) picks the
+//     digit, extends the prefix and re-arms the histogram.  The result is the
+//     threshold key T* and the number of keys == T* that complete the K;
+//  3. count: per CTA, the keys > T* and the keys == T* of its slice;
+//  4. write: each CTA turns the counts of the CTAs before it into offsets and
+//     compacts its selected keys in slot order (ties: only the first needed
+//     keys == T* in slot order);
+//  5. sort: rank sort of the <= K candidates by (key desc, slot asc), one
+//     thread per candidate counting the candidates before it in shared memory;
+//     each writes itself at its rank (W > 1: also into every peer's mailbox).
 // The global merge is the FIFO/LIFO merge with the TopK order (fifo.cu).
+// Every launch is stream-ordered and every counter re-arms itself, so the
+// sequence can be captured in a CUDA graph.
 #include "mbox.cuh"
 
 namespace gear {
 
 namespace {
 
-constexpr int kThreads = 1024;
-constexpr int kWarps = kThreads / 32;
+constexpr int kThreads = 256;
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
 
-__device__ __forceinline__ uint32_t block_sum_u32(uint32_t v, uint32_t* s_red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
-  if (lane == 0) s_red[warp] = v;
-  __syncthreads();
-  uint32_t t = 0;
-  for (int w = 0; w < kWarps; ++w) t += s_red[w];
-  __syncthreads();
-  return t;
+struct Slice {
+  uint64_t begin, end;  // slot range of this CTA within its shard
+};
+
+__device__ __forceinline__ Slice cta_slice(uint64_t shard_cap, uint32_t G, uint32_t g) {
+  const uint64_t per = ((shard_cap + G - 1) / G + kThreads - 1) / kThreads * kThreads;
+  Slice s;
+  s.begin = min(shard_cap, (uint64_t)g * per);
+  s.end = min(shard_cap, s.begin + per);
+  return s;
 }
 
-// Candidate order of TopK: larger key first, then smaller slot.
-__device__ __forceinline__ bool before(const Cand& a, const Cand& b) {
-  return a.seq > b.seq || (a.seq == b.seq && a.slot < b.slot);
+// Last CTA of shard `ls` to arrive (threadfence + counter); re-arms it.
+__device__ __forceinline__ bool last_cta(uint32_t* ctr, uint32_t G, bool* s_flag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    *s_flag = atomicAdd(ctr, 1u) == G - 1;
+    if (*s_flag) *ctr = 0;
+  }
+  __syncthreads();
+  if (*s_flag) __threadfence();
+  return *s_flag;
 }
 
 __global__ void __launch_bounds__(kThreads)
-    topk_local_kernel(const uint64_t* __restrict__ key, uint64_t shard_cap, uint32_t first_shard,
-                      uint32_t K, uint32_t Kpow2, Cand* __restrict__ cand_out,
-                      ShardTotals* __restrict__ totals_out, const __grid_constant__ Mbox m0,
-                      int xchg) {
-  extern __shared__ __align__(16) Cand s_sel[];  // [Kpow2]
-  __shared__ uint32_t s_hist[256];
-  __shared__ uint32_t s_red[kWarps];
+    stats_kernel(const uint64_t* __restrict__ key, uint64_t shard_cap, uint32_t G, uint32_t K,
+                 TopkState* st) {
+  __shared__ bool s_last;
   __shared__ unsigned long long s_max;
-  __shared__ uint32_t s_digit, s_need, s_count;
-  const Mbox m = xchg ? mbox_at_next_epoch(m0) : m0;  // the FIFO/TopK epoch advances later
-  const uint32_t ls = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ uint32_t s_cnt;
+  const uint32_t ls = blockIdx.y;
+  const Slice sl = cta_slice(shard_cap, G, blockIdx.x);
   const uint64_t* k = key + (uint64_t)ls * shard_cap;
-  const uint32_t shard = first_shard + ls;
-
-  // 1. selectable count and maximum key
-  if (tid == 0) s_max = 0;
+  if (threadIdx.x == 0) {
+    s_max = 0;
+    s_cnt = 0;
+  }
   __syncthreads();
   uint32_t cnt = 0;
   unsigned long long mx = 0;
-  for (uint64_t i = tid; i < shard_cap; i += kThreads) {
+  for (uint64_t i = sl.begin + threadIdx.x; i < sl.end; i += kThreads) {
     const uint64_t x = k[i];
     cnt += x > 0;
     mx = x > mx ? x : mx;
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
+    cnt += __shfl_xor_sync(kFull, cnt, d);
     const unsigned long long o = __shfl_xor_sync(kFull, mx, d);
     mx = o > mx ? o : mx;
   }
-  if (lane == 0) atomicMax(&s_max, mx);
-  const uint32_t n_sel = block_sum_u32(cnt, s_red);
-
-  // 2. radix select of the K-th largest key (only if needed)
-  uint64_t thr = 1, mask = 0;  // select keys > thr, plus `need` keys == thr
-  uint32_t need = 0;
-  if (n_sel > K) {
-    uint32_t kk = K;  // rank of the wanted key among the keys matching the prefix
-    uint64_t prefix = 0;
-    const int top = s_max ? 63 - __clzll(s_max) : 0;
-    for (int shift = (top / 8) * 8; shift >= 0; shift -= 8) {
-      for (int b = tid; b < 256; b += kThreads) s_hist[b] = 0;
-      __syncthreads();
-      for (uint64_t i = tid; i < shard_cap; i += kThreads) {
-        const uint64_t x = k[i];
-        if (x > 0 && (x & mask) == prefix) atomicAdd(&s_hist[(x >> shift) & 255], 1u);
-      }
-      __syncthreads();
-      if (tid == 0) {  // walk the digits from the top
-        uint32_t above = 0;
-        int v = 255;
-        for (; v > 0; --v) {
-          if (above + s_hist[v] >= kk) break;
-          above += s_hist[v];
-        }
-        s_digit = (uint32_t)v;
-        s_need = kk - above;
-      }
-      __syncthreads();
-      prefix |= (uint64_t)s_digit << shift;
-      mask |= 255ull << shift;
-      kk = s_need;
-      __syncthreads();
-    }
-    thr = prefix;  // the K-th largest key
-    need = kk;     // how many keys equal to thr complete the K
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&s_cnt, cnt);
+    atomicMax(&s_max, mx);
   }
-  const bool all = n_sel <= K;
-
-  // 3. stable compaction in slot order into shared memory
-  if (tid == 0) s_count = 0;
-  uint32_t eq_seen = 0;  // keys == thr passed so far (block-uniform)
   __syncthreads();
-  for (uint64_t i0 = 0; i0 < shard_cap; i0 += kThreads) {
+  TopkState& S = st[ls];
+  if (threadIdx.x == 0) {
+    atomicAdd(&S.n_sel, s_cnt);
+    atomicMax(&S.max_key, s_max);
+  }
+  if (!last_cta(&S.ctr, G, &s_last)) return;
+  if (threadIdx.x == 0) {  // set up the radix select
+    const uint64_t mxk = *(volatile unsigned long long*)&S.max_key;
+    const uint32_t n = *(volatile uint32_t*)&S.n_sel;
+    S.all = n <= K;
+    S.k_remain = K;
+    S.prefix = 0;
+    S.mask = 0;
+    S.shift = mxk ? ((63 - __clzll(mxk)) / 8) * 8 : 0;
+  }
+  for (int b = threadIdx.x; b < 256; b += kThreads) S.hist[b] = 0;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    hist_kernel(const uint64_t* __restrict__ key, uint64_t shard_cap, uint32_t G, TopkState* st) {
+  __shared__ uint32_t s_hist[256];
+  __shared__ bool s_last;
+  const uint32_t ls = blockIdx.y;
+  TopkState& S = st[ls];
+  const int shift = *(volatile int*)&S.shift;
+  if (S.all || shift < 0) return;  // selection finished (uniform over the shard)
+  const uint64_t prefix = S.prefix, mask = S.mask;
+  const Slice sl = cta_slice(shard_cap, G, blockIdx.x);
+  const uint64_t* k = key + (uint64_t)ls * shard_cap;
+  for (int b = threadIdx.x; b < 256; b += kThreads) s_hist[b] = 0;
+  __syncthreads();
+  for (uint64_t i = sl.begin + threadIdx.x; i < sl.end; i += kThreads) {
+    const uint64_t x = k[i];
+    if (x > 0 && (x & mask) == prefix) atomicAdd(&s_hist[(x >> shift) & 255], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < 256; b += kThreads)
+    if (s_hist[b]) atomicAdd(&S.hist[b], s_hist[b]);
+  if (!last_cta(&S.ctr, G, &s_last)) return;
+  // The digit: the largest v whose suffix count sum_{u >= v} hist[u] reaches
+  // k_remain.  Thread t owns bin 255 - t; block-wide inclusive scan over t.
+  static_assert(kThreads == 256, "one thread per digit");
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t kk = S.k_remain;
+  const uint32_t h = *(volatile uint32_t*)&S.hist[255 - t];
+  uint32_t suf = h;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(kFull, suf, d);
+    if (lane >= d) suf += o;
+  }
+  if (lane == 31) s_hist[warp] = suf;  // warp totals (the local histogram is dead)
+  __syncthreads();
+  for (int w = 0; w < warp; ++w) suf += s_hist[w];
+  if (suf >= kk && suf - h < kk) {  // exactly one thread
+    const uint32_t v = 255 - t;
+    S.prefix = prefix | ((uint64_t)v << shift);
+    S.mask = mask | (255ull << shift);
+    S.k_remain = kk - (suf - h);
+    // done after the last byte, or as soon as every key of the bin is needed
+    // (then the keys > T* and == T* are those above / in the bin, ties moot)
+    S.shift = h == kk - (suf - h) ? -1 : shift - 8;
+  }
+  __syncthreads();  // every thread has read the histogram
+  for (int b = threadIdx.x; b < 256; b += kThreads) S.hist[b] = 0;
+}
+
+// Keys taken: all selectable ones (all), or the keys whose resolved bytes
+// (x & mask) exceed the prefix plus the first k_remain keys whose resolved
+// bytes equal it, in slot order.  With every byte resolved the prefix is the
+// K-th largest key T* itself and this is "key > T*, then ties by slot".
+__device__ __forceinline__ void classify(const TopkState& S, uint64_t x, bool* gt, bool* eq) {
+  if (S.all) {
+    *gt = x > 0;
+    *eq = false;
+  } else {
+    const uint64_t xm = x & S.mask;
+    *gt = x > 0 && xm > S.prefix;
+    *eq = x > 0 && xm == S.prefix;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    count_kernel(const uint64_t* __restrict__ key, uint64_t shard_cap, uint32_t G, TopkState* st,
+                 uint32_t* cnt /* [R][G][2] */) {
+  __shared__ uint32_t s_gt, s_eq;
+  const uint32_t ls = blockIdx.y;
+  const TopkState& S = st[ls];
+  const Slice sl = cta_slice(shard_cap, G, blockIdx.x);
+  const uint64_t* k = key + (uint64_t)ls * shard_cap;
+  if (threadIdx.x == 0) s_gt = s_eq = 0;
+  __syncthreads();
+  uint32_t g = 0, e = 0;
+  for (uint64_t i = sl.begin + threadIdx.x; i < sl.end; i += kThreads) {
+    bool gt, eq;
+    classify(S, k[i], &gt, &eq);
+    g += gt;
+    e += eq;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    g += __shfl_xor_sync(kFull, g, d);
+    e += __shfl_xor_sync(kFull, e, d);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&s_gt, g);
+    atomicAdd(&s_eq, e);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    cnt[((uint64_t)ls * G + blockIdx.x) * 2 + 0] = s_gt;
+    cnt[((uint64_t)ls * G + blockIdx.x) * 2 + 1] = s_eq;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    write_kernel(const uint64_t* __restrict__ key, uint64_t shard_cap, uint32_t G, uint32_t K,
+                 uint32_t first_shard, const TopkState* st, const uint32_t* __restrict__ cnt,
+                 Cand* __restrict__ cand_out, ShardTotals* __restrict__ totals_out) {
+  __shared__ uint32_t s_red[kThreads / 32];
+  __shared__ uint32_t s_base_gt, s_base_eq, s_tot;
+  const uint32_t ls = blockIdx.y;
+  const TopkState& S = st[ls];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t need = S.all ? 0u : S.k_remain;
+  __shared__ uint32_t s_tg, s_te;
+  if (tid == 0) s_base_gt = s_base_eq = s_tg = s_te = 0;
+  __syncthreads();
+  {  // offsets from the CTAs before this one (slot order), block-wide
+    uint32_t bg = 0, be = 0, tg = 0, te = 0;
+    for (uint32_t c = tid; c < G; c += kThreads) {
+      const uint2 ge = *reinterpret_cast<const uint2*>(cnt + ((uint64_t)ls * G + c) * 2);
+      if (c < blockIdx.x) {
+        bg += ge.x;
+        be += ge.y;
+      }
+      tg += ge.x;
+      te += ge.y;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      bg += __shfl_xor_sync(kFull, bg, d);
+      be += __shfl_xor_sync(kFull, be, d);
+      tg += __shfl_xor_sync(kFull, tg, d);
+      te += __shfl_xor_sync(kFull, te, d);
+    }
+    if (lane == 0 && (tg | te)) {
+      atomicAdd(&s_base_gt, bg);
+      atomicAdd(&s_base_eq, be);
+      atomicAdd(&s_tg, tg);
+      atomicAdd(&s_te, te);
+    }
+    __syncthreads();
+    if (tid == 0) s_tot = min(K, s_tg + min(need, s_te));
+    __syncthreads();
+  }
+  const uint32_t base_gt = s_base_gt;
+  uint32_t eq_seen = s_base_eq;  // keys == T* in earlier slots (block-uniform)
+  // taken so far = gt before + ties taken before
+  uint32_t taken = base_gt + min(need, eq_seen);
+  const Slice sl = cta_slice(shard_cap, G, blockIdx.x);
+  const uint64_t* k = key + (uint64_t)ls * shard_cap;
+  Cand* out = cand_out + (uint64_t)ls * K;
+  for (uint64_t i0 = sl.begin; i0 < sl.end; i0 += kThreads) {
     const uint64_t i = i0 + tid;
-    const uint64_t x = i < shard_cap ? k[i] : 0;
-    const bool gt = all ? x > 0 : x > thr;
-    const bool eq = !all && x == thr && x > 0;
+    const uint64_t x = i < sl.end ? k[i] : 0;
+    bool gt = false, eq = false;
+    if (i < sl.end) classify(S, x, &gt, &eq);
     const unsigned mg = __ballot_sync(kFull, gt), me = __ballot_sync(kFull, eq);
     if (lane == 0) s_red[warp] = (__popc(me) << 16) | __popc(mg);
     __syncthreads();
-    uint32_t gt_before = 0, eq_before = 0, eq_total = 0, gt_total = 0;
-    for (int w = 0; w < kWarps; ++w) {
+    uint32_t gt_before = 0, eq_before = 0, gt_total = 0, eq_total = 0;
+    for (int w = 0; w < kThreads / 32; ++w) {
       const uint32_t c = s_red[w];
       if (w < warp) {
         gt_before += c & 0xffff;
@@ -136,79 +273,89 @@ __global__ void __launch_bounds__(kThreads)
       eq_total += c >> 16;
     }
     const uint32_t lt = (1u << lane) - 1u;
-    const uint32_t my_eq = eq_seen + eq_before + __popc(me & lt);
-    const bool take_eq = eq && my_eq < need;
-    // position = #taken before me in slot order
-    const uint32_t eq_taken_before =
-        min(need, eq_seen + eq_before + __popc(me & lt)) - min(need, eq_seen);
-    const uint32_t base = s_count;
-    if (gt || take_eq) {
+    const uint32_t my_eq_rank = eq_seen + eq_before + __popc(me & lt);  // among keys == T*
+    const uint32_t eq_taken_before = min(need, my_eq_rank) - min(need, eq_seen);
+    if (gt || (eq && my_eq_rank < need)) {
       Cand c;
       c.seq = x;
-      c.shard = shard;
+      c.shard = first_shard + ls;
       c.slot = (uint32_t)i;
-      s_sel[base + gt_before + __popc(mg & lt) + eq_taken_before] = c;
+      const uint32_t pos = taken + gt_before + __popc(mg & lt) + eq_taken_before;
+      if (pos < K) out[pos] = c;  // always true when the selection invariant holds
     }
-    __syncthreads();
-    if (tid == 0) s_count = base + gt_total + (min(need, eq_seen + eq_total) - min(need, eq_seen));
+    taken += gt_total + (min(need, eq_seen + eq_total) - min(need, eq_seen));
     eq_seen += eq_total;
     __syncthreads();
   }
-  const uint32_t n = s_count;  // == min(K, n_sel)
-  for (uint32_t i = n + tid; i < Kpow2; i += kThreads) {  // sentinels sort last
-    Cand c;
-    c.seq = 0;
-    c.shard = 0;
-    c.slot = 0xffffffffu;
-    s_sel[i] = c;
-  }
-  __syncthreads();
-
-  // 4. bitonic sort of Kpow2 entries: (key desc, slot asc)
-  for (uint32_t size = 2; size <= Kpow2; size <<= 1) {
-    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-      for (uint32_t i = tid; i < Kpow2; i += kThreads) {
-        const uint32_t j = i ^ stride;
-        if (j > i) {
-          const bool asc = (i & size) == 0;  // "ascending" in the `before` order
-          const Cand a = s_sel[i], b = s_sel[j];
-          if (asc ? before(b, a) : before(a, b)) {
-            s_sel[i] = b;
-            s_sel[j] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  Cand* out = cand_out + (uint64_t)ls * K;
-  for (uint32_t i = tid; i < n; i += kThreads) out[i] = s_sel[i];
-  if (tid == 0) {
+  if (blockIdx.x == 0 && tid == 0) {
     ShardTotals t;
     t.total_and_parity = 0;
-    t.aux = n;
+    t.aux = s_tot;
     totals_out[ls] = t;
   }
-  if (!xchg) return;
-  // W > 1: push the sorted list and its length into every peer's mailbox.
-  const MboxLayout L = mbox_layout(m.W, m.S, m.MB);
-  const uint32_t b = mbox_buf(m);
-  for (uint32_t r = 0; r < m.W; ++r) {
-    Cand* dst = mbox_at<Cand>(m, r, L.cand) + ((uint64_t)b * m.S + shard) * K;
-    for (uint32_t i = tid; i < n; i += kThreads) dst[i] = s_sel[i];
-    if (tid == 0) {
-      ShardTotals t;
-      t.total_and_parity = 0;
-      t.aux = n;
-      mbox_at<ShardTotals>(m, r, L.ccnt)[b * m.S + shard] = t;
+}
+
+// Candidate order of TopK: larger key first, then smaller slot.
+__device__ __forceinline__ bool before(const Cand& a, const Cand& b) {
+  return a.seq > b.seq || (a.seq == b.seq && a.slot < b.slot);
+}
+
+// Rank sort: the position of a candidate is the number of candidates before
+// it in the TopK order (keys and slots are distinct, so the ranks are a
+// permutation).  One warp per candidate: the lanes compare it with a strided
+// 1/32 of the list (L1-resident after the first warps) and sum; kSortWarps
+// candidates per CTA, ceil(K / kSortWarps) CTAs per shard.
+__global__ void __launch_bounds__(kSortThreads)
+    sort_kernel(uint32_t K, uint32_t first_shard, const Cand* __restrict__ unsorted,
+                Cand* __restrict__ sorted, const ShardTotals* __restrict__ totals, TopkState* st,
+                const __grid_constant__ Mbox m0, int xchg) {
+  __shared__ bool s_last;
+  const Mbox m = xchg ? mbox_at_next_epoch(m0) : m0;  // the FIFO/TopK epoch advances later
+  const uint32_t ls = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t n = (uint32_t)totals[ls].aux;
+  const uint32_t i = blockIdx.x * kSortWarps + (tid >> 5);
+  const uint32_t shard = first_shard + ls;
+  if (blockIdx.x == 0 && tid == 0) {  // re-arm this shard's selection state for the next call
+    TopkState& S = st[ls];
+    S.n_sel = 0;
+    S.max_key = 0;
+  }
+  if (i < n) {
+    const Cand* in = unsorted + (uint64_t)ls * K;
+    const Cand me = in[i];
+    uint32_t rank = 0;
+#pragma unroll 4
+    for (uint32_t j = lane; j < n; j += 32) rank += before(in[j], me);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) rank += __shfl_xor_sync(kFull, rank, d);
+    if (lane == 0) sorted[(uint64_t)ls * K + rank] = me;
+    if (xchg && lane < m.W) {  // W > 1: straight into every peer's mailbox as well
+      const MboxLayout L = mbox_layout(m.W, m.S, m.MB);
+      const uint32_t b = mbox_buf(m);
+      mbox_at<Cand>(m, lane, L.cand)[((uint64_t)b * m.S + shard) * K + rank] = me;
     }
   }
+  if (!xchg) return;
+  // The last CTA of the shard publishes the list length and the epoch flag.
   __syncthreads();
   if (tid == 0) {
     __threadfence_system();
-    for (uint32_t r = 0; r < m.W; ++r)
-      st_release_sys_u64(mbox_at<uint64_t>(m, r, L.cflag) + b * m.S + shard, m.epoch);
+    s_last = atomicAdd(&st[ls].ctr, 1u) == gridDim.x - 1;
+    if (s_last) st[ls].ctr = 0;
   }
+  __syncthreads();
+  if (!s_last || tid != 0) return;
+  __threadfence_system();
+  const MboxLayout L = mbox_layout(m.W, m.S, m.MB);
+  const uint32_t b = mbox_buf(m);
+  ShardTotals t;
+  t.total_and_parity = 0;
+  t.aux = n;
+  for (uint32_t r = 0; r < m.W; ++r) mbox_at<ShardTotals>(m, r, L.ccnt)[b * m.S + shard] = t;
+  __threadfence_system();
+  for (uint32_t r = 0; r < m.W; ++r)
+    st_release_sys_u64(mbox_at<uint64_t>(m, r, L.cflag) + b * m.S + shard, m.epoch);
 }
 
 }  // namespace
@@ -216,22 +363,29 @@ __global__ void __launch_bounds__(kThreads)
 uint32_t topk_max_k() { return 8192; }
 
 cudaError_t launch_topk_local(const uint64_t* key, uint64_t shard_cap, uint32_t n_shards_local,
-                              uint32_t first_shard, uint32_t K, Cand* cand_out,
-                              ShardTotals* totals_out, const Mbox* mbox, cudaStream_t s) {
-  uint32_t Kpow2 = 1;
-  while (Kpow2 < K) Kpow2 <<= 1;
-  const size_t smem = (size_t)Kpow2 * sizeof(Cand);
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(topk_local_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(smem < 48 * 1024 ? 48 * 1024 : smem));
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  count_launch();
-  topk_local_kernel<<<n_shards_local, kThreads, smem, s>>>(key, shard_cap, first_shard, K, Kpow2,
-                                                           cand_out, totals_out,
-                                                           mbox ? *mbox : Mbox{}, mbox != nullptr);
+                              uint32_t first_shard, uint32_t K, Cand* cand_tmp, Cand* cand_out,
+                              ShardTotals* totals_out, TopkState* state, uint32_t* cnt,
+                              const Mbox* mbox, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // CTAs per shard: ~2 waves of the GPU over all local shards, >= 1 slice of 256 keys
+  uint32_t G = (uint32_t)(2 * sms) / n_shards_local;
+  G = G < 1 ? 1 : G;
+  const uint64_t max_g = (shard_cap + kThreads - 1) / kThreads;
+  G = (uint64_t)G > max_g ? (uint32_t)max_g : G;
+  G = G > kTopkMaxCtas ? kTopkMaxCtas : G;
+  const dim3 grid(G, n_shards_local);
+  count_launch(12);
+  stats_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, K, state);
+  for (int pass = 0; pass < 8; ++pass)  // one per key byte; no-ops once selected
+    hist_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, state);
+  count_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, state, cnt);
+  write_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, K, first_shard, state, cnt, cand_tmp,
+                                         totals_out);
+  const dim3 sgrid((K + kSortWarps - 1) / kSortWarps, n_shards_local);
+  sort_kernel<<<sgrid, kSortThreads, 0, s>>>(K, first_shard, cand_tmp, cand_out, totals_out,
+                                                state, mbox ? *mbox : Mbox{}, mbox != nullptr);
   return cudaGetLastError();
 }
 

@@ -141,6 +141,9 @@ struct gear_table {
   uint32_t* glob_shard = nullptr;    // [W*max_batch] merged FIFO/LIFO list
   uint32_t* glob_slot = nullptr;
   gear::Cand* cand_local = nullptr;  // [R * W*max_batch]
+  gear::TopkState* topk_state = nullptr;  // [R]
+  gear::Cand* topk_tmp = nullptr;         // [R * W*max_batch] unsorted TopK lists
+  uint32_t* topk_cnt = nullptr;           // [R][kTopkMaxCtas][2]
   gear::Cand* cand_all = nullptr;    // [S * W*max_batch]
 
   // update scratch

@@ -195,6 +195,31 @@ def test_topk_with_ties(torch_cuda, R):
     P.close()
 
 
+@pytest.mark.parametrize("R,kind", [(1, "ties"), (1, "lognormal"), (3, "ties"), (2, "equal")])
+def test_topk_large_multi_cta(torch_cuda, R, kind):
+    """TopK over shards spread across many CTAs per shard (radix-select
+    histograms merged in global memory, offsets across CTAs) at the maximum
+    K = 8192: ties straddling CTA slices, continuous keys (early exit of the
+    select), and every key equal (the K taken are the K smallest slots)."""
+    cols = [synth.ColSpec("x", "u8", (8,))]
+    Cs = 120_000
+    P = _pair(capacity=Cs * R, seq_len=1, colspecs=cols, R=R, max_batch=8192)
+    rng = np.random.default_rng(77 + R)
+    if kind == "ties":
+        vals = np.array([0.0, 0.5, 1.0, 2.0, 4.0])
+        prio = vals[rng.integers(0, len(vals), size=Cs * R)]
+    elif kind == "lognormal":
+        prio = synth.priorities(Cs * R, seed=5, zero_frac=0.05)
+    else:
+        prio = np.full(Cs * R, 1.5)
+    P.fill(prio)
+    for B in (1, 777, 8192):
+        idx = P.check_sample(G.GEAR_TOPK, B, 0)
+        assert idx is not None
+    P.check_collect(idx)
+    P.close()
+
+
 def test_insert_bad_priority_and_device_sources(torch_cuda):
     cols = [synth.ColSpec("a", "u8", (7,)), synth.ColSpec("b", "i32", (3,))]
     P = _pair(capacity=64, seq_len=3, colspecs=cols, R=2)
