@@ -141,6 +141,13 @@ typedef struct {
   uint32_t shards_per_rank;    /* R (0 -> 1); W*R <= 32.  R > 1 emulates a
                                   larger world on fewer GPUs (tests). */
   uint32_t max_batch;          /* upper bound of B and of per-call n (0 -> 4096) */
+  double priority_alpha;       /* PER exponent alpha (Schaul et al.; Q7):
+                                  every priority p of gear_insert and
+                                  gear_update_priorities becomes the key
+                                  Q_F(p^alpha) with p^alpha rounded to the nearest
+                                  double (p = 0 stays 0).  0 -> 1 (the priority
+                                  itself); alpha = 0 is GEAR_UNIFORM.  Finite,
+                                  >= 0, else INVALID_ARG. */
 } gear_table_desc;
 
 typedef struct {
@@ -152,9 +159,10 @@ typedef struct {
   uint32_t ncols;
   uint64_t row_bytes_total;  /* sum of the columns' row bytes */
   uint64_t q_max;            /* largest fixed-point key = floor((2^62-1)/N) */
-  double p_max;              /* q_max / 2^F: priorities above it saturate */
+  double p_max;              /* q_max / 2^F: values of p^alpha above it saturate */
   uint32_t frac_bits;
   uint32_t max_batch;
+  double alpha;              /* PER exponent of the keys */
 } gear_table_info;
 
 typedef struct gear_comm gear_comm;

@@ -13,6 +13,7 @@ only marshals numpy arrays into it.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 
@@ -102,6 +103,36 @@ def quantize(p: float, frac_bits: int, qmax: int):
     return st, int(q[0])
 
 
+def pow_alpha(p, alpha: float) -> np.ndarray:
+    """PER priority exponent (Schaul et al. 2016, P(i) = p_i^alpha / sum_k p_k^alpha;
+    the paper names PER at PAPER.md:55,121 and gives no formula -- reading Q7):
+    every finite p > 0 becomes p^alpha rounded to the nearest double (ties to
+    even).  The power is taken by mpmath at 200-bit precision -- exact when it
+    fits in 200 bits (p^2, p^3, ...), else within a few 2^-200 -- and rounded
+    once to 53 bits.  Results above DBL_MAX become DBL_MAX and results below
+    the least subnormal become it, so a positive priority never turns into 0
+    (below 2^-1022 only positivity matters: such keys are clamped to 1).
+    p = 0 and invalid values (NaN, inf, negative) pass through unchanged for
+    the quantiser to handle."""
+    p = np.ascontiguousarray(p, dtype=np.float64)
+    if alpha == 1.0:
+        return p.copy()
+    from mpmath import mp, mpf
+    out = p.copy()
+    with mp.workprec(200):
+        a = mpf(float(alpha))
+        for i, x in enumerate(p.tolist()):
+            if not (x > 0.0 and math.isfinite(x)):
+                continue
+            f = float(mpf(x) ** a)
+            if f == math.inf:
+                f = float(np.finfo(np.float64).max)
+            elif f == 0.0:
+                f = 5e-324
+            out[i] = f
+    return out
+
+
 def cdf(key: np.ndarray) -> np.ndarray:
     key = np.ascontiguousarray(key, dtype=np.uint64)
     C = np.zeros_like(key)
@@ -184,8 +215,10 @@ class Table:
     only the unit of insertion and of FIFO tie-breaks.
     """
 
-    def __init__(self, shard_cap: int, n_shards: int, frac_bits: int = 32, removal: int = 0):
+    def __init__(self, shard_cap: int, n_shards: int, frac_bits: int = 32, removal: int = 0,
+                 alpha: float = 1.0):
         self.cap, self.S, self.F, self.removal = shard_cap, n_shards, frac_bits, removal
+        self.alpha = alpha          # keys are Q_F(pow_alpha(p)) (reading Q7)
         n = shard_cap * n_shards
         self.key = np.zeros(n, dtype=np.uint64)
         self.seq = np.zeros(n, dtype=np.uint64)
@@ -198,7 +231,7 @@ class Table:
         return self.cap * self.S
 
     def insert(self, shard: int, prio) -> tuple[int, np.ndarray]:
-        prio = np.ascontiguousarray(prio, dtype=np.float64)
+        prio = pow_alpha(prio, self.alpha)
         out = np.zeros(prio.size, dtype=np.uint64)
         nf = self.next_free[shard:shard + 1].copy()
         sc = self.seq_ctr[shard:shard + 1].copy()
@@ -210,7 +243,7 @@ class Table:
         return st, out
 
     def update(self, idx, p, gen_in=None):
-        return update(self.key, self.gen, self.F, idx, p, gen_in)
+        return update(self.key, self.gen, self.F, idx, pow_alpha(p, self.alpha), gen_in)
 
     def sample(self, strategy, n_ranks, rank, B, seed, beta=0.0, owner_affine=False):
         fn = sample_owner_affine if owner_affine else sample

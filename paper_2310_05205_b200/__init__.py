@@ -71,7 +71,8 @@ class _TableDesc(ctypes.Structure):
     _fields_ = [("capacity_global", ctypes.c_uint64), ("seq_len", ctypes.c_uint32),
                 ("ncols", ctypes.c_uint32), ("cols", ctypes.POINTER(_ColumnDesc)),
                 ("priority_frac_bits", ctypes.c_uint32), ("removal", ctypes.c_int),
-                ("shards_per_rank", ctypes.c_uint32), ("max_batch", ctypes.c_uint32)]
+                ("shards_per_rank", ctypes.c_uint32), ("max_batch", ctypes.c_uint32),
+                ("priority_alpha", ctypes.c_double)]
 
 
 class _TableInfo(ctypes.Structure):
@@ -80,7 +81,7 @@ class _TableInfo(ctypes.Structure):
                 ("shards_per_rank", ctypes.c_uint32), ("ncols", ctypes.c_uint32),
                 ("row_bytes_total", ctypes.c_uint64), ("q_max", ctypes.c_uint64),
                 ("p_max", ctypes.c_double), ("frac_bits", ctypes.c_uint32),
-                ("max_batch", ctypes.c_uint32)]
+                ("max_batch", ctypes.c_uint32), ("alpha", ctypes.c_double)]
 
 
 # exported symbols and their signatures (also checked by the CPU tests)
@@ -208,7 +209,8 @@ class Column:
 
 def gear_table_create(capacity: int, seq_len: int, columns: Sequence[Column], comm: int | None = None,
                       frac_bits: int = 32, removal: int = GEAR_REMOVE_FIFO,
-                      shards_per_rank: int = 1, max_batch: int = 4096) -> int:
+                      shards_per_rank: int = 1, max_batch: int = 4096,
+                      alpha: float = 1.0) -> int:
     cols = (_ColumnDesc * len(columns))()
     keep = []
     for c, col in zip(cols, columns):
@@ -218,7 +220,8 @@ def gear_table_create(capacity: int, seq_len: int, columns: Sequence[Column], co
         c.name, c.dtype, c.ndim = name, col.dtype, len(col.shape)
         c.shape = ctypes.cast(shape, ctypes.POINTER(ctypes.c_int64))
         c.placement = col.placement
-    d = _TableDesc(capacity, seq_len, len(columns), cols, frac_bits, removal, shards_per_rank, max_batch)
+    d = _TableDesc(capacity, seq_len, len(columns), cols, frac_bits, removal, shards_per_rank,
+                   max_batch, alpha)
     out = ctypes.c_void_p()
     _check("gear_table_create", load().gear_table_create(ctypes.byref(d), comm, ctypes.byref(out)))
     return out.value

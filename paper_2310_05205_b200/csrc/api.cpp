@@ -24,6 +24,14 @@ using namespace gear;
 
 namespace {
 
+Quant quant(const gear_table* t) {
+  Quant q{};
+  q.q_max = t->qmax;
+  q.frac_bits = t->F;
+  q.alpha = t->alpha;
+  return q;
+}
+
 uint64_t dtype_size(gear_dtype d) {
   switch (d) {
     case GEAR_U8: return 1;
@@ -148,7 +156,7 @@ void destroy_table(gear_table* t) {
   dfree(t->topk_state); dfree(t->topk_cnt); dfree(t->topk_tmp);
   dfree(t->draw_list); dfree(t->pos_scratch); dfree(t->ov_scratch);
   dfree(t->glob_shard); dfree(t->glob_slot);
-  dfree(t->upd_local); dfree(t->upd_all); dfree(t->upd_idx); dfree(t->upd_prio); dfree(t->upd_gen);
+  dfree(t->upd_local); dfree(t->upd_all); dfree(t->upd_idx); dfree(t->upd_prio); dfree(t->upd_pow); dfree(t->upd_gen);
   dfree(t->n_stale); dfree(t->err); dfree(t->d_epoch); dfree(t->d_seed); dfree(t->d_xep);
   dfree(t->col_idx.p);
   dfree(t->d_meta); dfree(t->d_ord); dfree(t->d_out); dfree(t->d_rows);
@@ -183,6 +191,9 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   t->F = d->priority_frac_bits ? d->priority_frac_bits : 32;
   if (t->F > 62) return set_error(GEAR_ERR_INVALID_ARG, "priority_frac_bits > 62");
   t->qmax = ((1ull << 62) - 1) / t->N;
+  if (!std::isfinite(d->priority_alpha) || d->priority_alpha < 0.0)
+    return set_error(GEAR_ERR_INVALID_ARG, "priority_alpha must be finite and >= 0");
+  t->alpha = d->priority_alpha == 0.0 ? 1.0 : d->priority_alpha;
   t->removal = d->removal;
   if (t->removal != GEAR_REMOVE_FIFO && t->removal != GEAR_REMOVE_LIFO)
     return set_error(GEAR_ERR_INVALID_ARG, "bad removal");
@@ -396,6 +407,7 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_TRY(dalloc(&t->upd_all, K));
   GEAR_TRY(dalloc(&t->upd_idx, MB));
   GEAR_TRY(dalloc(&t->upd_prio, MB));
+  GEAR_TRY(dalloc(&t->upd_pow, MB));
   GEAR_TRY(dalloc(&t->upd_gen, MB));
   GEAR_TRY(dalloc(&t->d_xep, 4));
   GEAR_CUDA(cudaMemset(t->d_xep, 0, 32));
@@ -508,6 +520,7 @@ gear_status gear_table_info_get(const gear_table* t, gear_table_info* info) {
   info->q_max = t->qmax;
   info->p_max = std::ldexp((double)t->qmax, -(int)t->F);
   info->frac_bits = t->F;
+  info->alpha = t->alpha;
   info->max_batch = t->max_batch;
   return GEAR_OK;
 }
@@ -649,7 +662,7 @@ gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* c
     }
     sp.total_chunks = chunks;
     GEAR_CUDA(launch_scatter(sp, s));
-    GEAR_CUDA(launch_insert_meta(t->d_meta, n_meta, t->d_ord, n_ord, t->F, t->qmax, t->key,
+    GEAR_CUDA(launch_insert_meta(t->d_meta, n_meta, t->d_ord, n_ord, quant(t), t->key,
                                  t->seq, t->gen, t->ord, s));
     if (out_idx) {
       if (mem_kind(out_idx) == MemKind::Device) {
@@ -692,24 +705,32 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
     }
     if (gen) GEAR_TRY(stage_in(gen, n, t->upd_gen, s, &d_gen));
   }
+  // PER exponent: the update kernels quantise p^alpha computed here first
+  Quant qz = quant(t);
+  if (t->alpha != 1.0 && n > 0) {
+    GEAR_CUDA(launch_alpha(d_prio, prio_dtype == GEAR_F64, n, t->alpha, t->upd_pow, s));
+    d_prio = t->upd_pow;
+    prio_dtype = GEAR_F64;
+  }
+  qz.alpha = 1.0;
   const uint64_t local_begin = (uint64_t)t->rank * t->Clocal;
   const bool fused = t->update_fused && (uint64_t)n * t->W <= update_fused_max();
   if (t->W == 1 && fused) {
     // one launch: quantise, tag, block barrier, apply
     GEAR_CUDA(launch_update_fused(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, nullptr, n, t->N,
-                                  t->F, t->qmax, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
+                                  qz, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
                                   t->n_stale, t->err, t->key, s));
   } else if (t->W > 1 && fused && t->peer_xchg) {
     // one launch: quantise, push records to every peer over NVLink, wait for
     // every rank's records, tag, barrier, apply
     Mbox mb = t->mb;
     mb.epoch_dev = t->d_xep + 1;  // update-exchange epoch (advanced by the kernel)
-    GEAR_CUDA(launch_update_xchg(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N, t->F,
-                                 t->qmax, mb, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
+    GEAR_CUDA(launch_update_xchg(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N, qz,
+                                 mb, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
                                  t->n_stale, t->err, t->key, s));
   } else {
-    GEAR_CUDA(launch_update_quantize(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N, t->F,
-                                     t->qmax, t->upd_local, t->err, s));
+    GEAR_CUDA(launch_update_quantize(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N,
+                                     qz, t->upd_local, t->err, s));
     const UpdRec* recs = t->upd_local;
     uint32_t m = n;
     if (t->W > 1) {
@@ -718,7 +739,7 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
       m = n * t->W;
     }
     if (fused) {
-      GEAR_CUDA(launch_update_fused(nullptr, nullptr, 0, nullptr, recs, m, t->N, t->F, t->qmax,
+      GEAR_CUDA(launch_update_fused(nullptr, nullptr, 0, nullptr, recs, m, t->N, qz,
                                     local_begin, t->Clocal, t->gen, t->tag, t->d_epoch, t->n_stale,
                                     t->err, t->key, s));
     } else {
@@ -779,7 +800,8 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     // the FIFO-exchange epoch advances after the merge (and assignment)
     mb.epoch_dev = t->d_xep + 2;
     if (topk)
-      GEAR_CUDA(launch_topk_local(t->key, t->Cs, t->R, t->rank * t->R, K, t->topk_tmp, t->cand_local,
+      GEAR_CUDA(launch_topk_local(t->key, t->Cs, t->R, t->rank * t->R, K, t->topk_tmp,
+                                  t->cand_local,
                                   t->fifo_totals_local, t->topk_state, t->topk_cnt,
                                   xchg ? &mb : nullptr, s));
     else

@@ -14,7 +14,7 @@ using namespace gear;
 namespace {
 
 constexpr char kMagic[8] = {'G', 'E', 'A', 'R', 'C', 'K', 'P', 'T'};
-constexpr uint32_t kVersion = 1;
+constexpr uint32_t kVersion = 2;
 constexpr size_t kStage = 64ull << 20;
 
 struct Header {
@@ -23,6 +23,7 @@ struct Header {
   uint64_t N, Cs;
   uint64_t rb[kMaxCols];
   uint32_t placement[kMaxCols];
+  double alpha;  // PER exponent the keys were made with
 };
 
 Header make_header(const gear_table* t) {
@@ -37,6 +38,7 @@ Header make_header(const gear_table* t) {
   h.removal = (uint32_t)t->removal;
   h.N = t->N;
   h.Cs = t->Cs;
+  h.alpha = t->alpha;
   for (size_t c = 0; c < t->cols.size(); ++c) {
     h.rb[c] = t->cols[c].rb;
     h.placement[c] = (uint32_t)t->cols[c].placement;

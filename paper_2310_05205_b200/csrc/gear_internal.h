@@ -25,6 +25,14 @@ constexpr uint32_t kErrTimeout = 16u;
 // Strategy codes (mirror gear_strategy).
 constexpr int kFifo = 0, kLifo = 1, kUniform = 2, kWeighted = 3, kPrioritized = 4;
 
+// Priority quantisation parameters (common.cuh quantize): key = Q_F(p^alpha).
+struct Quant {
+  uint64_t q_max;
+  uint32_t frac_bits;
+  uint32_t pad;
+  double alpha;  // PER exponent (1: the priority itself)
+};
+
 // Per-shard totals record exchanged between ranks (16 B): total weight T_s of
 // the shard's CDF with the CDF buffer parity in bit 63 (T_s < 2^62 by q_max),
 // and the number of valid FIFO/LIFO candidates the shard offers.
@@ -247,9 +255,12 @@ uint32_t scan_tiles_per_shard(uint64_t shard_cap);
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s);
 
 // K6: priority update.
+// prio (f32 or f64) -> RN(p^alpha) as f64 (0 and invalid values unchanged).
+cudaError_t launch_alpha(const void* prio, int prio_is_f64, uint32_t n, double alpha,
+                         double* out, cudaStream_t s);
 cudaError_t launch_update_quantize(const uint64_t* idx, const void* prio, int prio_is_f64,
                                    const uint32_t* gen, uint32_t n, uint64_t n_global,
-                                   uint32_t frac_bits, uint64_t q_max, UpdRec* out,
+                                   Quant qz, UpdRec* out,
                                    uint32_t* err, cudaStream_t s);
 cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                               uint64_t local_rows, const uint32_t* gen, unsigned long long* tag,
@@ -265,7 +276,7 @@ cudaError_t launch_update_apply(const UpdRec* recs, uint32_t m, uint64_t local_b
 uint32_t update_fused_max();
 cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_is_f64,
                                 const uint32_t* gen_in, const UpdRec* recs, uint32_t m,
-                                uint64_t n_global, uint32_t frac_bits, uint64_t q_max,
+                                uint64_t n_global, Quant qz,
                                 uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
                                 unsigned long long* tag, uint32_t* epoch_dev,
                                 unsigned long long* n_stale, uint32_t* err, uint64_t* key,
@@ -275,7 +286,7 @@ cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_
 // update_fused_max()).
 cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_is_f64,
                                const uint32_t* gen_in, uint32_t n, uint64_t n_global,
-                               uint32_t frac_bits, uint64_t q_max, const Mbox& mb,
+                               Quant qz, const Mbox& mb,
                                uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
                                unsigned long long* tag, uint32_t* epoch_dev,
                                unsigned long long* n_stale, uint32_t* err, uint64_t* key,
@@ -285,7 +296,7 @@ cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_i
 cudaError_t launch_collect(const CollectParams& p, cudaStream_t s);
 cudaError_t launch_scatter(const ScatterParams& p, cudaStream_t s);
 cudaError_t launch_insert_meta(const InsMeta* meta, uint32_t m, const OrdRec* ord_recs,
-                               uint32_t n_ord, uint32_t frac_bits, uint64_t q_max,
+                               uint32_t n_ord, Quant qz,
                                uint64_t* key, uint64_t* seq, uint32_t* gen, uint32_t* ord,
                                cudaStream_t s);
 

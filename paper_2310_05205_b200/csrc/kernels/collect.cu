@@ -246,14 +246,14 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
 
 __global__ void __launch_bounds__(kThreads)
     insert_meta_kernel(const InsMeta* __restrict__ meta, uint32_t m,
-                       const OrdRec* __restrict__ ord_recs, uint32_t n_ord, uint32_t frac_bits,
-                       uint64_t q_max, uint64_t* key, uint64_t* seq, uint32_t* gen,
+                       const OrdRec* __restrict__ ord_recs, uint32_t n_ord, Quant qz,
+                       uint64_t* key, uint64_t* seq, uint32_t* gen,
                        uint32_t* ord) {
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   if (k < m) {
     const InsMeta r = meta[k];
     uint64_t q = 0;
-    quantize(r.prio, frac_bits, q_max, &q);  // validated on the host
+    quantize(r.prio, qz, &q);  // validated on the host
     key[r.local] = q;
     seq[r.local] = r.seq;
     gen[r.local] += r.gen_inc;
@@ -322,14 +322,14 @@ cudaError_t launch_scatter(const ScatterParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_insert_meta(const InsMeta* meta, uint32_t m, const OrdRec* ord_recs,
-                               uint32_t n_ord, uint32_t frac_bits, uint64_t q_max,
+                               uint32_t n_ord, Quant qz,
                                uint64_t* key, uint64_t* seq, uint32_t* gen, uint32_t* ord,
                                cudaStream_t s) {
   const uint32_t n = m > n_ord ? m : n_ord;
   if (n == 0) return cudaSuccess;
   count_launch();
   insert_meta_kernel<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(
-      meta, m, ord_recs, n_ord, frac_bits, q_max, key, seq, gen, ord);
+      meta, m, ord_recs, n_ord, qz, key, seq, gen, ord);
   return cudaGetLastError();
 }
 

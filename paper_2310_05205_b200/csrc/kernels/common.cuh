@@ -5,6 +5,7 @@
 #include <type_traits>
 
 #include "../gear_internal.h"
+#include "pow_dd.cuh"
 
 namespace gear {
 
@@ -37,22 +38,33 @@ __device__ __forceinline__ uint64_t draw_bits(uint64_t seed, uint64_t j) {
   return (uint64_t)x.x | ((uint64_t)x.y << 32);
 }
 
-// Fixed-point key Q_F(p) (gear.h, gear_update_priorities).  Returns false for
-// NaN, +-inf or negative p.  x = p*2^F is exact; __double2ull_rn rounds half
-// to even; x >= 2^62 saturates.
-__device__ __forceinline__ bool quantize(double p, uint32_t frac_bits, uint64_t q_max,
-                                         uint64_t* q) {
-  if (!(p >= 0.0) || isinf(p)) return false;  // NaN fails p >= 0
-  if (p == 0.0) {
+// Fixed-point key Q_F(v) (gear.h, gear_update_priorities) of a value already
+// raised to the table's alpha.  Returns false for NaN, +-inf or negative v.
+// v == 0 is key 0; x = v*2^F is exact, __double2ull_rn rounds half to even,
+// x >= 2^62 saturates and the key is clamped to [1, q_max].
+__device__ __forceinline__ bool quantize_fixed(double v, const Quant& qz, uint64_t* q) {
+  if (!(v >= 0.0) || isinf(v)) return false;  // NaN fails v >= 0
+  if (v == 0.0) {
     *q = 0;
     return true;
   }
-  const double x = scalbn(p, (int)frac_bits);
-  uint64_t r = (x >= 4611686018427387904.0) ? q_max : __double2ull_rn(x);
+  const double x = scalbn(v, (int)qz.frac_bits);
+  uint64_t r = (x >= 4611686018427387904.0) ? qz.q_max : __double2ull_rn(x);
   r = r < 1 ? 1 : r;
-  r = r > q_max ? q_max : r;
+  r = r > qz.q_max ? qz.q_max : r;
   *q = r;
   return true;
+}
+
+// The PER exponent (reading Q7): a finite p > 0 becomes RN(p^alpha)
+// (pow_dd.cuh); 0 and invalid values pass through to quantize_fixed.
+__device__ __forceinline__ double apply_alpha(double p, double alpha) {
+  return (p > 0.0 && !isinf(p)) ? pow_rn(p, alpha) : p;
+}
+
+// Q_F(p^alpha).
+__device__ __forceinline__ bool quantize(double p, const Quant& qz, uint64_t* q) {
+  return quantize_fixed(apply_alpha(p, qz.alpha), qz, q);
 }
 
 // Relaxed 64-bit global loads/stores for the look-back status words.

@@ -10,6 +10,10 @@
 // tags of earlier calls smaller, so the tag array never needs clearing; it
 // lives in device memory and the kernels advance it themselves, so an update
 // captured in a CUDA graph stays correct when the graph is replayed.
+//
+// A table with a PER exponent alpha != 1 first raises the priorities to alpha
+// (alpha_kernel, one f64 per entry); the update kernels then quantise with
+// quantize_fixed, so the double-double code stays out of their registers.
 #include "mbox.cuh"
 
 namespace gear {
@@ -21,7 +25,7 @@ constexpr int kThreads = 256;
 __global__ void __launch_bounds__(kThreads)
     quantize_kernel(const uint64_t* __restrict__ idx, const void* __restrict__ prio,
                     int prio_is_f64, const uint32_t* __restrict__ gen, uint32_t n,
-                    uint64_t n_global, uint32_t frac_bits, uint64_t q_max, UpdRec* out,
+                    uint64_t n_global, Quant qz, UpdRec* out,
                     uint32_t* err) {
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   if (k >= n) return;
@@ -36,7 +40,7 @@ __global__ void __launch_bounds__(kThreads)
     // padding entry: ignored
   } else if (r.idx >= n_global) {
     atomicOr(err, kErrIndexRange);
-  } else if (!quantize(p, frac_bits, q_max, &r.q)) {
+  } else if (!quantize_fixed(p, qz, &r.q)) {
     atomicOr(err, kErrBadPriority);
   } else {
     r.flags |= 1u;
@@ -106,7 +110,7 @@ constexpr int kFusedPer = kFusedMax / kFusedThreads;
 __global__ void __launch_bounds__(kFusedThreads)
     fused_kernel(const uint64_t* __restrict__ idx, const void* __restrict__ prio, int prio_is_f64,
                  const uint32_t* __restrict__ gen_in, const UpdRec* __restrict__ recs, uint32_t m,
-                 uint64_t n_global, uint32_t frac_bits, uint64_t q_max, uint64_t local_begin,
+                 uint64_t n_global, Quant qz, uint64_t local_begin,
                  uint64_t local_rows, const uint32_t* __restrict__ gen, unsigned long long* tag,
                  uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err, uint64_t* key) {
   const uint32_t epoch = *epoch_dev + 1;  // device-resident: graph-replayable
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(kFusedThreads)
       if (r[u].idx == kIdxNone) {
       } else if (r[u].idx >= n_global) {
         e |= kErrIndexRange;
-      } else if (!quantize(p, frac_bits, q_max, &r[u].q)) {
+      } else if (!quantize_fixed(p, qz, &r[u].q)) {
         e |= kErrBadPriority;
       } else {
         r[u].flags |= 1u;
@@ -167,7 +171,7 @@ __global__ void __launch_bounds__(kFusedThreads)
 __global__ void __launch_bounds__(kFusedThreads)
     xchg_kernel(const uint64_t* __restrict__ idx, const void* __restrict__ prio, int prio_is_f64,
                 const uint32_t* __restrict__ gen_in, uint32_t n, uint64_t n_global,
-                uint32_t frac_bits, uint64_t q_max, const __grid_constant__ Mbox mb0,
+                Quant qz, const __grid_constant__ Mbox mb0,
                 uint64_t local_begin, uint64_t local_rows, const uint32_t* __restrict__ gen,
                 unsigned long long* tag, uint32_t* epoch_dev, unsigned long long* n_stale,
                 uint32_t* err, uint64_t* key) {
@@ -187,7 +191,7 @@ __global__ void __launch_bounds__(kFusedThreads)
     if (r.idx == kIdxNone) {
     } else if (r.idx >= n_global) {
       e |= kErrIndexRange;
-    } else if (!quantize(p, frac_bits, q_max, &r.q)) {
+    } else if (!quantize_fixed(p, qz, &r.q)) {
       e |= kErrBadPriority;
     } else {
       r.flags |= 1u;
@@ -254,21 +258,21 @@ uint32_t update_fused_max() { return kFusedMax; }
 
 cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_is_f64,
                                const uint32_t* gen_in, uint32_t n, uint64_t n_global,
-                               uint32_t frac_bits, uint64_t q_max, const Mbox& mb,
+                               Quant qz, const Mbox& mb,
                                uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
                                unsigned long long* tag, uint32_t* epoch_dev,
                                unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                cudaStream_t s) {
   count_launch();
-  xchg_kernel<<<1, kFusedThreads, 0, s>>>(idx, prio, prio_is_f64, gen_in, n, n_global, frac_bits,
-                                          q_max, mb, local_begin, local_rows, gen, tag, epoch_dev,
+  xchg_kernel<<<1, kFusedThreads, 0, s>>>(idx, prio, prio_is_f64, gen_in, n, n_global, qz, mb,
+                                          local_begin, local_rows, gen, tag, epoch_dev,
                                           n_stale, err, key);
   return cudaGetLastError();
 }
 
 cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_is_f64,
                                 const uint32_t* gen_in, const UpdRec* recs, uint32_t m,
-                                uint64_t n_global, uint32_t frac_bits, uint64_t q_max,
+                                uint64_t n_global, Quant qz,
                                 uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
                                 unsigned long long* tag, uint32_t* epoch_dev,
                                 unsigned long long* n_stale, uint32_t* err, uint64_t* key,
@@ -276,19 +280,40 @@ cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_
   if (m == 0) return cudaSuccess;
   count_launch();
   fused_kernel<<<1, kFusedThreads, 0, s>>>(idx, prio, prio_is_f64, gen_in, recs, m, n_global,
-                                           frac_bits, q_max, local_begin, local_rows, gen, tag,
+                                           qz, local_begin, local_rows, gen, tag,
                                            epoch_dev, n_stale, err, key);
+  return cudaGetLastError();
+}
+
+namespace {
+__global__ void __launch_bounds__(kThreads)
+    alpha_kernel(const void* __restrict__ prio, int prio_is_f64, uint32_t n, double alpha,
+                 double* __restrict__ out) {
+  const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
+  if (k >= n) return;
+  const double p = prio_is_f64 ? static_cast<const double*>(prio)[k]
+                               : (double)static_cast<const float*>(prio)[k];
+  out[k] = apply_alpha(p, alpha);
+}
+}  // namespace
+
+cudaError_t launch_alpha(const void* prio, int prio_is_f64, uint32_t n, double alpha,
+                         double* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  count_launch();
+  alpha_kernel<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(prio, prio_is_f64, n, alpha,
+                                                                 out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_update_quantize(const uint64_t* idx, const void* prio, int prio_is_f64,
                                    const uint32_t* gen, uint32_t n, uint64_t n_global,
-                                   uint32_t frac_bits, uint64_t q_max, UpdRec* out,
+                                   Quant qz, UpdRec* out,
                                    uint32_t* err, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   count_launch();
   quantize_kernel<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(
-      idx, prio, prio_is_f64, gen, n, n_global, frac_bits, q_max, out, err);
+      idx, prio, prio_is_f64, gen, n, n_global, qz, out, err);
   return cudaGetLastError();
 }
 

@@ -90,6 +90,7 @@ struct gear_table {
   uint32_t W = 1, rank = 0, R = 1, S = 1;
   uint64_t Cs = 0, Clocal = 0, N = 0;
   uint32_t F = 32;
+  double alpha = 1.0;  // PER priority exponent (keys are Q_F(p^alpha))
   uint64_t qmax = 0;
   gear_removal removal = GEAR_REMOVE_FIFO;
   uint32_t max_batch = 4096;
@@ -151,6 +152,7 @@ struct gear_table {
   gear::UpdRec* upd_all = nullptr;    // [W*max_batch]
   uint64_t* upd_idx = nullptr;
   double* upd_prio = nullptr;
+  double* upd_pow = nullptr;        // [max_batch] p^alpha (alpha != 1)
   uint32_t* upd_gen = nullptr;
   uint32_t* d_epoch = nullptr;      // update tag epoch (device-resident, advanced by the kernels)
   uint64_t* d_seed = nullptr;       // device seed counter (gear_sample with GEAR_SAMPLE_DEVICE_SEED)

@@ -18,7 +18,7 @@ class Pair:
     """A GPU table (W=1 rank, R virtual shards) and its oracle twin."""
 
     def __init__(self, capacity, seq_len, colspecs, R=1, placement=None, removal=0,
-                 max_batch=4096, frac_bits=32, mirror=True):
+                 max_batch=4096, frac_bits=32, mirror=True, alpha=1.0):
         import torch
         self.torch = torch
         self.cols = []
@@ -27,10 +27,10 @@ class Pair:
             self.cols.append(gear.Column(c.name, DT[c.dtype], tuple(c.shape),
                                          gear.GEAR_HOST if pl == "host" else gear.GEAR_DEVICE))
         self.t = gear.Table(capacity, seq_len, self.cols, None, frac_bits=frac_bits, removal=removal,
-                            shards_per_rank=R, max_batch=max_batch)
+                            shards_per_rank=R, max_batch=max_batch, alpha=alpha)
         self.R, self.N = R, capacity
         self.Cs = capacity // R
-        self.o = oracle.Table(self.Cs, R, frac_bits=frac_bits, removal=removal)
+        self.o = oracle.Table(self.Cs, R, frac_bits=frac_bits, removal=removal, alpha=alpha)
         self.rb = self.t.row_bytes
         self.mirror = [np.zeros((capacity, rb), np.uint8) for rb in self.rb] if mirror else None
         self.content = np.full(capacity, -1, np.int64)   # trajectory id held by each slot

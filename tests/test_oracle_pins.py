@@ -254,6 +254,69 @@ def test_quantize_special_cases(oracle_mod):
 
 
 # --------------------------------------------------------------------------
+# PER exponent alpha (Q7): p -> RN(p^alpha), keys Q_F(RN(p^alpha))
+# --------------------------------------------------------------------------
+def _wide_priorities(n, seed):
+    rng = np.random.default_rng(seed)
+    return np.exp(rng.normal(0.0, 8.0, n))      # ~1e-10 .. 1e10 and beyond
+
+
+def test_pow_alpha_ieee_special_exponents(oracle_mod):
+    """alpha = 1/2 and 2 reduce to single IEEE operations, which are correctly
+    rounded by definition: RN(p^0.5) = sqrt(p), RN(p^2) = p*p, bit for bit."""
+    p = _wide_priorities(3000, 1)
+    p = p[(p > 1e-150) & (p < 1e150)]            # p*p stays finite and normal
+    assert np.array_equal(oracle_mod.pow_alpha(p, 0.5), np.sqrt(p))
+    assert np.array_equal(oracle_mod.pow_alpha(p, 2.0), p * p)
+    assert np.array_equal(oracle_mod.pow_alpha(p, 1.0), p)
+    # exact midpoint of p^2: p = 2^27 - 1 -> p^2 = 2^54 - 2^28 + 1 needs 54 bits;
+    # IEEE p*p rounds the tie to even
+    x = np.array([2.0 ** 27 - 1, 2.0 ** 27 + 1, 3.0 * 2 ** 25 + 1])
+    assert np.array_equal(oracle_mod.pow_alpha(x, 2.0), x * x)
+
+
+def test_pow_alpha_closed_forms_and_libm(oracle_mod):
+    exact = [(4.0, 1.5, 8.0), (0.25, 1.5, 0.125), (9.0, 0.5, 3.0), (1.0, 0.6, 1.0),
+             (2.0, 10.0, 1024.0), (1024.0, 0.1, 2.0), (27.0, 3.0, 19683.0), (2.0 ** -6, 0.5, 0.125)]
+    for p, a, want in exact:
+        assert oracle_mod.pow_alpha(np.array([p]), a)[0] == want, (p, a)
+    # within one ulp of libm's pow (itself < 1 ulp), for PER-typical and odd alphas
+    p = _wide_priorities(2000, 2)
+    for a in (0.6, 0.7, 0.4, 1.3, 3.0, 0.05):
+        got = oracle_mod.pow_alpha(p, a)
+        ref = np.power(p, a)
+        ok = np.isfinite(ref) & (ref > 1e-300)
+        ulp = np.spacing(ref[ok])
+        assert np.all(np.abs(got[ok] - ref[ok]) <= ulp), a
+        # monotone in p
+        order = np.argsort(p)
+        assert np.all(np.diff(got[order]) >= 0)
+    # 0 and invalid values pass through; overflow / underflow clamp, stay positive
+    out = oracle_mod.pow_alpha(np.array([0.0, -1.0, np.inf, 1e300, 1e-300]), 3.0)
+    assert out[0] == 0.0 and out[1] == -1.0 and out[2] == np.inf
+    assert out[3] == np.finfo(np.float64).max and out[4] == 5e-324
+
+
+def test_pow_alpha_keys_through_table(oracle_mod):
+    """The table applies the exponent before Q_F on insert and update: a table
+    with alpha = 1/2 holds the keys of a table with alpha = 1 fed sqrt(p)."""
+    p = _wide_priorities(500, 3)
+    p[::17] = 0.0
+    a = oracle_mod.Table(250, 2, alpha=0.5)
+    b = oracle_mod.Table(250, 2)
+    for s in range(2):
+        a.insert(s, p[s * 250:(s + 1) * 250])
+        b.insert(s, np.sqrt(p[s * 250:(s + 1) * 250]))
+    assert np.array_equal(a.key, b.key)
+    ids = np.arange(0, 500, 3, dtype=np.uint64)
+    q = _wide_priorities(ids.size, 4)
+    a.update(ids, q)
+    b.update(ids, np.sqrt(q))
+    assert np.array_equal(a.key, b.key)
+    assert np.all((a.key > 0) == (np.concatenate([p]) > 0) | np.isin(np.arange(500), ids))
+
+
+# --------------------------------------------------------------------------
 # Update round trip (Q11)
 # --------------------------------------------------------------------------
 def test_update_round_trip_last_writer_wins(oracle_mod):
