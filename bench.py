@@ -320,28 +320,60 @@ def run_gpu(args):
                                         "ms_per_step": ms / args.steps}
             ms, launches = ms_g, launches_g
 
-    # End-to-end through the C-ABI with HOST buffers, one stream: the step's
-    # priority update reads ids + f64 priorities from pinned host memory (H2D
-    # inside gear_update_priorities), gear_sample writes the ids and IS weights
-    # to pinned host memory (D2H inside the call), gear_collect reads the ids
-    # from that host buffer (H2D inside the call) and writes the batch to HBM,
-    # and the host waits for the step before issuing the next one.
+    # End-to-end through the C-ABI with HOST buffers, pipelined like the device
+    # step.  Every step: gear_sample writes the IS weights straight to pinned
+    # host memory (D2H inside the call) and the ids to HBM, from where they are
+    # copied to pinned host memory for the host; gear_update_priorities reads
+    # that step's f64 priorities from pinned host memory (H2D inside the call);
+    # gear_collect (collect stream) gathers the rows into HBM.  The host
+    # consumes each step's ids and weights one step behind (waits for
+    # sample(i-1) and reads its host buffers) while step i runs.  Host buffers
+    # are double buffered.
     barrier()
-    h_idx.copy_(idx.cpu())
+    h_idx2 = [h_idx, torch.empty(B, dtype=torch.int64, pin_memory=True)]
+    h_w2 = [h_w, torch.empty(B, dtype=torch.float32, pin_memory=True)]
+    ev_hs = [torch.cuda.Event() for _ in range(2)]
+    np_idx2 = [x.numpy() for x in h_idx2]   # host views of the pinned buffers
+    np_w2 = [x.numpy() for x in h_w2]
+    consumed = 0.0
+
+    def step_e2e(i):
+        b = i % 2
+        if i >= 2:
+            stream.wait_event(ev_collected[b])   # collect(i-2) has read idx2[b]
+        gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + 7919 + i, cfg.beta,
+                         idx2[b], h_w2[b], None, None, stream)
+        ev_sampled[b].record(stream)
+        with torch.cuda.stream(stream):
+            h_idx2[b].copy_(idx2[b], non_blocking=True)
+        ev_hs[b].record(stream)
+        if cfg.update:
+            gear.gear_update_priorities(t.handle, B, idx2[b], h_prio[i % 16], gear.GEAR_F64,
+                                        None, stream)
+        cstream.wait_event(ev_sampled[b])
+        gear.gear_collect(t.handle, B, idx2[b], col_ids, outs, cstream)
+        ev_collected[b].record(cstream)
+
+    for i in range(args.warmup):
+        step_e2e(i)
+    barrier()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
+    cstream.wait_event(e2)
     for i in range(args.steps):
-        if cfg.update:
-            gear.gear_update_priorities(t.handle, B, h_idx, h_prio[i % 16], gear.GEAR_F64, None, stream)
-        gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + 7919 + i, cfg.beta, h_idx, h_w,
-                         None, None, stream)
-        gear.gear_collect(t.handle, B, h_idx, col_ids, outs, stream)
-        stream.synchronize()     # the host consumes the ids before the next step
+        step_e2e(i)
+        if i >= 1:   # the host reads step i-1's result while step i runs
+            ev_hs[(i - 1) % 2].synchronize()
+            consumed += float(np_w2[(i - 1) % 2][0]) + float(np_idx2[(i - 1) % 2][B - 1])
+    ev_hs[(args.steps - 1) % 2].synchronize()
+    consumed += float(np_w2[(args.steps - 1) % 2][0])
+    stream.wait_stream(cstream)
     e3.record(stream)
     barrier()
+    assert consumed == consumed   # the host did read the results
     e2e_ms = e2.elapsed_time(e3)
-    e2e_h2d = (16 * B if cfg.update else 0) + 8 * B
-    e2e_d2h = 12 * B
+    e2e_h2d = 8 * B if cfg.update else 0    # f64 priorities
+    e2e_d2h = 12 * B                         # u64 ids + f32 weights
 
     times = torch.tensor([ms, e2e_ms, coll_ms_p, ms_serial, coll_ms_s], device="cuda")
     if world > 1:
@@ -378,6 +410,11 @@ def run_gpu(args):
     roof["algorithmic_bytes_per_launch"] = alg
     roof["remote_fraction"] = f_remote
     roof["traffic"] = args.traffic
+    if args.traffic is None and cfg.name == "c2_dt_atari" and world == 1 and args.strategy is None:
+        # dram__bytes_read.sum + dram__bytes_write.sum of collect_tma_kernel<3>
+        # (unchanged since) from ncu --set full at this config
+        roof["traffic"] = (433.055232 + 384.025856) * 1e6
+        roof["traffic_source"] = "profiles/r01e/ncu_collect_tma_full_raw.csv (one launch)"
     # The whole step against the same bound: the step's algorithmic bytes of
     # the binding resource over the (headline) time per step.
     roof["step_achieved"] = alg / (ms / args.steps / 1e3) / 1e9
@@ -407,7 +444,9 @@ def run_gpu(args):
         "roofline": roof,
         "e2e": {"value": traj / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": e2e_h2d,
                 "d2h_bytes_per_step": e2e_d2h,
-                "path": "C-ABI with pinned host ids/priorities/weights; batch in HBM; host sync per step"},
+                "path": ("C-ABI; priorities from pinned host memory, ids and IS weights to "
+                         "pinned host memory, batch in HBM; pipelined (collect on a 2nd stream), "
+                         "the host reads each step's ids and weights one step behind")},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
