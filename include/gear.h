@@ -304,7 +304,15 @@ gear_status gear_table_load(gear_table* t, const char* path);
  *                   inside the step's kernels (default), 0 = NCCL all-gathers;
  *   "update_fused": 1 = priority updates of <= 8192 entries (all ranks) run
  *                   tag + apply in one single-CTA launch (default), 0 = two
- *                   grid-wide launches.
+ *                   grid-wide launches;
+ *   "cdf_levels":   same value on every rank; 2 = two-level CDF (default):
+ *                   every 4096-key tile of a shard holds its own prefix sum,
+ *                   the shard a prefix sum of the tile totals, and a rebuild
+ *                   rescans only the tiles whose keys changed since that CDF
+ *                   buffer was last built (incremental, no look-back);
+ *                   1 = one flat prefix sum per shard rebuilt whole by the
+ *                   decoupled look-back scan.  The sampled ids
+ *                   are identical (synchronises the device).
  * Initial values also come from the environment (GEAR_COLLECT_IMPL=lsu|tma,
  * GEAR_COLLECT_CHUNK, GEAR_TMA_CHUNK).  INVALID_ARG for an unknown key or
  * value. */

@@ -24,6 +24,14 @@ using namespace gear;
 
 namespace {
 
+TileDirty tile_dirty(const gear_table* t) {
+  TileDirty d{};
+  d.bits = t->tile_dirty;
+  d.shard_cap = t->Cs;
+  d.tiles_per_shard = scan_tiles_per_shard(t->Cs);
+  return d;
+}
+
 Quant quant(const gear_table* t) {
   Quant q{};
   q.q_max = t->qmax;
@@ -148,6 +156,7 @@ void destroy_table(gear_table* t) {
     dfree(t->cdf[i]); dfree(t->scan_status[i]); dfree(t->scan_ticket[i]);
   }
   dfree(t->cdf_totals_local); dfree(t->cdf_totals_all);
+  dfree(t->tile_dirty); dfree(t->tile_tot); dfree(t->cdf_buf_mode); dfree(t->scan2_ctr);
   dfree(t->fifo_totals_local); dfree(t->fifo_totals_all);
   dfree(t->d_cdf_ptrs); dfree(t->d_gen_ptrs);
   dfree(t->q_scratch); dfree(t->qmin_slot); dfree(t->done_ctr);
@@ -321,13 +330,23 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_CUDA(cudaMemset(t->ord, 0, t->Clocal * 4));
   const uint32_t tiles = scan_tiles_per_shard(t->Cs) * t->R;
   for (int i = 0; i < 2; ++i) {
-    GEAR_TRY(dalloc(&t->cdf[i], t->Clocal));
-    GEAR_CUDA(cudaMemset(t->cdf[i], 0, t->Clocal * 8));
+    // flat CDF (R*C_s), or tile-local prefixes (R*C_s) + tile prefixes (tiles)
+    GEAR_TRY(dalloc(&t->cdf[i], t->Clocal + tiles));
+    GEAR_CUDA(cudaMemset(t->cdf[i], 0, (t->Clocal + tiles) * 8));
     GEAR_TRY(dalloc(&t->scan_status[i], tiles));
     GEAR_CUDA(cudaMemset(t->scan_status[i], 0, tiles * 8));
     GEAR_TRY(dalloc(&t->scan_ticket[i], 1));
     GEAR_CUDA(cudaMemset(t->scan_ticket[i], 0, 4));
   }
+  // two-level CDF bookkeeping: nothing built yet (buffer modes 0) -> the first
+  // rebuild of each buffer rescans every tile
+  GEAR_TRY(dalloc(&t->tile_dirty, tiles));
+  GEAR_CUDA(cudaMemset(t->tile_dirty, 0, tiles * 4));
+  GEAR_TRY(dalloc(&t->tile_tot, 2 * (size_t)tiles));
+  GEAR_TRY(dalloc(&t->cdf_buf_mode, 2));
+  GEAR_CUDA(cudaMemset(t->cdf_buf_mode, 0, 8));
+  GEAR_TRY(dalloc(&t->scan2_ctr, t->R + 1));
+  GEAR_CUDA(cudaMemset(t->scan2_ctr, 0, (t->R + 1) * 4));
   GEAR_TRY(dalloc(&t->cdf_totals_local, t->R));
   GEAR_TRY(dalloc(&t->cdf_totals_all, t->S));
   GEAR_TRY(dalloc(&t->fifo_totals_local, t->R));
@@ -663,7 +682,7 @@ gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* c
     sp.total_chunks = chunks;
     GEAR_CUDA(launch_scatter(sp, s));
     GEAR_CUDA(launch_insert_meta(t->d_meta, n_meta, t->d_ord, n_ord, quant(t), t->key,
-                                 t->seq, t->gen, t->ord, s));
+                                 tile_dirty(t), t->seq, t->gen, t->ord, s));
     if (out_idx) {
       if (mem_kind(out_idx) == MemKind::Device) {
         GEAR_CUDA(cudaMemcpyAsync(out_idx + k0, t->h_out, m * 8, cudaMemcpyHostToDevice, s));
@@ -719,7 +738,7 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
     // one launch: quantise, tag, block barrier, apply
     GEAR_CUDA(launch_update_fused(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, nullptr, n, t->N,
                                   qz, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
-                                  t->n_stale, t->err, t->key, s));
+                                  t->n_stale, t->err, t->key, tile_dirty(t), s));
   } else if (t->W > 1 && fused && t->peer_xchg) {
     // one launch: quantise, push records to every peer over NVLink, wait for
     // every rank's records, tag, barrier, apply
@@ -727,7 +746,7 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
     mb.epoch_dev = t->d_xep + 1;  // update-exchange epoch (advanced by the kernel)
     GEAR_CUDA(launch_update_xchg(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N, qz,
                                  mb, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
-                                 t->n_stale, t->err, t->key, s));
+                                 t->n_stale, t->err, t->key, tile_dirty(t), s));
   } else {
     GEAR_CUDA(launch_update_quantize(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N,
                                      qz, t->upd_local, t->err, s));
@@ -741,12 +760,12 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
     if (fused) {
       GEAR_CUDA(launch_update_fused(nullptr, nullptr, 0, nullptr, recs, m, t->N, qz,
                                     local_begin, t->Clocal, t->gen, t->tag, t->d_epoch, t->n_stale,
-                                    t->err, t->key, s));
+                                    t->err, t->key, tile_dirty(t), s));
     } else {
       GEAR_CUDA(launch_update_tag(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
                                   t->n_stale, t->err, s));
       GEAR_CUDA(launch_update_apply(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
-                                    t->key, s));
+                                    t->key, tile_dirty(t), s));
     }
   }
   t->dirty = true;
@@ -841,9 +860,14 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     const int mode = strategy == GEAR_UNIFORM ? 1 : 0;
     if (t->dirty || t->cdf_mode != mode) {
       // Rebuild into the buffer peers are not reading (device-resident parity).
-      GEAR_CUDA(launch_scan(t->key, t->cdf[0], t->cdf[1], t->Cs, t->R, mode, t->d_xep + 3,
-                            t->cdf_totals_local, t->scan_status[0], t->scan_ticket[0],
-                            t->scan_ticket[1], s));
+      if (t->cdf_levels == 2)  // incremental: only tiles changed since this buffer's build
+        GEAR_CUDA(launch_scan2(t->key, t->cdf[0], t->cdf[1], t->Cs, t->R, mode, t->d_xep + 3,
+                               t->cdf_totals_local, t->tile_dirty, t->tile_tot, t->cdf_buf_mode,
+                               t->scan2_ctr, t->scan2_ctr + t->R, s));
+      else
+        GEAR_CUDA(launch_scan(t->key, t->cdf[0], t->cdf[1], t->Cs, t->R, mode, t->d_xep + 3,
+                              t->cdf_totals_local, t->scan_status[0], t->scan_ticket[0],
+                              t->scan_ticket[1], s));
       t->scan_launches += 1;
       t->cdf_mode = mode;
       t->dirty = false;
@@ -872,6 +896,8 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     // 1: the sample kernel exchanges; 2: the assign kernel did, read the mailbox
     sp.xchg = xchg ? (affine ? 2 : 1) : 0;
     sp.cdf_ptrs = t->d_cdf_ptrs;
+    sp.cdf_levels = (uint32_t)t->cdf_levels;
+    sp.tiles_per_shard = scan_tiles_per_shard(t->Cs);
     sp.gen_ptrs = t->d_gen_ptrs;
     sp.shard_cap = t->Cs;
     sp.n_shards = t->S;
@@ -1002,6 +1028,12 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     GEAR_CUDA(cudaMemcpy(t->d_seed, &v, 8, cudaMemcpyHostToDevice));
   } else if (!strcmp(key, "peer_xchg") && (value == 0 || value == 1)) {
     t->peer_xchg = (int)value;  // must be set identically on every rank
+  } else if (!strcmp(key, "cdf_levels") && (value == 1 || value == 2)) {
+    // must be set identically on every rank (peers search each other's CDFs)
+    GEAR_CUDA(cudaDeviceSynchronize());
+    GEAR_CUDA(cudaMemset(t->cdf_buf_mode, 0, 8));  // both buffers: full rebuild
+    t->cdf_levels = (int)value;
+    t->dirty = true;
   } else if (!strcmp(key, "update_fused") && (value == 0 || value == 1)) {
     t->update_fused = (int)value;
   } else if (!strcmp(key, "tma_ctas_per_sm") && value >= 1 && value <= 8 &&

@@ -165,6 +165,7 @@ gear_status gear_table_load(gear_table* t, const char* path) {
   GEAR_CUDA(cudaMemset(t->tag, 0, t->Clocal * 8));
   GEAR_CUDA(cudaDeviceSynchronize());
   t->dirty = true;
+  GEAR_CUDA(cudaMemset(t->cdf_buf_mode, 0, 8));  // two-level CDF: rescan every tile
   return GEAR_OK;
 }
 

@@ -33,6 +33,19 @@ struct Quant {
   double alpha;  // PER exponent (1: the priority itself)
 };
 
+// Two-level CDF (kernels/scan.cu, scan2): tiles of kCdfTile keys per shard,
+// each with its own inclusive prefix, plus a per-shard inclusive prefix of
+// the tile totals.  Key writers mark the tile of every key they change dirty
+// for both CDF buffers (bits 0 and 1); a rebuild of buffer b rescans only the
+// tiles whose bit b is set.
+constexpr uint32_t kCdfTile = 4096;
+struct TileDirty {
+  uint32_t* bits;           // [R * tiles_per_shard]
+  uint64_t shard_cap;       // C_s
+  uint32_t tiles_per_shard;
+  uint32_t pad;
+};
+
 // Per-shard totals record exchanged between ranks (16 B): total weight T_s of
 // the shard's CDF with the CDF buffer parity in bit 63 (T_s < 2^62 by q_max),
 // and the number of valid FIFO/LIFO candidates the shard offers.
@@ -188,6 +201,8 @@ struct SampleParams {
   uint64_t shard_cap;                 // C_s
   uint32_t n_shards;                  // S
   uint32_t shards_per_rank;           // R
+  uint32_t cdf_levels;                // 1: flat CDF (scan_kernel), 2: two-level (scan2_kernel)
+  uint32_t tiles_per_shard;           // two-level: tiles of kCdfTile keys per shard
   uint64_t seed;
   uint32_t rank;
   uint32_t B;
@@ -250,6 +265,14 @@ cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf0, uint64_t* cdf1, uin
                         ShardTotals* totals_out, uint64_t* status, uint32_t* ticket,
                         uint32_t* done, cudaStream_t s);
 uint32_t scan_tiles_per_shard(uint64_t shard_cap);
+// Two-level incremental CDF (scan.cu, scan2_kernel): cdf0/cdf1 hold
+// R*C_s tile-local prefixes followed by R*tiles_per_shard tile prefixes;
+// ttot holds each buffer's tile totals ([2][R*tiles_per_shard]).
+cudaError_t launch_scan2(const uint64_t* key, uint64_t* cdf0, uint64_t* cdf1, uint64_t shard_cap,
+                         uint32_t n_shards_local, int indicator, uint64_t* par_dev,
+                         ShardTotals* totals_out, uint32_t* dirty, uint64_t* ttot,
+                         uint32_t* buf_mode, uint32_t* shard_ctr, uint32_t* done,
+                         cudaStream_t s);
 
 // K2/K3/K7: draw + warp-cooperative search + IS weights.
 cudaError_t launch_sample(const SampleParams& p, cudaStream_t s);
@@ -269,7 +292,7 @@ cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_beg
 cudaError_t launch_update_apply(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                                 uint64_t local_rows, const uint32_t* gen,
                                 const unsigned long long* tag, uint32_t* epoch_dev, uint64_t* key,
-                                cudaStream_t s);
+                                TileDirty td, cudaStream_t s);
 
 // Single-launch update for m <= update_fused_max() entries (one CTA): raw
 // W = 1 inputs when idx != nullptr, else all-gathered records.
@@ -280,7 +303,7 @@ cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_
                                 uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
                                 unsigned long long* tag, uint32_t* epoch_dev,
                                 unsigned long long* n_stale, uint32_t* err, uint64_t* key,
-                                cudaStream_t s);
+                                TileDirty td, cudaStream_t s);
 
 // W > 1 collective update through the peer mailboxes, one launch (n*W <=
 // update_fused_max()).
@@ -290,15 +313,15 @@ cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_i
                                uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
                                unsigned long long* tag, uint32_t* epoch_dev,
                                unsigned long long* n_stale, uint32_t* err, uint64_t* key,
-                               cudaStream_t s);
+                               TileDirty td, cudaStream_t s);
 
 // K5: collect (gather) and the insert-side scatter.
 cudaError_t launch_collect(const CollectParams& p, cudaStream_t s);
 cudaError_t launch_scatter(const ScatterParams& p, cudaStream_t s);
 cudaError_t launch_insert_meta(const InsMeta* meta, uint32_t m, const OrdRec* ord_recs,
                                uint32_t n_ord, Quant qz,
-                               uint64_t* key, uint64_t* seq, uint32_t* gen, uint32_t* ord,
-                               cudaStream_t s);
+                               uint64_t* key, TileDirty td, uint64_t* seq, uint32_t* gen,
+                               uint32_t* ord, cudaStream_t s);
 
 // K4: FIFO/LIFO local selection and merge.
 struct FifoRings {

@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
 __global__ void __launch_bounds__(kThreads)
     insert_meta_kernel(const InsMeta* __restrict__ meta, uint32_t m,
                        const OrdRec* __restrict__ ord_recs, uint32_t n_ord, Quant qz,
-                       uint64_t* key, uint64_t* seq, uint32_t* gen,
+                       uint64_t* key, TileDirty td, uint64_t* seq, uint32_t* gen,
                        uint32_t* ord) {
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   if (k < m) {
@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(kThreads)
     uint64_t q = 0;
     quantize(r.prio, qz, &q);  // validated on the host
     key[r.local] = q;
+    mark_tile(td, r.local);
     seq[r.local] = r.seq;
     gen[r.local] += r.gen_inc;
   }
@@ -323,13 +324,13 @@ cudaError_t launch_scatter(const ScatterParams& p, cudaStream_t s) {
 
 cudaError_t launch_insert_meta(const InsMeta* meta, uint32_t m, const OrdRec* ord_recs,
                                uint32_t n_ord, Quant qz,
-                               uint64_t* key, uint64_t* seq, uint32_t* gen, uint32_t* ord,
-                               cudaStream_t s) {
+                               uint64_t* key, TileDirty td, uint64_t* seq, uint32_t* gen,
+                               uint32_t* ord, cudaStream_t s) {
   const uint32_t n = m > n_ord ? m : n_ord;
   if (n == 0) return cudaSuccess;
   count_launch();
   insert_meta_kernel<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(
-      meta, m, ord_recs, n_ord, qz, key, seq, gen, ord);
+      meta, m, ord_recs, n_ord, qz, key, td, seq, gen, ord);
   return cudaGetLastError();
 }
 

@@ -67,6 +67,14 @@ __device__ __forceinline__ bool quantize(double p, const Quant& qz, uint64_t* q)
   return quantize_fixed(apply_alpha(p, qz.alpha), qz, q);
 }
 
+// A key of rank-local slot `local` changed: its CDF tile is stale in both
+// buffers.
+__device__ __forceinline__ void mark_tile(const TileDirty& d, uint64_t local) {
+  const uint64_t ls = local / d.shard_cap;
+  const uint64_t i = local - ls * d.shard_cap;
+  d.bits[ls * d.tiles_per_shard + i / kCdfTile] = 3u;
+}
+
 // Relaxed 64-bit global loads/stores for the look-back status words.
 __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
   uint64_t v;

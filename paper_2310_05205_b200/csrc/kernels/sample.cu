@@ -25,8 +25,11 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-__device__ __forceinline__ uint64_t search_shard(const uint64_t* __restrict__ c, uint64_t n,
-                                                 uint64_t u, int lane, uint64_t* q_out) {
+// min{ i < n : c[i] > u } for a non-decreasing c with c[n-1] > u; also
+// returns c[i] and c[i-1] (0 for i == 0).
+__device__ __forceinline__ uint64_t search_bin(const uint64_t* __restrict__ c, uint64_t n,
+                                               uint64_t u, int lane, uint64_t* c_at,
+                                               uint64_t* c_prev) {
   uint64_t lo = 0, hi = n;  // answer in [lo, hi); c[hi-1] > u
   while (hi - lo > 32) {
     const uint64_t len = hi - lo;
@@ -35,7 +38,7 @@ __device__ __forceinline__ uint64_t search_shard(const uint64_t* __restrict__ c,
     piv = piv > hi - 1 ? hi - 1 : piv;
     const bool gt = c[piv] > u;
     const unsigned m = __ballot_sync(kFull, gt);
-    const int f = __ffs(m) - 1;
+    const int f = m ? __ffs(m) - 1 : 31;  // m == 0 only on a corrupt CDF: still terminates
     const uint64_t piv_f = __shfl_sync(kFull, piv, f);
     const uint64_t piv_b = __shfl_sync(kFull, piv, f > 0 ? f - 1 : 0);
     hi = piv_f + 1;
@@ -45,15 +48,39 @@ __device__ __forceinline__ uint64_t search_shard(const uint64_t* __restrict__ c,
   const uint64_t cv = pos < hi ? c[pos] : ~0ull;
   const uint64_t before = (lane == 0 && lo > 0) ? c[lo - 1] : 0ull;
   const unsigned m = __ballot_sync(kFull, pos < hi && cv > u);
-  const int f = __ffs(m) - 1;
-  const uint64_t cf = __shfl_sync(kFull, cv, f);
+  const int f = m ? __ffs(m) - 1 : 0;
   const uint64_t cprev_lane = __shfl_sync(kFull, cv, f > 0 ? f - 1 : 0);
   const uint64_t cprev0 = __shfl_sync(kFull, before, 0);
-  *q_out = cf - (f > 0 ? cprev_lane : cprev0);
+  *c_at = __shfl_sync(kFull, cv, f);
+  *c_prev = f > 0 ? cprev_lane : cprev0;
   return lo + (uint64_t)f;
 }
 
-__global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
+// Bin of offset u within shard s (0 <= u < T_s); q = its weight.
+//  levels 1: flat inclusive prefix C of the shard (decoupled look-back scan).
+//  levels 2: tile prefixes P then the tile's own prefix L (scan2_kernel);
+//            L_s sits at cdf, P_s after the R*C_s tile-local prefixes.
+__device__ __forceinline__ uint64_t search_shard(const uint64_t* __restrict__ cdf,
+                                                 const SampleParams& p, uint32_t s, uint64_t u,
+                                                 int lane, uint64_t* q_out) {
+  uint64_t at, prev;
+  if (p.cdf_levels != 2) {
+    const uint64_t i = search_bin(cdf, p.shard_cap, u, lane, &at, &prev);
+    *q_out = at - prev;
+    return i;
+  }
+  const uint64_t ls = s % p.shards_per_rank;
+  const uint64_t tps = p.tiles_per_shard;
+  const uint64_t* P = cdf - ls * p.shard_cap + (uint64_t)p.shards_per_rank * p.shard_cap + ls * tps;
+  const uint64_t t = search_bin(P, tps, u, lane, &at, &prev);
+  const uint64_t begin = t * kCdfTile;
+  const uint64_t cnt = min((uint64_t)kCdfTile, p.shard_cap - begin);
+  const uint64_t i = search_bin(cdf + begin, cnt, u - prev, lane, &at, &prev);
+  *q_out = at - prev;
+  return begin + i;
+}
+
+__global__ void __launch_bounds__(kThreads) sample_kernel(const __grid_constant__ SampleParams p) {
   __shared__ unsigned long long s_min[kWarps];
   __shared__ bool s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -101,7 +128,7 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(SampleParams p) {
       const uint64_t Ts_s = __shfl_sync(kFull, Ts, s);
       const uint32_t par_s = __shfl_sync(kFull, par, s);
       const uint64_t* cdf = p.cdf_ptrs[(uint64_t)par_s * S + s];
-      const uint64_t i = search_shard(cdf, p.shard_cap, u - (Gs_incl - Ts_s), lane, &q);
+      const uint64_t i = search_shard(cdf, p, (uint32_t)s, u - (Gs_incl - Ts_s), lane, &q);
       g = (uint64_t)s * p.shard_cap + i;
       if (lane == 0) {
         if (p.out_gen) {

@@ -184,7 +184,189 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(
   }
 }
 
+// Two-level CDF (NEXT-3, incremental): tile t of shard s holds the inclusive
+// prefix of its own keys, L[i] = sum of the tile's keys up to i, and the
+// shard holds P[t] = sum of the totals of tiles 0..t, so the flat CDF is
+// C[t*kTile + i] = P[t-1] + L[i].  No look-back: tiles are independent.  A
+// rebuild of buffer b rescans only the tiles whose dirty bit b is set (every
+// key writer sets both bits of its tile), or every tile when the buffer was
+// last built in the other mode (weights vs indicator); the last tile of each
+// shard to arrive recomputes P from the tile totals, and the last shard flips
+// the parity and records the buffer's mode.  Buffer layout: L of the R shards
+// (R*C_s u64) followed by P of the R shards (R*tiles_per_shard u64).
+template <bool kIndicator>
+__global__ void __launch_bounds__(kThreads) scan2_kernel(
+    const uint64_t* __restrict__ key, uint64_t* __restrict__ cdf0, uint64_t* __restrict__ cdf1,
+    uint64_t shard_cap, uint32_t tiles_per_shard, uint32_t n_shards_local, uint64_t* par_dev,
+    ShardTotals* totals, uint32_t* __restrict__ dirty, uint64_t* __restrict__ ttot0,
+    uint64_t* __restrict__ ttot1, uint32_t* buf_mode, uint32_t* shard_ctr, uint32_t* done) {
+  static_assert(kTile == (int)kCdfTile, "tile of the dirty map");
+  const uint32_t t = blockIdx.x;
+  // The four control words only change at kernel boundaries (the last CTA
+  // writes parity and mode after every CTA has read them): one round trip.
+  const uint64_t par_old = __ldcg(par_dev);
+  const uint32_t mode0 = __ldcg(buf_mode), mode1 = __ldcg(buf_mode + 1);
+  const uint32_t dirty_t = __ldcg(dirty + t);
+  const uint32_t parity = (uint32_t)(par_old & 1) ^ 1u;
+  uint64_t* __restrict__ cdf = parity ? cdf1 : cdf0;
+  uint64_t* __restrict__ ttot = parity ? ttot1 : ttot0;  // this buffer's tile totals
+  const uint32_t mode = kIndicator ? 2u : 1u;
+  __shared__ uint64_t s_k[kTile + kTile / 16];
+  __shared__ uint64_t s_warp[kThreads / 32];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t shard = t / tiles_per_shard;
+  const uint32_t tt = t - shard * tiles_per_shard;
+  const bool full = (parity ? mode1 : mode0) != mode;
+  const uint32_t bit = 1u << parity;
+
+  if (full || (dirty_t & bit)) {
+    const uint64_t tile_begin = (uint64_t)tt * kTile;
+    const uint64_t gbase = (uint64_t)shard * shard_cap + tile_begin;
+    const uint32_t count = (uint32_t)min((uint64_t)kTile, shard_cap - tile_begin);
+    const bool vec = count == (uint32_t)kTile && (gbase & 1) == 0;
+    if (vec) {
+      const ulonglong2* src = reinterpret_cast<const ulonglong2*>(key + gbase);
+#pragma unroll
+      for (int it = 0; it < kItems / 2; ++it) {
+        const int vi = it * kThreads + tid;
+        const ulonglong2 x = __ldg(src + vi);
+        const int p = pad(2 * vi);
+        s_k[p] = x.x;
+        s_k[p + 1] = x.y;
+      }
+    } else {
+#pragma unroll
+      for (int it = 0; it < kItems; ++it) {
+        const int e = it * kThreads + tid;
+        s_k[pad(e)] = (uint32_t)e < count ? key[gbase + e] : 0ull;
+      }
+    }
+    __syncthreads();
+    uint64_t v[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const uint64_t x = s_k[tid * (kItems + 1) + i];
+      v[i] = kIndicator ? (x > 0 ? 1ull : 0ull) : x;
+    }
+#pragma unroll
+    for (int i = 1; i < kItems; ++i) v[i] += v[i - 1];
+    const uint64_t incl = warp_incl_scan_u64(v[kItems - 1], lane);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    uint64_t warp_excl = 0, agg = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const uint64_t x = s_warp[w];
+      warp_excl += (w < warp) ? x : 0ull;
+      agg += x;
+    }
+    const uint64_t base = warp_excl + incl - v[kItems - 1];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) s_k[tid * (kItems + 1) + i] = base + v[i];
+    __syncthreads();
+    uint64_t* dst_l = cdf + gbase;
+    if (vec) {
+      ulonglong2* dst = reinterpret_cast<ulonglong2*>(dst_l);
+#pragma unroll
+      for (int it = 0; it < kItems / 2; ++it) {
+        const int vi = it * kThreads + tid;
+        const int p = pad(2 * vi);
+        dst[vi] = make_ulonglong2(s_k[p], s_k[p + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int it = 0; it < kItems; ++it) {
+        const int e = it * kThreads + tid;
+        if ((uint32_t)e < count) dst_l[e] = s_k[pad(e)];
+      }
+    }
+    if (tid == 0) {
+      ttot[t] = agg;
+      dirty[t] = dirty_t & ~bit;
+    }
+  }
+  // Arrival of this tile; the shard's last tile builds P.
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(shard_ctr + shard, 1u) == tiles_per_shard - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // Level 2: P = inclusive prefix of this buffer's tile totals (rescanned
+  // now or kept from this buffer's last build, in this buffer's mode), in
+  // coalesced chunks of 4 totals per thread.
+  uint64_t* P = cdf + (uint64_t)n_shards_local * shard_cap + (uint64_t)shard * tiles_per_shard;
+  const uint64_t* tot = ttot + (uint64_t)shard * tiles_per_shard;
+  uint64_t carry = 0;
+  for (uint32_t c0 = 0; c0 < tiles_per_shard; c0 += 4 * kThreads) {
+    uint64_t x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t c = c0 + 4 * tid + k;
+      x[k] = c < tiles_per_shard ? __ldcg(tot + c) : 0ull;
+    }
+    x[1] += x[0];
+    x[2] += x[1];
+    x[3] += x[2];
+    const uint64_t incl = warp_incl_scan_u64(x[3], lane);
+    __syncthreads();  // s_warp of the previous use consumed
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    uint64_t warp_excl = 0, agg = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      const uint64_t y = s_warp[w];
+      warp_excl += (w < warp) ? y : 0ull;
+      agg += y;
+    }
+    const uint64_t base = carry + warp_excl + incl - x[3];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t c = c0 + 4 * tid + k;
+      if (c < tiles_per_shard) P[c] = base + x[k];
+    }
+    carry += agg;
+  }
+  if (tid == 0) {
+    ShardTotals r;
+    r.total_and_parity = carry | ((uint64_t)parity << 63);
+    r.aux = 0;
+    totals[shard] = r;
+    shard_ctr[shard] = 0;
+    __threadfence();
+    if (atomicAdd(done, 1u) == n_shards_local - 1) {  // every shard is built
+      *done = 0;
+      buf_mode[parity] = mode;
+      *par_dev = parity;  // every tile read the old parity before arriving
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_scan2(const uint64_t* key, uint64_t* cdf0, uint64_t* cdf1, uint64_t shard_cap,
+                         uint32_t n_shards_local, int indicator, uint64_t* par_dev,
+                         ShardTotals* totals_out, uint32_t* dirty, uint64_t* ttot,
+                         uint32_t* buf_mode, uint32_t* shard_ctr, uint32_t* done,
+                         cudaStream_t s) {
+  const uint32_t tps = scan_tiles_per_shard(shard_cap);
+  const uint32_t n_tiles = tps * n_shards_local;
+  count_launch();
+  if (indicator)
+    scan2_kernel<true><<<n_tiles, kThreads, 0, s>>>(key, cdf0, cdf1, shard_cap, tps,
+                                                    n_shards_local, par_dev, totals_out, dirty,
+                                                    ttot, ttot + n_tiles, buf_mode, shard_ctr,
+                                                    done);
+  else
+    scan2_kernel<false><<<n_tiles, kThreads, 0, s>>>(key, cdf0, cdf1, shard_cap, tps,
+                                                     n_shards_local, par_dev, totals_out, dirty,
+                                                     ttot, ttot + n_tiles, buf_mode, shard_ctr,
+                                                     done);
+  return cudaGetLastError();
+}
 
 uint32_t scan_tiles_per_shard(uint64_t shard_cap) {
   return (uint32_t)((shard_cap + kTile - 1) / kTile);

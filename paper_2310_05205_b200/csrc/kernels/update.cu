@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kThreads)
     apply_kernel(const UpdRec* __restrict__ recs, uint32_t m, uint64_t local_begin,
                  uint64_t local_rows, const uint32_t* __restrict__ gen,
                  const unsigned long long* __restrict__ tag, const uint32_t* epoch_dev,
-                 uint64_t* key) {
+                 uint64_t* key, TileDirty td) {
   const uint32_t epoch = *epoch_dev + 1;
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   if (k >= m) return;
@@ -95,8 +95,10 @@ __global__ void __launch_bounds__(kThreads)
   uint64_t local;
   bool stale;
   if (owned_and_fresh(r, local_begin, local_rows, gen, &local, &stale) &&
-      tag[local] == (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1)))
+      tag[local] == (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1))) {
     key[local] = r.q;
+    mark_tile(td, local);
+  }
 }
 
 // Single-CTA variant for up to kFusedMax entries: tag pass, block barrier,
@@ -112,7 +114,8 @@ __global__ void __launch_bounds__(kFusedThreads)
                  const uint32_t* __restrict__ gen_in, const UpdRec* __restrict__ recs, uint32_t m,
                  uint64_t n_global, Quant qz, uint64_t local_begin,
                  uint64_t local_rows, const uint32_t* __restrict__ gen, unsigned long long* tag,
-                 uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err, uint64_t* key) {
+                 uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err, uint64_t* key,
+                 TileDirty td) {
   const uint32_t epoch = *epoch_dev + 1;  // device-resident: graph-replayable
   UpdRec r[kFusedPer];
   bool mine[kFusedPer];
@@ -156,8 +159,10 @@ __global__ void __launch_bounds__(kFusedThreads)
   for (int u = 0; u < kFusedPer; ++u) {
     const uint32_t k = threadIdx.x + u * kFusedThreads;
     if (mine[u] && __ldcg(tag + loc[u]) ==
-                       (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1)))
+                       (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1))) {
       key[loc[u]] = r[u].q;
+      mark_tile(td, loc[u]);
+    }
   }
   __syncthreads();  // every thread has read the epoch before it advances
   if (threadIdx.x == 0) *epoch_dev = epoch;
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(kFusedThreads)
                 Quant qz, const __grid_constant__ Mbox mb0,
                 uint64_t local_begin, uint64_t local_rows, const uint32_t* __restrict__ gen,
                 unsigned long long* tag, uint32_t* epoch_dev, unsigned long long* n_stale,
-                uint32_t* err, uint64_t* key) {
+                uint32_t* err, uint64_t* key, TileDirty td) {
   const uint32_t epoch = *epoch_dev + 1;  // device-resident tag epoch
   const Mbox mb = mbox_at_next_epoch(mb0);  // device-resident exchange epoch
   const MboxLayout L = mbox_layout(mb.W, mb.S, mb.MB);
@@ -240,8 +245,10 @@ __global__ void __launch_bounds__(kFusedThreads)
   for (int u = 0; u < kFusedPer; ++u) {
     const uint32_t k = threadIdx.x + u * kFusedThreads;
     if (mine[u] && __ldcg(tag + loc[u]) ==
-                       (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1)))
+                       (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1))) {
       key[loc[u]] = r[u].q;
+      mark_tile(td, loc[u]);
+    }
   }
   __syncthreads();  // every thread has read the epoch before it advances
   if (threadIdx.x == 0) {
@@ -262,11 +269,11 @@ cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_i
                                uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
                                unsigned long long* tag, uint32_t* epoch_dev,
                                unsigned long long* n_stale, uint32_t* err, uint64_t* key,
-                               cudaStream_t s) {
+                               TileDirty td, cudaStream_t s) {
   count_launch();
   xchg_kernel<<<1, kFusedThreads, 0, s>>>(idx, prio, prio_is_f64, gen_in, n, n_global, qz, mb,
                                           local_begin, local_rows, gen, tag, epoch_dev,
-                                          n_stale, err, key);
+                                          n_stale, err, key, td);
   return cudaGetLastError();
 }
 
@@ -276,12 +283,12 @@ cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_
                                 uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
                                 unsigned long long* tag, uint32_t* epoch_dev,
                                 unsigned long long* n_stale, uint32_t* err, uint64_t* key,
-                                cudaStream_t s) {
+                                TileDirty td, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   count_launch();
   fused_kernel<<<1, kFusedThreads, 0, s>>>(idx, prio, prio_is_f64, gen_in, recs, m, n_global,
                                            qz, local_begin, local_rows, gen, tag,
-                                           epoch_dev, n_stale, err, key);
+                                           epoch_dev, n_stale, err, key, td);
   return cudaGetLastError();
 }
 
@@ -331,12 +338,12 @@ cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_beg
 cudaError_t launch_update_apply(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                                 uint64_t local_rows, const uint32_t* gen,
                                 const unsigned long long* tag, uint32_t* epoch_dev, uint64_t* key,
-                                cudaStream_t s) {
+                                TileDirty td, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   count_launch(2);
   apply_kernel<<<(m + kThreads - 1) / kThreads, kThreads, 0, s>>>(recs, m, local_begin,
                                                                   local_rows, gen, tag, epoch_dev,
-                                                                  key);
+                                                                  key, td);
   epoch_bump_kernel<<<1, 1, 0, s>>>(epoch_dev);  // after every apply block read it
   return cudaGetLastError();
 }

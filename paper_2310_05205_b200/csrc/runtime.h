@@ -110,6 +110,11 @@ struct gear_table {
   uint64_t scan_launches = 0;
   int cdf_mode = -1;      // -1 none, 0 weighted keys, 1 indicator
   bool dirty = true;
+  int cdf_levels = 2;     // 1: flat CDF (decoupled look-back), 2: two-level incremental
+  uint32_t* tile_dirty = nullptr;    // [R*tiles] bit b: tile changed since buffer b's build
+  uint64_t* tile_tot = nullptr;      // [2][R*tiles] each buffer's tile totals
+  uint32_t* cdf_buf_mode = nullptr;  // [2] mode each buffer was built in (0 none, 1 w, 2 ind)
+  uint32_t* scan2_ctr = nullptr;     // [R+1] per-shard arrivals, shards done
   gear::ShardTotals* cdf_totals_local = nullptr;  // [R]
   gear::ShardTotals* cdf_totals_all = nullptr;    // [S]
   gear::ShardTotals* fifo_totals_local = nullptr; // [R]

@@ -137,6 +137,36 @@ def test_quantize_edges_on_gpu(torch_cuda):
     P.close()
 
 
+@pytest.mark.parametrize("levels", [2, 1])
+def test_cdf_levels_incremental(torch_cuda, levels):
+    """The two-level incremental CDF (default) and the flat look-back CDF give
+    the oracle's draws through: a first build, sparse updates (a few dirty
+    tiles of a few shards), no-change samples, alternating UNIFORM (indicator)
+    and PRIORITIZED (weights) builds -- each CDF buffer remembers its own
+    mode -- inserts, and a ragged last tile."""
+    cols = [synth.ColSpec("x", "u8", (8,))]
+    R, Cs = 3, 10_000                       # 3 tiles per shard, the last ragged
+    P = _pair(capacity=Cs * R, seq_len=1, colspecs=cols, R=R)
+    G.gear_table_set_tuning(P.t.handle, "cdf_levels", levels)
+    rng = np.random.default_rng(5)
+    P.fill(synth.priorities(Cs * R, seed=3, zero_frac=0.1))
+    seed = 100
+    for rnd in range(6):
+        strat = G.GEAR_UNIFORM if rnd in (2, 3) else G.GEAR_PRIORITIZED
+        P.check_sample(strat, 4096, seed)
+        seed += 1
+        P.check_sample(strat, 777, seed)    # nothing changed: no rebuild
+        seed += 1
+        ids = rng.choice(Cs * R, size=int(rng.integers(1, 6)), replace=False).astype(np.uint64)
+        P.update(ids, rng.lognormal(0, 3, ids.size) * (rng.random(ids.size) > 0.3))
+    P.insert(1, synth.priorities(50, seed=9))
+    P.check_sample(G.GEAR_WEIGHTED, 4096, seed)
+    P.check_sample(G.GEAR_UNIFORM, 4096, seed + 1)
+    G.gear_table_set_tuning(P.t.handle, "cdf_levels", 3 - levels)   # switch layouts
+    P.check_sample(G.GEAR_PRIORITIZED, 4096, seed + 2)
+    P.close()
+
+
 @pytest.mark.parametrize("alpha", [0.6, 0.7, 0.4, 1.3, 3.0, 0.05, 7.5, 0.5, 2.0])
 def test_priority_alpha_keys(torch_cuda, alpha):
     """PER exponent (Q7): keys Q_F(RN(p^alpha)) made on the GPU (double-double
