@@ -24,7 +24,7 @@ _SRC = os.path.join(_HERE, "gear_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 FIFO, LIFO, UNIFORM, WEIGHTED, PRIORITIZED, TOPK = 0, 1, 2, 3, 4, 5
-OK, BAD_PRIORITY, INDEX_RANGE, STALE, EMPTY, INVALID = 0, 1, 2, 4, 8, 16
+OK, BAD_PRIORITY, INDEX_RANGE, STALE, EMPTY, INVALID, FULL = 0, 1, 2, 4, 8, 16, 32
 IDX_NONE = np.uint64(0xFFFFFFFFFFFFFFFF)
 
 
@@ -66,13 +66,17 @@ def lib():
         L.gor_sample.restype = i32
         L.gor_sample_owner_affine.argtypes = [i32, P, P, u64, u32, u32, u32, u32, u64, f64, P, P, P]
         L.gor_sample_owner_affine.restype = i32
-        L.gor_update.argtypes = [P, P, u64, u32, u32, P, P, P, P]
+        L.gor_update.argtypes = [P, P, P, u64, u32, u32, P, P, P, P]
         L.gor_update.restype = i32
         L.gor_translate.argtypes = [u64, u64, P, P]
         L.gor_collect.argtypes = [P, u64, u64, u32, P, P]
         L.gor_collect.restype = i32
         L.gor_insert.argtypes = [P, P, P, u64, u64, u32, u32, u32, P, P, u32, P, P]
         L.gor_insert.restype = i32
+        L.gor_allocate.argtypes = [P, P, P, u64, u32, u32, P, u32, P]
+        L.gor_allocate.restype = i32
+        L.gor_commit.argtypes = [P, P, P, u64, u64, u32, u32, P, u32, P, P]
+        L.gor_commit.restype = i32
         _lib = L
     return _lib
 
@@ -178,14 +182,15 @@ def sample_owner_affine(strategy: int, key: np.ndarray, seq: np.ndarray | None, 
     return st, idx, w, p
 
 
-def update(key: np.ndarray, gen: np.ndarray, frac_bits: int, idx, p, gen_in=None):
+def update(key: np.ndarray, seq: np.ndarray, gen: np.ndarray, frac_bits: int, idx, p,
+           gen_in=None):
     """In-place on key.  Returns (status bitmask, n_stale)."""
-    assert key.dtype == np.uint64 and gen.dtype == np.uint32
+    assert key.dtype == np.uint64 and seq.dtype == np.uint64 and gen.dtype == np.uint32
     idx = np.ascontiguousarray(idx, dtype=np.uint64)
     p = np.ascontiguousarray(p, dtype=np.float64)
     gi = None if gen_in is None else np.ascontiguousarray(gen_in, dtype=np.uint32)
     ns = np.zeros(1, dtype=np.uint64)
-    st = lib().gor_update(_p(key), _p(gen), key.size, frac_bits, idx.size, _p(idx), _p(p),
+    st = lib().gor_update(_p(key), _p(seq), _p(gen), key.size, frac_bits, idx.size, _p(idx), _p(p),
                           _p(gi), _p(ns))
     return st, int(ns[0])
 
@@ -243,7 +248,25 @@ class Table:
         return st, out
 
     def update(self, idx, p, gen_in=None):
-        return update(self.key, self.gen, self.F, idx, pow_alpha(p, self.alpha), gen_in)
+        return update(self.key, self.seq, self.gen, self.F, idx, pow_alpha(p, self.alpha), gen_in)
+
+    def allocate(self, shard: int, n: int) -> tuple[int, np.ndarray]:
+        """Split writer API (Q21): n ongoing slots of `shard`."""
+        out = np.zeros(n, dtype=np.uint64)
+        nf = self.next_free[shard:shard + 1].copy()
+        st = lib().gor_allocate(_p(self.key), _p(self.seq), _p(self.gen), self.cap, shard,
+                                self.removal, _p(nf), n, _p(out))
+        self.next_free[shard] = nf[0]
+        return st, out
+
+    def commit(self, shard: int, idx, prio) -> int:
+        idx = np.ascontiguousarray(idx, dtype=np.uint64)
+        prio = pow_alpha(prio, self.alpha)
+        sc = self.seq_ctr[shard:shard + 1].copy()
+        st = lib().gor_commit(_p(self.key), _p(self.seq), _p(self.gen), self.cap, self.n, shard,
+                              self.F, _p(sc), idx.size, _p(idx), _p(prio))
+        self.seq_ctr[shard] = sc[0]
+        return st
 
     def sample(self, strategy, n_ranks, rank, B, seed, beta=0.0, owner_affine=False):
         fn = sample_owner_affine if owner_affine else sample

@@ -276,7 +276,7 @@ int gor_sample_owner_affine(int strategy, const uint64_t* key, const uint64_t* s
 }
 
 /* Q11: apply the list in order; the last valid writer of a slot wins. */
-int gor_update(uint64_t* key, const uint32_t* gen, uint64_t n_global,
+int gor_update(uint64_t* key, const uint64_t* seq, const uint32_t* gen, uint64_t n_global,
                uint32_t frac_bits, uint32_t n, const uint64_t* idx, const double* p,
                const uint32_t* gen_in, uint64_t* n_stale) {
   int err = GOR_OK;
@@ -287,7 +287,8 @@ int gor_update(uint64_t* key, const uint32_t* gen, uint64_t n_global,
     if (g >= n_global) { err |= GOR_INDEX_RANGE; continue; }
     uint64_t q;
     if (gor_quantize(p[k], frac_bits, qmax, &q) != GOR_OK) { err |= GOR_BAD_PRIORITY; continue; }
-    if (gen[g] == 0 || (gen_in && gen_in[k] != gen[g])) {
+    /* never inserted (gen 0) or allocated but not committed (seq 0, Q21) */
+    if (gen[g] == 0 || seq[g] == 0 || (gen_in && gen_in[k] != gen[g])) {
       err |= GOR_STALE;
       if (n_stale) ++*n_stale;
       continue;
@@ -313,8 +314,32 @@ int gor_collect(const uint8_t* col, uint64_t n_global, uint64_t row_bytes,
   return GOR_OK;
 }
 
+/* The committed slot of shard [base, base+cap) a full free queue evicts:
+ * smallest seq (FIFO removal) or largest (LIFO removal) among committed slots
+ * (seq != 0; ongoing slots -- allocated, not committed -- have seq 0).
+ * UINT64_MAX if none. */
+static uint64_t victim(const uint64_t* seq, uint64_t base, uint64_t cap, uint32_t removal) {
+  uint64_t best = UINT64_MAX;
+  for (uint64_t i = 0; i < cap; ++i) {
+    uint64_t h = base + i;
+    if (seq[h] == 0) continue;
+    if (best == UINT64_MAX || (removal == 0 ? (seq[h] < seq[best]) : (seq[h] > seq[best])))
+      best = h;
+  }
+  return best;
+}
+
+/* Free entries plus committed slots of a shard: what n allocations can use. */
+static uint64_t available(const uint64_t* seq, uint64_t base, uint64_t cap, uint64_t next_free) {
+  uint64_t c = cap - next_free;
+  for (uint64_t i = 0; i < cap; ++i) c += seq[base + i] != 0;
+  return c;
+}
+
 /* PAPER.md:186 single free queue; PAPER.md:193 allocate/commit;
- * PAPER.md:195 victim by removal strategy when no index is free. */
+ * PAPER.md:195 victim by removal strategy when no index is free.  Each row is
+ * allocated and committed before the next one (a later row can evict an
+ * earlier one of the same call). */
 int gor_insert(uint64_t* key, uint64_t* seq, uint32_t* gen, uint64_t shard_cap,
                uint64_t n_global, uint32_t shard, uint32_t removal, uint32_t frac_bits,
                uint64_t* next_free, uint64_t* seq_ctr,
@@ -325,20 +350,14 @@ int gor_insert(uint64_t* key, uint64_t* seq, uint32_t* gen, uint64_t shard_cap,
     uint64_t q;
     if (gor_quantize(prio[k], frac_bits, qmax, &q) != GOR_OK) return GOR_BAD_PRIORITY;
   }
+  if (n > 0 && available(seq, base, shard_cap, *next_free) == 0) return GOR_FULL;
   for (uint32_t k = 0; k < n; ++k) {
     uint64_t g;
     if (*next_free < shard_cap) {
       g = base + *next_free;                 /* dequeue from the free queue */
       *next_free += 1;
     } else {
-      uint64_t best = UINT64_MAX;             /* victim among committed slots */
-      for (uint64_t i = 0; i < shard_cap; ++i) {
-        uint64_t h = base + i;
-        if (gen[h] == 0) continue;
-        if (best == UINT64_MAX) { best = h; continue; }
-        if (removal == 0 ? (seq[h] < seq[best]) : (seq[h] > seq[best])) best = h;
-      }
-      g = best;
+      g = victim(seq, base, shard_cap, removal);
     }
     uint64_t q;
     gor_quantize(prio[k], frac_bits, qmax, &q);
@@ -349,4 +368,61 @@ int gor_insert(uint64_t* key, uint64_t* seq, uint32_t* gen, uint64_t shard_cap,
     out_idx[k] = g;
   }
   return GOR_OK;
+}
+
+/* PAPER.md:193 steps 3-4 ("requests a free index from the block allocator"),
+ * reading Q21: n indices of shard s, each from the free queue or, when it is
+ * empty, by evicting the victim of the removal strategy.  An
+ * allocated slot is ongoing: gen += 1, key = 0 and seq = 0 (not selectable,
+ * not a victim, updates to it are stale) until it is committed.  All or
+ * nothing: GOR_FULL (and nothing allocated) when fewer than n free or
+ * committed slots exist. */
+int gor_allocate(uint64_t* key, uint64_t* seq, uint32_t* gen, uint64_t shard_cap,
+                 uint32_t shard, uint32_t removal, uint64_t* next_free, uint32_t n,
+                 uint64_t* out_idx) {
+  uint64_t base = (uint64_t)shard * shard_cap;
+  if (available(seq, base, shard_cap, *next_free) < n) {
+    for (uint32_t k = 0; k < n; ++k) out_idx[k] = UINT64_MAX;
+    return GOR_FULL;
+  }
+  for (uint32_t k = 0; k < n; ++k) {
+    uint64_t g;
+    if (*next_free < shard_cap) {
+      g = base + *next_free;
+      *next_free += 1;
+    } else {
+      g = victim(seq, base, shard_cap, removal);
+    }
+    gen[g] += 1;
+    key[g] = 0;
+    seq[g] = 0;
+    out_idx[k] = g;
+  }
+  return GOR_OK;
+}
+
+/* PAPER.md:193 step 5 ("commits the buffer, triggering an update in the
+ * Status Table ... designates the index as available for selection"): in
+ * order, each ongoing id of shard s gets seq = (*seq_ctr)++ and key =
+ * Q_F(prio[k]).  An id outside the shard is skipped with GOR_INDEX_RANGE, one
+ * that is not ongoing (never allocated, already committed -- e.g. the second
+ * copy of a duplicate) with GOR_STALE, an invalid priority with
+ * GOR_BAD_PRIORITY (the slot stays ongoing).  Returns the bitmask. */
+int gor_commit(uint64_t* key, uint64_t* seq, const uint32_t* gen, uint64_t shard_cap,
+               uint64_t n_global, uint32_t shard, uint32_t frac_bits, uint64_t* seq_ctr,
+               uint32_t n, const uint64_t* idx, const double* prio) {
+  int err = GOR_OK;
+  uint64_t qmax = gor_q_max(n_global);
+  uint64_t base = (uint64_t)shard * shard_cap;
+  for (uint32_t k = 0; k < n; ++k) {
+    uint64_t g = idx[k];
+    if (g < base || g >= base + shard_cap) { err |= GOR_INDEX_RANGE; continue; }
+    if (gen[g] == 0 || seq[g] != 0) { err |= GOR_STALE; continue; }
+    uint64_t q;
+    if (gor_quantize(prio[k], frac_bits, qmax, &q) != GOR_OK) { err |= GOR_BAD_PRIORITY; continue; }
+    seq[g] = *seq_ctr;
+    *seq_ctr += 1;
+    key[g] = q;
+  }
+  return err;
 }

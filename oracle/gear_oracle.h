@@ -34,6 +34,7 @@ extern "C" {
 #define GOR_STALE 4
 #define GOR_EMPTY 8
 #define GOR_INVALID 16
+#define GOR_FULL 32
 
 /* Strategies (paper PAPER.md:55 lists FIFO, LIFO, weighted, prioritized;
  * PAPER.md:222 adds uniform). */
@@ -101,11 +102,12 @@ int gor_sample_owner_affine(int strategy, const uint64_t* key, const uint64_t* s
 
 /* Priority update, applied as the concatenation of every rank's list in
  * (rank, position) order, so the last writer wins (Q11).  Entries with an
- * out-of-range id, an invalid priority, a never-inserted slot (gen == 0) or
+ * out-of-range id, an invalid priority, a never-inserted slot (gen == 0), an
+ * allocated but uncommitted one (seq == 0, Q21) or
  * (when gen_in != NULL) a generation mismatch are skipped.  Returns a bitmask
  * of GOR_INDEX_RANGE | GOR_BAD_PRIORITY | GOR_STALE; *n_stale counts stale
  * skips (may be NULL).  p is f64; callers holding f32 widen exactly. */
-int gor_update(uint64_t* key, const uint32_t* gen, uint64_t n_global,
+int gor_update(uint64_t* key, const uint64_t* seq, const uint32_t* gen, uint64_t n_global,
                uint32_t frac_bits, uint32_t n, const uint64_t* idx, const double* p,
                const uint32_t* gen_in, uint64_t* n_stale);
 
@@ -120,14 +122,26 @@ int gor_collect(const uint8_t* col, uint64_t n_global, uint64_t row_bytes,
 /* Insertion into shard s:
  * a free queue per shard seeded 0..cap-1 ascending (*next_free counts the
  * dequeued entries); when it is empty the victim is the committed slot of
- * the shard with the smallest seq (FIFO removal, removal=0) or the largest
- * (LIFO removal, removal=1).  Then seq[g] = (*seq_ctr)++, gen[g]++,
+ * the shard (seq != 0) with the smallest seq (FIFO removal, removal=0) or the
+ * largest (LIFO removal, removal=1).  Then seq[g] = (*seq_ctr)++, gen[g]++,
  * key[g] = Q_F(prio[k]); row bytes are copied by the caller using out_idx.
- * Returns GOR_OK or GOR_BAD_PRIORITY (nothing inserted). */
+ * Row by row (allocate + commit each).  Returns GOR_OK, GOR_BAD_PRIORITY or
+ * GOR_FULL (no free or committed slot at all); nothing inserted on error. */
 int gor_insert(uint64_t* key, uint64_t* seq, uint32_t* gen, uint64_t shard_cap,
                uint64_t n_global, uint32_t shard, uint32_t removal, uint32_t frac_bits,
                uint64_t* next_free, uint64_t* seq_ctr,
                uint32_t n, const double* prio, uint64_t* out_idx);
+
+/* Split writer API (reading Q21): allocate n ongoing slots of
+ * shard s (gen += 1, key = seq = 0; all or nothing, GOR_FULL), the caller
+ * writes the rows in place, then commit them (seq = (*seq_ctr)++, key =
+ * Q_F(prio)).  See gear_oracle.c for the per-entry errors of commit. */
+int gor_allocate(uint64_t* key, uint64_t* seq, uint32_t* gen, uint64_t shard_cap,
+                 uint32_t shard, uint32_t removal, uint64_t* next_free, uint32_t n,
+                 uint64_t* out_idx);
+int gor_commit(uint64_t* key, uint64_t* seq, const uint32_t* gen, uint64_t shard_cap,
+               uint64_t n_global, uint32_t shard, uint32_t frac_bits, uint64_t* seq_ctr,
+               uint32_t n, const uint64_t* idx, const double* prio);
 
 #ifdef __cplusplus
 }

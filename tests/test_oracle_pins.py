@@ -422,6 +422,116 @@ def test_insert_matches_state_machine(oracle_mod, removal):
             assert st == 0 and [int(x) for x in idx] == live[::-1]
 
 
+class _ShardModel:
+    """Independent model of one shard under the split writer API (Q21):
+    a free deque, a deque of committed slots in commit order, a set of
+    ongoing slots and generation counts."""
+
+    def __init__(self, cap, removal):
+        self.free, self.live, self.ongoing = deque(range(cap)), deque(), set()
+        self.removal, self.gen = removal, Counter()
+
+    def take(self):
+        if self.free:
+            return self.free.popleft()
+        return self.live.popleft() if self.removal == 0 else self.live.pop()
+
+    def allocate(self, n):
+        if n > len(self.free) + len(self.live):
+            return None
+        out = []
+        for _ in range(n):
+            g = self.take()
+            self.gen[g] += 1
+            self.ongoing.add(g)
+            out.append(g)
+        return out
+
+    def commit(self, ids, ok_prio):
+        errs = 0
+        for g, ok in zip(ids, ok_prio):
+            if g not in self.ongoing:
+                errs |= 4
+                continue
+            if not ok:
+                errs |= 1
+                continue
+            self.ongoing.discard(g)
+            self.live.append(g)
+        return errs
+
+    def insert(self, n):
+        out = []
+        for _ in range(n):
+            if not self.free and not self.live:
+                return None
+            g = self.take()
+            self.gen[g] += 1
+            self.live.append(g)
+            out.append(g)
+        return out
+
+
+@pytest.mark.parametrize("removal", [0, 1])
+def test_allocate_commit_matches_state_machine(oracle_mod, removal):
+    """gor_allocate / gor_commit (and gor_insert interleaved with them) against
+    the deque model: slot choice, eviction of committed slots only, ongoing
+    slots unselectable and immune to updates, all-or-nothing FULL, commit
+    order = seq order = FIFO selection order, duplicate / stale / bad-priority
+    commits skipped."""
+    rng = np.random.default_rng(40 + removal)
+    for trial in range(60):
+        cap = int(rng.integers(1, 10))
+        t = oracle_mod.Table(shard_cap=cap, n_shards=1, removal=removal)
+        m = _ShardModel(cap, removal)
+        pending = []
+        for _ in range(int(rng.integers(1, 25))):
+            op = rng.integers(0, 3)
+            if op == 0:                                   # allocate
+                n = int(rng.integers(1, 5))
+                st, ids = t.allocate(0, n)
+                want = m.allocate(n)
+                if want is None:
+                    assert st == oracle_mod.FULL
+                    assert np.all(ids == oracle_mod.IDX_NONE)
+                else:
+                    assert st == 0 and [int(x) for x in ids] == want
+                    for g in want:
+                        assert t.key[g] == 0 and t.seq[g] == 0
+                    pending += want
+            elif op == 1 and pending:                     # commit some, maybe duplicated
+                k = int(rng.integers(1, len(pending) + 1))
+                ids = list(rng.permutation(pending)[:k])
+                if rng.random() < 0.3:
+                    ids.append(ids[0])                    # duplicate -> second is stale
+                if rng.random() < 0.2:
+                    ids.append(int(rng.integers(0, cap)))  # maybe not ongoing
+                prio = rng.lognormal(0, 1, len(ids))
+                ok = rng.random(len(ids)) > 0.1
+                prio[~ok] = -1.0
+                st = t.commit(0, np.array(ids, np.uint64), prio)
+                assert st == m.commit(ids, ok)
+                pending = sorted(m.ongoing)
+            else:                                         # combined insert
+                n = int(rng.integers(1, 4))
+                want = m.insert(n)
+                st, ids = t.insert(0, np.ones(n))
+                if want is None:
+                    assert st == oracle_mod.FULL
+                else:
+                    assert st == 0 and [int(x) for x in ids] == want
+            assert [t.gen[g] for g in range(cap)] == [m.gen[g] for g in range(cap)]
+            # updates to ongoing slots are stale; committed order is FIFO order
+            for g in m.ongoing:
+                key = t.key.copy()
+                st, ns = t.update([g], [5.0])
+                assert st & oracle_mod.STALE and ns == 1 and np.array_equal(t.key, key)
+            live = list(m.live)
+            if live:
+                st, idx, _, _ = t.sample(oracle_mod.FIFO, 1, 0, len(live), 0)
+                assert st == 0 and [int(x) for x in idx] == live
+
+
 def test_fifo_lifo_order_and_sharded_merge(oracle_mod):
     """FIFO output strictly ascending in (seq, shard), LIFO strictly
     descending; equals a full sort of selectable (seq, shard) pairs."""
