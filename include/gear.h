@@ -62,6 +62,7 @@ typedef int32_t gear_status;
 #define GEAR_DEVERR_STALE 4u        /* an update hit a never-inserted slot or a stale generation */
 #define GEAR_DEVERR_EMPTY 8u        /* a sample found nothing (or < W*B for FIFO/LIFO) selectable */
 #define GEAR_DEVERR_TIMEOUT 16u     /* a peer-mailbox exchange waited > 4 s for a peer (SPMD broken) */
+#define GEAR_DEVERR_FULL 32u        /* an insert / allocate found too few free or committed slots */
 
 /* Padding id: update entries with this id are ignored (lets ranks with fewer
  * updates pass the common n of a collective update). */
@@ -225,16 +226,60 @@ gear_status gear_column_row_bytes(const gear_table* t, uint32_t col, uint64_t* o
  *   col_src[c]: n rows of column c, [n][row_bytes_c], host or device.
  *   prio:       HOST array of n f64 priorities (0 = stored, not selectable).
  *   out_idx:    n u64 global ids (host or device), may be NULL.
- * If two of the n rows land in one slot (LIFO removal, or n > C_s) the later
- * row wins.  Errors: INVALID_ARG, BAD_PRIORITY (nothing inserted).  Must not
- * overlap a sample/collect of the same step on any rank (caller barrier). */
+ * Each row is allocated and committed before the next (victims are
+ * committed slots only -- never ongoing ones of gear_allocate).  If two of
+ * the n rows land in one slot (LIFO removal, or n > free + committed slots)
+ * the later row wins.  The allocation runs on the device (kernels/alloc.cu);
+ * a host out_idx makes the call synchronise the stream.  Errors: INVALID_ARG,
+ * BAD_PRIORITY (nothing inserted); GEAR_DEVERR_FULL is latched (nothing
+ * inserted) when every slot of the shard is ongoing.  Must not overlap a
+ * sample/collect of the same step on any rank (caller barrier). */
 gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* const* col_src,
                         const double* prio, uint64_t* out_idx, gear_stream stream);
+
+/* Split writer API ("the client initiates an allocate
+ * operation, which generates a buffer containing memory views of the blocks
+ * ... fills with trajectory data ... commits the buffer, triggering an update
+ * in the Status Table"; reading Q21).  Not collective; the block allocator of
+ * each shard lives in device memory, so both calls are stream-ordered, need
+ * no host round trip (unless out_idx is a host pointer: then the call
+ * synchronises the stream) and can be captured in a CUDA graph.
+ *
+ * gear_allocate: n slots of global shard `shard` (owned by this rank): free
+ *   slots first (queue seeded 0..C_s-1 ascending), then victims evicted from
+ *   the committed slots -- the oldest first (FIFO removal) or the newest
+ *   first (LIFO removal).  Each allocated slot is ongoing:
+ *   gen += 1, key = 0 and seq = 0, so it is not selectable, not a victim, and
+ *   updates to it are skipped as stale, until it is committed.  out_idx:
+ *   u64[n] global ids (device or host).  All or nothing: with fewer than n
+ *   free + committed slots, nothing is allocated, out_idx gets GEAR_IDX_NONE
+ *   and GEAR_DEVERR_FULL is latched.
+ * The caller writes each allocated trajectory's rows IN PLACE: row of global
+ *   id g in column c is at gear_column_base(c) + (g - rank*R*C_s) * row_bytes
+ *   (device memory for DEVICE columns, mapped host memory for HOST columns),
+ *   ordered before the commit on the stream.
+ * gear_commit: in order, every ongoing id of `shard` gets seq = the shard's
+ *   next counter value and key = Q_F(prio[k]^alpha), and joins the shard's
+ *   FIFO/LIFO order.  idx: u64[n] (device or host); prio: f64[n] (device or
+ *   host).  Entries outside the shard (INDEX_RANGE), not ongoing -- never
+ *   allocated, already committed, the second copy of a duplicate -- (STALE)
+ *   or with an invalid priority (BAD_PRIORITY; the slot stays ongoing) are
+ *   skipped and latched.  n <= max_batch for both calls. */
+gear_status gear_allocate(gear_table* t, uint32_t shard, uint32_t n, uint64_t* out_idx,
+                          gear_stream stream);
+gear_status gear_commit(gear_table* t, uint32_t shard, uint32_t n, const uint64_t* idx,
+                        const double* prio, gear_stream stream);
+
+/* Base address of this rank's rows of column `col` (R*C_s rows of
+ * row_bytes, rank-local slot order): a device pointer for DEVICE columns, the
+ * mapped host pointer for HOST columns. */
+gear_status gear_column_base(const gear_table* t, uint32_t col, void** out);
 
 /* Set the priorities of n trajectories.  Collective: every rank passes the
  * same n; pad with GEAR_IDX_NONE.  idx: u64 global ids; prio: n values of
  * prio_dtype (GEAR_F32 or GEAR_F64); gen: optional u32 generations (entries
- * whose generation differs from the slot's are skipped as stale).  The
+ * whose generation differs from the slot's are skipped as stale, as are
+ * never-inserted slots and allocated but uncommitted ones).  The
  * priority becomes key = Q_F(p): p == 0 -> 0 (not selectable), else
  * clamp(round_half_even(p * 2^F), 1, q_max).  Entries of all ranks are
  * applied in (rank, position) order -- the last writer wins.  Device-side

@@ -39,6 +39,7 @@ GEAR_DEVERR_BAD_PRIORITY = 2
 GEAR_DEVERR_STALE = 4
 GEAR_DEVERR_EMPTY = 8
 GEAR_DEVERR_TIMEOUT = 16
+GEAR_DEVERR_FULL = 32
 GEAR_IDX_NONE = 0xFFFFFFFFFFFFFFFF
 
 # dtypes / placements / strategies / removal (gear.h enums)
@@ -100,6 +101,9 @@ SIGNATURES = {
     "gear_column_id": ([_P, ctypes.c_char_p, _P], _i32),
     "gear_column_row_bytes": ([_P, _u32, _P], _i32),
     "gear_insert": ([_P, _u32, _u32, _P, _P, _P, _P], _i32),
+    "gear_allocate": ([_P, _u32, _u32, _P, _P], _i32),
+    "gear_commit": ([_P, _u32, _u32, _P, _P, _P], _i32),
+    "gear_column_base": ([_P, _u32, _P], _i32),
     "gear_update_priorities": ([_P, _u32, _P, _P, _i32, _P, _P], _i32),
     "gear_sample": ([_P, _i32, _u32, _u64, _f64, _P, _P, _P, _P, _P], _i32),
     "gear_collect": ([_P, _u32, _P, _u32, _P, _P, _P], _i32),
@@ -256,6 +260,21 @@ def gear_insert(t: int, shard: int, n: int, col_src: Sequence, prio, out_idx=Non
                                              _stream(stream)))
 
 
+def gear_allocate(t: int, shard: int, n: int, out_idx, stream=None):
+    _check("gear_allocate", load().gear_allocate(t, shard, n, _ptr(out_idx), _stream(stream)))
+
+
+def gear_commit(t: int, shard: int, n: int, idx, prio, stream=None):
+    prio = np.ascontiguousarray(prio, dtype=np.float64) if not hasattr(prio, "data_ptr") else prio
+    _check("gear_commit", load().gear_commit(t, shard, n, _ptr(idx), _ptr(prio), _stream(stream)))
+
+
+def gear_column_base(t: int, col: int) -> int:
+    out = ctypes.c_void_p()
+    _check("gear_column_base", load().gear_column_base(t, col, ctypes.byref(out)))
+    return out.value or 0
+
+
 def gear_update_priorities(t: int, n: int, idx, prio, prio_dtype: int, gen=None, stream=None):
     _check("gear_update_priorities",
            load().gear_update_priorities(t, n, _ptr(idx), _ptr(prio), prio_dtype, _ptr(gen),
@@ -331,6 +350,15 @@ class Table:
 
     def insert(self, shard, col_src, prio, out_idx=None, stream=None):
         gear_insert(self.handle, shard, len(prio), col_src, prio, out_idx, stream)
+
+    def allocate(self, shard, n, out_idx, stream=None):
+        gear_allocate(self.handle, shard, n, out_idx, stream)
+
+    def commit(self, shard, idx, prio, stream=None):
+        gear_commit(self.handle, shard, len(idx), idx, prio, stream)
+
+    def column_base(self, col):
+        return gear_column_base(self.handle, col)
 
     def update_priorities(self, idx, prio, gen=None, stream=None):
         dt = GEAR_F64 if str(getattr(prio, "dtype", "")).endswith("float64") else GEAR_F32

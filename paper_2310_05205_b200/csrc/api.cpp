@@ -169,8 +169,8 @@ void destroy_table(gear_table* t) {
   dfree(t->n_stale); dfree(t->err); dfree(t->d_epoch); dfree(t->d_seed); dfree(t->d_xep);
   dfree(t->col_idx.p);
   dfree(t->d_meta); dfree(t->d_ord); dfree(t->d_out); dfree(t->d_rows);
-  if (t->h_meta) cudaFreeHost(t->h_meta);
-  if (t->h_ord) cudaFreeHost(t->h_ord);
+  dfree(t->d_prio_ins); dfree(t->d_alloc);
+  if (t->h_prio) cudaFreeHost(t->h_prio);
   if (t->h_out) cudaFreeHost(t->h_out);
   if (t->staging_ev) cudaEventDestroy(t->staging_ev);
   delete t;
@@ -438,17 +438,22 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_TRY(dalloc(&t->err, 1));
   GEAR_CUDA(cudaMemset(t->n_stale, 0, 8));
   GEAR_CUDA(cudaMemset(t->err, 0, 4));
-  GEAR_CUDA(cudaHostAlloc((void**)&t->h_meta, MB * sizeof(InsMeta), cudaHostAllocDefault));
-  GEAR_CUDA(cudaHostAlloc((void**)&t->h_ord, MB * sizeof(OrdRec), cudaHostAllocDefault));
+  GEAR_CUDA(cudaHostAlloc((void**)&t->h_prio, MB * sizeof(double), cudaHostAllocDefault));
   GEAR_CUDA(cudaHostAlloc((void**)&t->h_out, MB * sizeof(uint64_t), cudaHostAllocDefault));
+  GEAR_TRY(dalloc(&t->d_prio_ins, MB));
+  GEAR_TRY(dalloc(&t->d_alloc, t->R));
+  {
+    std::vector<AllocState> a0(t->R);
+    for (auto& a : a0) a = AllocState{0, 1, 0, 0};  // free queue full, seq counter at 1
+    GEAR_CUDA(cudaMemcpy(t->d_alloc, a0.data(), t->R * sizeof(AllocState),
+                         cudaMemcpyHostToDevice));
+  }
   GEAR_TRY(dalloc(&t->d_meta, MB));
   GEAR_TRY(dalloc(&t->d_ord, MB));
   GEAR_TRY(dalloc(&t->d_out, MB));
   GEAR_CUDA(cudaEventCreateWithFlags(&t->staging_ev, cudaEventDisableTiming));
   GEAR_CUDA(cudaEventRecord(t->staging_ev, 0));
 
-  t->rings.resize(t->R);
-  for (auto& r : t->rings) r.ord.assign(t->Cs, 0);
   GEAR_CUDA(cudaDeviceSynchronize());
   return GEAR_OK;
 }
@@ -587,7 +592,6 @@ gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* c
       return set_error(GEAR_ERR_BAD_PRIORITY, "prio[%u] = %g is not a finite non-negative number", k, p[k]);
 
   const uint32_t ls = shard % t->R;
-  ShardRing& ring = t->rings[ls];
   uint64_t row_total = 0;
   for (auto& c : t->cols) row_total += c.rb;
   // Rows per chunk: bounded by the staging arrays and by 256 MB of row data.
@@ -596,52 +600,18 @@ gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* c
   std::vector<MemKind> kinds(t->cols.size());
   for (size_t c = 0; c < t->cols.size(); ++c) kinds[c] = mem_kind(col_src[c]);
 
-  std::unordered_map<uint32_t, uint32_t> slot_at;   // slot -> meta index
-  std::unordered_map<uint32_t, uint32_t> pos_at;    // ring position -> ord index
   for (uint32_t k0 = 0; k0 < n; k0 += chunk_rows) {
     const uint32_t m = std::min(chunk_rows, n - k0);
     GEAR_CUDA(cudaEventSynchronize(t->staging_ev));  // staging buffers free again
-    slot_at.clear();
-    pos_at.clear();
-    uint32_t n_meta = 0, n_ord = 0;
-    for (uint32_t k = 0; k < m; ++k) {
-      uint32_t slot;
-      if (ring.next_free < t->Cs) {
-        slot = (uint32_t)ring.next_free++;
-      } else if (t->removal == GEAR_REMOVE_FIFO) {  // evict the oldest: ring front
-        slot = ring.ord[ring.head];
-        ring.head = (uint32_t)((ring.head + 1) % t->Cs);
-        ring.len -= 1;
-      } else {  // evict the newest: ring back
-        slot = ring.ord[(ring.head + ring.len - 1) % t->Cs];
-        ring.len -= 1;
-      }
-      const uint32_t pos = (uint32_t)((ring.head + ring.len) % t->Cs);
-      ring.ord[pos] = slot;
-      ring.len += 1;
-      auto it = pos_at.find(pos);
-      if (it == pos_at.end()) {
-        pos_at[pos] = n_ord;
-        t->h_ord[n_ord++] = OrdRec{(uint32_t)(ls * t->Cs + pos), slot};
-      } else {
-        t->h_ord[it->second].slot = slot;
-      }
-      const uint64_t seqv = ring.seq_ctr++;
-      auto jt = slot_at.find(slot);
-      if (jt == slot_at.end()) {
-        slot_at[slot] = n_meta;
-        t->h_meta[n_meta++] = InsMeta{ls * t->Cs + slot, seqv, 1u, k, p[k0 + k]};
-      } else {
-        InsMeta& im = t->h_meta[jt->second];
-        im.seq = seqv;
-        im.gen_inc += 1;
-        im.src_row = k;
-        im.prio = p[k0 + k];
-      }
-      t->h_out[k] = (uint64_t)shard * t->Cs + slot;
-    }
-    GEAR_CUDA(cudaMemcpyAsync(t->d_meta, t->h_meta, n_meta * sizeof(InsMeta), cudaMemcpyHostToDevice, s));
-    GEAR_CUDA(cudaMemcpyAsync(t->d_ord, t->h_ord, n_ord * sizeof(OrdRec), cudaMemcpyHostToDevice, s));
+    // The allocator runs on the device (kernels/alloc.cu): slots, ring
+    // positions, seq and generation counts of the m rows in one launch.
+    std::memcpy(t->h_prio, p.data() + k0, m * sizeof(double));
+    GEAR_CUDA(cudaMemcpyAsync(t->d_prio_ins, t->h_prio, m * sizeof(double),
+                              cudaMemcpyHostToDevice, s));
+    GEAR_CUDA(launch_insert_plan(t->d_alloc, ls, shard, t->Cs, t->removal == GEAR_REMOVE_LIFO, m,
+                                 t->d_prio_ins, t->ord, t->d_meta, t->d_ord, t->d_out, t->err,
+                                 s));
+    const uint32_t n_meta = m, n_ord = m;  // rows a later row overrides are skipped
     // Row sources: device / pinned host are read in place; pageable host is
     // staged into device memory first.
     ScatterParams sp{};
@@ -685,8 +655,10 @@ gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* c
                                  tile_dirty(t), t->seq, t->gen, t->ord, s));
     if (out_idx) {
       if (mem_kind(out_idx) == MemKind::Device) {
-        GEAR_CUDA(cudaMemcpyAsync(out_idx + k0, t->h_out, m * 8, cudaMemcpyHostToDevice, s));
-      } else {
+        GEAR_CUDA(cudaMemcpyAsync(out_idx + k0, t->d_out, m * 8, cudaMemcpyDeviceToDevice, s));
+      } else {  // a host id list: the ids are known once the plan ran
+        GEAR_CUDA(cudaMemcpyAsync(t->h_out, t->d_out, m * 8, cudaMemcpyDeviceToHost, s));
+        GEAR_CUDA(cudaStreamSynchronize(s));
         std::memcpy(out_idx + k0, t->h_out, m * 8);
       }
     }
@@ -737,7 +709,7 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
   if (t->W == 1 && fused) {
     // one launch: quantise, tag, block barrier, apply
     GEAR_CUDA(launch_update_fused(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, nullptr, n, t->N,
-                                  qz, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
+                                  qz, local_begin, t->Clocal, t->gen, t->seq, t->tag, t->d_epoch,
                                   t->n_stale, t->err, t->key, tile_dirty(t), s));
   } else if (t->W > 1 && fused && t->peer_xchg) {
     // one launch: quantise, push records to every peer over NVLink, wait for
@@ -745,7 +717,7 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
     Mbox mb = t->mb;
     mb.epoch_dev = t->d_xep + 1;  // update-exchange epoch (advanced by the kernel)
     GEAR_CUDA(launch_update_xchg(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N, qz,
-                                 mb, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
+                                 mb, local_begin, t->Clocal, t->gen, t->seq, t->tag, t->d_epoch,
                                  t->n_stale, t->err, t->key, tile_dirty(t), s));
   } else {
     GEAR_CUDA(launch_update_quantize(d_idx, d_prio, prio_dtype == GEAR_F64, d_gen, n, t->N,
@@ -759,12 +731,12 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
     }
     if (fused) {
       GEAR_CUDA(launch_update_fused(nullptr, nullptr, 0, nullptr, recs, m, t->N, qz,
-                                    local_begin, t->Clocal, t->gen, t->tag, t->d_epoch, t->n_stale,
+                                    local_begin, t->Clocal, t->gen, t->seq, t->tag, t->d_epoch, t->n_stale,
                                     t->err, t->key, tile_dirty(t), s));
     } else {
-      GEAR_CUDA(launch_update_tag(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
+      GEAR_CUDA(launch_update_tag(recs, m, local_begin, t->Clocal, t->gen, t->seq, t->tag, t->d_epoch,
                                   t->n_stale, t->err, s));
-      GEAR_CUDA(launch_update_apply(recs, m, local_begin, t->Clocal, t->gen, t->tag, t->d_epoch,
+      GEAR_CUDA(launch_update_apply(recs, m, local_begin, t->Clocal, t->gen, t->seq, t->tag, t->d_epoch,
                                     t->key, tile_dirty(t), s));
     }
   }
@@ -806,11 +778,6 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     const bool topk = strategy == GEAR_TOPK;
     if (topk && K > topk_max_k())
       return set_error(GEAR_ERR_UNSUPPORTED, "TopK needs W*B <= %u (got %u)", topk_max_k(), K);
-    FifoRings rings{};
-    for (uint32_t ls = 0; ls < t->R; ++ls) {
-      rings.head[ls] = t->rings[ls].head;
-      rings.len[ls] = t->rings[ls].len;
-    }
     const int lifo = topk ? 2 : (strategy == GEAR_LIFO ? 1 : 0);  // merge order
     const bool xchg = t->W > 1 && t->peer_xchg;
     Mbox mb = t->mb;
@@ -824,7 +791,7 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
                                   t->fifo_totals_local, t->topk_state, t->topk_cnt,
                                   xchg ? &mb : nullptr, s));
     else
-      GEAR_CUDA(launch_fifo_local(t->key, t->seq, t->ord, rings, t->Cs, t->R, t->rank * t->R, K,
+      GEAR_CUDA(launch_fifo_local(t->key, t->seq, t->ord, t->d_alloc, t->Cs, t->R, t->rank * t->R, K,
                                   lifo, t->cand_local, t->fifo_totals_local, xchg ? &mb : nullptr,
                                   s));
     const Cand* cand_all = t->cand_all;
@@ -932,6 +899,60 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
   if (h_w) GEAR_CUDA(cudaMemcpyAsync(out_w, d_w, B * 4ull, cudaMemcpyDeviceToHost, s));
   if (h_p) GEAR_CUDA(cudaMemcpyAsync(out_p, d_p, B * 8ull, cudaMemcpyDeviceToHost, s));
   if (h_gen) GEAR_CUDA(cudaMemcpyAsync(out_gen, d_gen, B * 4ull, cudaMemcpyDeviceToHost, s));
+  return GEAR_OK;
+}
+
+gear_status gear_allocate(gear_table* t, uint32_t shard, uint32_t n, uint64_t* out_idx,
+                          gear_stream stream) {
+  clear_error();
+  GEAR_TRY(check_table(t));
+  GEAR_CUDA(cudaSetDevice(t->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (shard / t->R != t->rank || shard >= t->S)
+    return set_error(GEAR_ERR_INVALID_ARG, "shard %u is not owned by rank %u", shard, t->rank);
+  if (n > t->max_batch) return set_error(GEAR_ERR_INVALID_ARG, "n %u > max_batch %u", n, t->max_batch);
+  if (n == 0) return GEAR_OK;
+  if (out_idx == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "out_idx is NULL");
+  const bool host_out = mem_kind(out_idx) != MemKind::Device;
+  uint64_t* d_out = host_out ? t->d_out : out_idx;
+  GEAR_CUDA(launch_allocate(t->d_alloc, shard % t->R, shard, t->Cs,
+                            t->removal == GEAR_REMOVE_LIFO, n, t->ord, t->key, t->seq, t->gen,
+                            tile_dirty(t), d_out, t->err, s));
+  if (host_out) {
+    GEAR_CUDA(cudaMemcpyAsync(out_idx, d_out, n * 8ull, cudaMemcpyDeviceToHost, s));
+    GEAR_CUDA(cudaStreamSynchronize(s));
+  }
+  t->dirty = true;
+  return GEAR_OK;
+}
+
+gear_status gear_commit(gear_table* t, uint32_t shard, uint32_t n, const uint64_t* idx,
+                        const double* prio, gear_stream stream) {
+  clear_error();
+  GEAR_TRY(check_table(t));
+  GEAR_CUDA(cudaSetDevice(t->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (shard / t->R != t->rank || shard >= t->S)
+    return set_error(GEAR_ERR_INVALID_ARG, "shard %u is not owned by rank %u", shard, t->rank);
+  if (n > t->max_batch) return set_error(GEAR_ERR_INVALID_ARG, "n %u > max_batch %u", n, t->max_batch);
+  if (n == 0) return GEAR_OK;
+  if (idx == nullptr || prio == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "idx / prio is NULL");
+  const uint64_t* d_idx = nullptr;
+  const double* d_prio = nullptr;
+  GEAR_TRY(stage_in(idx, n, t->upd_idx, s, &d_idx));
+  GEAR_TRY(stage_in(prio, n, t->upd_prio, s, &d_prio));
+  GEAR_CUDA(launch_commit(t->d_alloc, shard % t->R, shard, t->Cs, n, d_idx, d_prio, quant(t),
+                          t->key, t->seq, t->gen, t->ord, t->tag, t->d_epoch, tile_dirty(t),
+                          t->err, s));
+  t->dirty = true;
+  return GEAR_OK;
+}
+
+gear_status gear_column_base(const gear_table* t, uint32_t col, void** out) {
+  clear_error();
+  if (t == nullptr || out == nullptr || col >= t->cols.size())
+    return set_error(GEAR_ERR_INVALID_ARG, "bad table, column %u or NULL output", col);
+  *out = t->cols[col].local;
   return GEAR_OK;
 }
 

@@ -108,10 +108,16 @@ gear_status gear_table_save(gear_table* t, const char* path) {
   GEAR_TRY(dev_to_file(file.f, t->key, t->Clocal * 8, stage.p));
   GEAR_TRY(dev_to_file(file.f, t->seq, t->Clocal * 8, stage.p));
   GEAR_TRY(dev_to_file(file.f, t->gen, t->Clocal * 4, stage.p));
-  for (const ShardRing& r : t->rings) {
-    const uint64_t st[4] = {r.next_free, r.head, r.len, r.seq_ctr};
+  // the device-resident allocator state and ring of every local shard
+  std::vector<AllocState> a(t->R);
+  GEAR_CUDA(cudaMemcpy(a.data(), t->d_alloc, t->R * sizeof(AllocState), cudaMemcpyDeviceToHost));
+  std::vector<uint32_t> ord(t->Cs);
+  for (uint32_t ls = 0; ls < t->R; ++ls) {
+    const uint64_t st[4] = {a[ls].next_free, a[ls].head, a[ls].len, a[ls].seq_ctr};
     GEAR_TRY(wr(file.f, st, sizeof(st)));
-    GEAR_TRY(wr(file.f, r.ord.data(), r.ord.size() * 4));
+    GEAR_CUDA(cudaMemcpy(ord.data(), t->ord + (uint64_t)ls * t->Cs, t->Cs * 4,
+                         cudaMemcpyDeviceToHost));
+    GEAR_TRY(wr(file.f, ord.data(), t->Cs * 4));
   }
   for (const ColumnState& c : t->cols) {
     if (c.placement == GEAR_DEVICE) GEAR_TRY(dev_to_file(file.f, c.local, c.bytes_local, stage.p));
@@ -143,19 +149,20 @@ gear_status gear_table_load(gear_table* t, const char* path) {
   GEAR_TRY(file_to_dev(file.f, t->key, t->Clocal * 8, stage.p));
   GEAR_TRY(file_to_dev(file.f, t->seq, t->Clocal * 8, stage.p));
   GEAR_TRY(file_to_dev(file.f, t->gen, t->Clocal * 4, stage.p));
-  for (ShardRing& r : t->rings) {
+  std::vector<AllocState> a(t->R);
+  std::vector<uint32_t> ord(t->Cs);
+  for (uint32_t ls = 0; ls < t->R; ++ls) {
     uint64_t st[4];
     GEAR_TRY(rd(file.f, st, sizeof(st)));
-    r.next_free = st[0];
-    r.head = (uint32_t)st[1];
-    r.len = (uint32_t)st[2];
-    r.seq_ctr = st[3];
-    GEAR_TRY(rd(file.f, r.ord.data(), r.ord.size() * 4));
-  }
-  // the device copy of the rings
-  for (uint32_t ls = 0; ls < t->R; ++ls)
-    GEAR_CUDA(cudaMemcpy(t->ord + (uint64_t)ls * t->Cs, t->rings[ls].ord.data(), t->Cs * 4,
+    a[ls].next_free = st[0];
+    a[ls].head = (uint32_t)st[1];
+    a[ls].len = (uint32_t)st[2];
+    a[ls].seq_ctr = st[3];
+    GEAR_TRY(rd(file.f, ord.data(), t->Cs * 4));
+    GEAR_CUDA(cudaMemcpy(t->ord + (uint64_t)ls * t->Cs, ord.data(), t->Cs * 4,
                          cudaMemcpyHostToDevice));
+  }
+  GEAR_CUDA(cudaMemcpy(t->d_alloc, a.data(), t->R * sizeof(AllocState), cudaMemcpyHostToDevice));
   for (ColumnState& c : t->cols) {
     if (c.placement == GEAR_DEVICE) GEAR_TRY(file_to_dev(file.f, c.local, c.bytes_local, stage.p));
     else GEAR_TRY(rd(file.f, c.local, c.bytes_local));

@@ -21,6 +21,7 @@ constexpr uint32_t kErrStale = 4u;
 constexpr uint32_t kErrEmpty = 8u;
 
 constexpr uint32_t kErrTimeout = 16u;
+constexpr uint32_t kErrFull = 32u;
 
 // Strategy codes (mirror gear_strategy).
 constexpr int kFifo = 0, kLifo = 1, kUniform = 2, kWeighted = 3, kPrioritized = 4;
@@ -63,9 +64,19 @@ struct UpdRec {
   uint32_t flags;  // bit0 valid, bit1 has generation
 };
 
-// One slot written by gear_insert (after host-side de-duplication).
+// Device-resident block allocator state of one local shard (kernels/alloc.cu):
+// free slots are [next_free, C_s); committed slots sit in commit order in the
+// ring ord[shard_local*C_s + (head + i) % C_s], i < len.
+struct AllocState {
+  uint64_t next_free;
+  uint64_t seq_ctr;  // next seq (starts at 1; 0 = never committed / ongoing)
+  uint32_t head;
+  uint32_t len;
+};
+
+// One row written by gear_insert (planned on the device, kernels/alloc.cu).
 struct InsMeta {
-  uint64_t local;    // rank-local slot (shard_local * C_s + i)
+  uint64_t local;    // rank-local slot (shard_local * C_s + i); kIdxNone: a later row wins
   uint64_t seq;      // new seq value
   uint32_t gen_inc;  // how many inserts landed in the slot in this call
   uint32_t src_row;  // row of the caller's source arrays that wins the slot
@@ -73,7 +84,8 @@ struct InsMeta {
 };
 
 // One ring-order entry written by gear_insert: ord[pos] = slot (both
-// rank-local; pos indexes the rank's concatenated per-shard rings).
+// rank-local; pos indexes the rank's concatenated per-shard rings;
+// 0xffffffff: a later row owns the position).
 struct OrdRec {
   uint32_t pos;
   uint32_t slot;
@@ -286,11 +298,12 @@ cudaError_t launch_update_quantize(const uint64_t* idx, const void* prio, int pr
                                    Quant qz, UpdRec* out,
                                    uint32_t* err, cudaStream_t s);
 cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_begin,
-                              uint64_t local_rows, const uint32_t* gen, unsigned long long* tag,
+                              uint64_t local_rows, const uint32_t* gen, const uint64_t* seq, unsigned long long* tag,
                               uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err,
                               cudaStream_t s);
 cudaError_t launch_update_apply(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                                 uint64_t local_rows, const uint32_t* gen,
+                               const uint64_t* seq,
                                 const unsigned long long* tag, uint32_t* epoch_dev, uint64_t* key,
                                 TileDirty td, cudaStream_t s);
 
@@ -301,6 +314,7 @@ cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_
                                 const uint32_t* gen_in, const UpdRec* recs, uint32_t m,
                                 uint64_t n_global, Quant qz,
                                 uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
+                               const uint64_t* seq,
                                 unsigned long long* tag, uint32_t* epoch_dev,
                                 unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                 TileDirty td, cudaStream_t s);
@@ -311,6 +325,7 @@ cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_i
                                const uint32_t* gen_in, uint32_t n, uint64_t n_global,
                                Quant qz, const Mbox& mb,
                                uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
+                               const uint64_t* seq,
                                unsigned long long* tag, uint32_t* epoch_dev,
                                unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                TileDirty td, cudaStream_t s);
@@ -323,13 +338,24 @@ cudaError_t launch_insert_meta(const InsMeta* meta, uint32_t m, const OrdRec* or
                                uint64_t* key, TileDirty td, uint64_t* seq, uint32_t* gen,
                                uint32_t* ord, cudaStream_t s);
 
-// K4: FIFO/LIFO local selection and merge.
-struct FifoRings {
-  uint32_t head[kMaxShards];  // ring start of each local shard (oldest entry)
-  uint32_t len[kMaxShards];   // committed entries in the ring
-};
+// NEXT-1: device-resident allocator (kernels/alloc.cu).
+cudaError_t launch_insert_plan(AllocState* st, uint32_t ls, uint32_t shard, uint64_t Cs, int lifo,
+                               uint32_t m, const double* prio, const uint32_t* ord, InsMeta* meta,
+                               OrdRec* ord_recs, uint64_t* out_idx, uint32_t* err,
+                               cudaStream_t s);
+cudaError_t launch_allocate(AllocState* st, uint32_t ls, uint32_t shard, uint64_t Cs, int lifo,
+                            uint32_t n, const uint32_t* ord, uint64_t* key, uint64_t* seq,
+                            uint32_t* gen, TileDirty td, uint64_t* out_idx, uint32_t* err,
+                            cudaStream_t s);
+cudaError_t launch_commit(AllocState* st, uint32_t ls, uint32_t shard, uint64_t Cs, uint32_t n,
+                          const uint64_t* idx, const double* prio, Quant qz, uint64_t* key,
+                          uint64_t* seq, const uint32_t* gen, uint32_t* ord,
+                          unsigned long long* tag, uint32_t* epoch_dev, TileDirty td,
+                          uint32_t* err, cudaStream_t s);
+
+// K4: FIFO/LIFO local selection and merge (ring state read from `alloc`).
 cudaError_t launch_fifo_local(const uint64_t* key, const uint64_t* seq, const uint32_t* ord,
-                              const FifoRings& rings, uint64_t shard_cap,
+                              const AllocState* alloc, uint64_t shard_cap,
                               uint32_t n_shards_local, uint32_t first_shard, uint32_t K,
                               int lifo, Cand* cand_out, ShardTotals* totals_out,
                               const Mbox* mbox, cudaStream_t s);

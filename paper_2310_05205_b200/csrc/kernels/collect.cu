@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant
     const uint64_t j = rel / col.chunks_per_row;
     const uint64_t k = rel - j * col.chunks_per_row;
     const InsMeta m = p.meta[j];
+    if (m.local == kIdxNone) continue;  // a later row of the call owns this slot
     const uint64_t off = k * (uint64_t)p.chunk_bytes;
     const uint64_t rem = col.rb - off;
     const uint64_t bytes = rem < p.chunk_bytes ? rem : p.chunk_bytes;
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(kThreads)
                        uint64_t* key, TileDirty td, uint64_t* seq, uint32_t* gen,
                        uint32_t* ord) {
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
-  if (k < m) {
+  if (k < m && meta[k].local != kIdxNone) {
     const InsMeta r = meta[k];
     uint64_t q = 0;
     quantize(r.prio, qz, &q);  // validated on the host
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(kThreads)
     seq[r.local] = r.seq;
     gen[r.local] += r.gen_inc;
   }
-  if (k < n_ord) ord[ord_recs[k].pos] = ord_recs[k].slot;
+  if (k < n_ord && ord_recs[k].pos != 0xffffffffu) ord[ord_recs[k].pos] = ord_recs[k].slot;
 }
 
 // Persistent grid: as many CTAs as can be resident at once (no second wave

@@ -3,7 +3,8 @@
 // "all servers can perform a local scan to generate k samples before the
 // global gathering operation, which can significantly reduce the
 // communication overhead from O(n) to O(mk)".  Each shard keeps its committed
-// slots in insertion order in a ring (`ord`, maintained by gear_insert), so
+// slots in commit order in a ring (`ord`, maintained by the device-side
+// allocator, kernels/alloc.cu), so
 // seq is increasing along the ring.  Local step: one CTA per local shard
 // walks the ring from the oldest (FIFO) or newest (LIFO) end and compacts the
 // first K = W*B selectable slots (key > 0) with a block-wide ballot scan,
@@ -23,7 +24,7 @@ constexpr int kMergeThreads = 256;
 
 __global__ void __launch_bounds__(kLocalThreads)
     fifo_local_kernel(const uint64_t* __restrict__ key, const uint64_t* __restrict__ seq,
-                      const uint32_t* __restrict__ ord, const __grid_constant__ FifoRings rings,
+                      const uint32_t* __restrict__ ord, const AllocState* __restrict__ alloc,
                       uint64_t shard_cap, uint32_t first_shard, uint32_t K, int lifo,
                       Cand* __restrict__ cand_out, ShardTotals* __restrict__ totals_out,
                       const __grid_constant__ Mbox m0, int xchg) {
@@ -33,7 +34,7 @@ __global__ void __launch_bounds__(kLocalThreads)
   const uint32_t ls = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t base = (uint64_t)ls * shard_cap;
-  const uint32_t head = rings.head[ls], len = rings.len[ls];
+  const uint32_t head = alloc[ls].head, len = alloc[ls].len;
   Cand* out = cand_out + (uint64_t)ls * K;
   if (tid == 0) s_count = 0;
   __syncthreads();
@@ -185,13 +186,13 @@ __global__ void __launch_bounds__(kMergeThreads)
 }  // namespace
 
 cudaError_t launch_fifo_local(const uint64_t* key, const uint64_t* seq, const uint32_t* ord,
-                              const FifoRings& rings, uint64_t shard_cap,
+                              const AllocState* alloc, uint64_t shard_cap,
                               uint32_t n_shards_local, uint32_t first_shard, uint32_t K,
                               int lifo, Cand* cand_out, ShardTotals* totals_out,
                               const Mbox* mbox, cudaStream_t s) {
   count_launch();
   fifo_local_kernel<<<n_shards_local, kLocalThreads, 0, s>>>(
-      key, seq, ord, rings, shard_cap, first_shard, K, lifo, cand_out, totals_out,
+      key, seq, ord, alloc, shard_cap, first_shard, K, lifo, cand_out, totals_out,
       mbox ? *mbox : Mbox{}, mbox != nullptr);
   return cudaGetLastError();
 }

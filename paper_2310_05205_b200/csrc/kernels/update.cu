@@ -48,17 +48,19 @@ __global__ void __launch_bounds__(kThreads)
   out[k] = r;
 }
 
-// Entry k is applied by the rank owning its id, if the slot has been inserted
-// (gen != 0) and the optional generation matches.
+// Entry k is applied by the rank owning its id, if the slot holds a committed
+// trajectory (gen != 0, seq != 0) and the optional generation matches.
 __device__ __forceinline__ bool owned_and_fresh(const UpdRec& r, uint64_t local_begin,
                                                 uint64_t local_rows, const uint32_t* gen,
+                                                const uint64_t* seq,
                                                 uint64_t* local, bool* stale) {
   *stale = false;
   if (!(r.flags & 1u)) return false;
   if (r.idx < local_begin || r.idx >= local_begin + local_rows) return false;
   *local = r.idx - local_begin;
   const uint32_t gcur = gen[*local];
-  if (gcur == 0 || ((r.flags & 2u) && r.gen != gcur)) {
+  // never inserted (gen 0) or allocated and not yet committed (seq 0, Q21)
+  if (gcur == 0 || seq[*local] == 0 || ((r.flags & 2u) && r.gen != gcur)) {
     *stale = true;
     return false;
   }
@@ -67,7 +69,8 @@ __device__ __forceinline__ bool owned_and_fresh(const UpdRec& r, uint64_t local_
 
 __global__ void __launch_bounds__(kThreads)
     tag_kernel(const UpdRec* __restrict__ recs, uint32_t m, uint64_t local_begin,
-               uint64_t local_rows, const uint32_t* __restrict__ gen, unsigned long long* tag,
+               uint64_t local_rows, const uint32_t* __restrict__ gen,
+                 const uint64_t* __restrict__ seq, unsigned long long* tag,
                uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err) {
   const uint32_t epoch = *epoch_dev + 1;
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
@@ -75,7 +78,7 @@ __global__ void __launch_bounds__(kThreads)
   const UpdRec r = recs[k];
   uint64_t local;
   bool stale;
-  if (owned_and_fresh(r, local_begin, local_rows, gen, &local, &stale)) {
+  if (owned_and_fresh(r, local_begin, local_rows, gen, seq, &local, &stale)) {
     atomicMax(tag + local, ((unsigned long long)epoch << 32) | (unsigned long long)(k + 1));
   } else if (stale) {
     atomicAdd(n_stale, 1ull);
@@ -86,6 +89,7 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     apply_kernel(const UpdRec* __restrict__ recs, uint32_t m, uint64_t local_begin,
                  uint64_t local_rows, const uint32_t* __restrict__ gen,
+                 const uint64_t* __restrict__ seq,
                  const unsigned long long* __restrict__ tag, const uint32_t* epoch_dev,
                  uint64_t* key, TileDirty td) {
   const uint32_t epoch = *epoch_dev + 1;
@@ -94,7 +98,7 @@ __global__ void __launch_bounds__(kThreads)
   const UpdRec r = recs[k];
   uint64_t local;
   bool stale;
-  if (owned_and_fresh(r, local_begin, local_rows, gen, &local, &stale) &&
+  if (owned_and_fresh(r, local_begin, local_rows, gen, seq, &local, &stale) &&
       tag[local] == (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1))) {
     key[local] = r.q;
     mark_tile(td, local);
@@ -113,7 +117,8 @@ __global__ void __launch_bounds__(kFusedThreads)
     fused_kernel(const uint64_t* __restrict__ idx, const void* __restrict__ prio, int prio_is_f64,
                  const uint32_t* __restrict__ gen_in, const UpdRec* __restrict__ recs, uint32_t m,
                  uint64_t n_global, Quant qz, uint64_t local_begin,
-                 uint64_t local_rows, const uint32_t* __restrict__ gen, unsigned long long* tag,
+                 uint64_t local_rows, const uint32_t* __restrict__ gen,
+                 const uint64_t* __restrict__ seq, unsigned long long* tag,
                  uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                  TileDirty td) {
   const uint32_t epoch = *epoch_dev + 1;  // device-resident: graph-replayable
@@ -144,7 +149,7 @@ __global__ void __launch_bounds__(kFusedThreads)
       r[u] = recs[k];
     }
     bool st;
-    mine[u] = owned_and_fresh(r[u], local_begin, local_rows, gen, &loc[u], &st);
+    mine[u] = owned_and_fresh(r[u], local_begin, local_rows, gen, seq, &loc[u], &st);
     stale += st ? 1u : 0u;
     if (mine[u])
       atomicMax(tag + loc[u], ((unsigned long long)epoch << 32) | (unsigned long long)(k + 1));
@@ -178,6 +183,7 @@ __global__ void __launch_bounds__(kFusedThreads)
                 const uint32_t* __restrict__ gen_in, uint32_t n, uint64_t n_global,
                 Quant qz, const __grid_constant__ Mbox mb0,
                 uint64_t local_begin, uint64_t local_rows, const uint32_t* __restrict__ gen,
+                 const uint64_t* __restrict__ seq,
                 unsigned long long* tag, uint32_t* epoch_dev, unsigned long long* n_stale,
                 uint32_t* err, uint64_t* key, TileDirty td) {
   const uint32_t epoch = *epoch_dev + 1;  // device-resident tag epoch
@@ -230,7 +236,7 @@ __global__ void __launch_bounds__(kFusedThreads)
     r[u].gen = __ldcg(&rp->gen);
     r[u].flags = __ldcg(&rp->flags);
     bool st;
-    mine[u] = owned_and_fresh(r[u], local_begin, local_rows, gen, &loc[u], &st);
+    mine[u] = owned_and_fresh(r[u], local_begin, local_rows, gen, seq, &loc[u], &st);
     stale += st ? 1u : 0u;
     if (mine[u])
       atomicMax(tag + loc[u], ((unsigned long long)epoch << 32) | (unsigned long long)(k + 1));
@@ -267,12 +273,13 @@ cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_i
                                const uint32_t* gen_in, uint32_t n, uint64_t n_global,
                                Quant qz, const Mbox& mb,
                                uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
+                               const uint64_t* seq,
                                unsigned long long* tag, uint32_t* epoch_dev,
                                unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                TileDirty td, cudaStream_t s) {
   count_launch();
   xchg_kernel<<<1, kFusedThreads, 0, s>>>(idx, prio, prio_is_f64, gen_in, n, n_global, qz, mb,
-                                          local_begin, local_rows, gen, tag, epoch_dev,
+                                          local_begin, local_rows, gen, seq, tag, epoch_dev,
                                           n_stale, err, key, td);
   return cudaGetLastError();
 }
@@ -281,13 +288,14 @@ cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_
                                 const uint32_t* gen_in, const UpdRec* recs, uint32_t m,
                                 uint64_t n_global, Quant qz,
                                 uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
+                                const uint64_t* seq,
                                 unsigned long long* tag, uint32_t* epoch_dev,
                                 unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                 TileDirty td, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   count_launch();
   fused_kernel<<<1, kFusedThreads, 0, s>>>(idx, prio, prio_is_f64, gen_in, recs, m, n_global,
-                                           qz, local_begin, local_rows, gen, tag,
+                                           qz, local_begin, local_rows, gen, seq, tag,
                                            epoch_dev, n_stale, err, key, td);
   return cudaGetLastError();
 }
@@ -325,25 +333,26 @@ cudaError_t launch_update_quantize(const uint64_t* idx, const void* prio, int pr
 }
 
 cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_begin,
-                              uint64_t local_rows, const uint32_t* gen, unsigned long long* tag,
+                              uint64_t local_rows, const uint32_t* gen, const uint64_t* seq, unsigned long long* tag,
                               uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err,
                               cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   count_launch();
   tag_kernel<<<(m + kThreads - 1) / kThreads, kThreads, 0, s>>>(
-      recs, m, local_begin, local_rows, gen, tag, epoch_dev, n_stale, err);
+      recs, m, local_begin, local_rows, gen, seq, tag, epoch_dev, n_stale, err);
   return cudaGetLastError();
 }
 
 cudaError_t launch_update_apply(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                                 uint64_t local_rows, const uint32_t* gen,
+                                const uint64_t* seq,
                                 const unsigned long long* tag, uint32_t* epoch_dev, uint64_t* key,
                                 TileDirty td, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   count_launch(2);
   apply_kernel<<<(m + kThreads - 1) / kThreads, kThreads, 0, s>>>(recs, m, local_begin,
-                                                                  local_rows, gen, tag, epoch_dev,
-                                                                  key, td);
+                                                                  local_rows, gen, seq, tag,
+                                                                  epoch_dev, key, td);
   epoch_bump_kernel<<<1, 1, 0, s>>>(epoch_dev);  // after every apply block read it
   return cudaGetLastError();
 }

@@ -68,14 +68,6 @@ struct ColumnState {
   std::string shm_name;                 // own shm object (W > 1 HOST columns)
 };
 
-struct ShardRing {
-  uint64_t next_free = 0;  // free queue seeded 0..C_s-1 ascending (cursor)
-  uint32_t head = 0;       // ring start: oldest committed slot
-  uint32_t len = 0;        // committed slots in the ring
-  uint64_t seq_ctr = 1;    // next seq value
-  std::vector<uint32_t> ord;  // host mirror of the ring (slot ids)
-};
-
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -167,10 +159,10 @@ struct gear_table {
   // collect scratch (host-resident id lists)
   gear::DevBuf<uint64_t> col_idx;
 
-  // insert staging
-  std::vector<gear::ShardRing> rings;
-  gear::InsMeta* h_meta = nullptr;  // pinned
-  gear::OrdRec* h_ord = nullptr;    // pinned
+  // block allocator (device-resident, kernels/alloc.cu) and insert staging
+  gear::AllocState* d_alloc = nullptr;  // [R]
+  double* h_prio = nullptr;         // pinned [max_batch]
+  double* d_prio_ins = nullptr;     // [max_batch]
   uint64_t* h_out = nullptr;        // pinned
   gear::InsMeta* d_meta = nullptr;
   gear::OrdRec* d_ord = nullptr;

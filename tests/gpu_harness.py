@@ -2,6 +2,8 @@
 fed the same seeded inputs (synth/), plus host mirrors of the columns."""
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 import oracle
@@ -12,6 +14,14 @@ DT = {"u8": gear.GEAR_U8, "i32": gear.GEAR_I32, "f32": gear.GEAR_F32}
 ORACLE_STRATEGY = {gear.GEAR_FIFO: oracle.FIFO, gear.GEAR_LIFO: oracle.LIFO,
                    gear.GEAR_UNIFORM: oracle.UNIFORM, gear.GEAR_WEIGHTED: oracle.WEIGHTED,
                    gear.GEAR_PRIORITIZED: oracle.PRIORITIZED, gear.GEAR_TOPK: oracle.TOPK}
+
+
+def oracle_bits_to_gear(st):
+    """GOR_* status bits -> GEAR_DEVERR_* bits."""
+    m = {oracle.BAD_PRIORITY: gear.GEAR_DEVERR_BAD_PRIORITY,
+         oracle.INDEX_RANGE: gear.GEAR_DEVERR_INDEX_RANGE, oracle.STALE: gear.GEAR_DEVERR_STALE,
+         oracle.EMPTY: gear.GEAR_DEVERR_EMPTY, oracle.FULL: gear.GEAR_DEVERR_FULL}
+    return sum(g for o, g in m.items() if st & o)
 
 
 class Pair:
@@ -119,6 +129,62 @@ class Pair:
         ost, ons = self.o.update(idx, p.astype(np.float64), gen)
         err, ns = self.t.sync()
         return ost, ons, err, ns
+
+    # --- split writer API (gear_allocate / in-place rows / gear_commit) -------
+    def allocate(self, shard, n):
+        torch = self.torch
+        out = torch.empty(n, dtype=torch.int64, device="cuda")
+        self.t.allocate(shard, n, out)
+        torch.cuda.synchronize()
+        gids = out.cpu().numpy().view(np.uint64)
+        st, oids = self.o.allocate(shard, n)
+        err, _ = self.t.sync()
+        if st == oracle.FULL:
+            assert err & gear.GEAR_DEVERR_FULL, err
+            assert np.all(gids == np.uint64(gear.GEAR_IDX_NONE))
+            return None
+        assert st == 0 and err == 0, (st, err)
+        assert np.array_equal(gids, oids), "allocated slots differ from the oracle"
+        return gids
+
+    def write_rows(self, ids):
+        """Write new trajectories' rows IN PLACE at the allocated slots
+        (gear_column_base), device columns with a device scatter, host
+        columns through the mapped host pointer."""
+        torch = self.torch
+        ids = np.asarray(ids, np.uint64)
+        traj = np.arange(self.next_traj, self.next_traj + ids.size)
+        self.next_traj += ids.size
+        for c, rb in enumerate(self.rb):
+            rows = synth.row_bytes_of(c, traj, rb)
+            base = self.t.column_base(c)
+            if self.cols[c].placement == gear.GEAR_DEVICE:
+                class _View:
+                    __cuda_array_interface__ = {"shape": (self.N, rb), "typestr": "|u1",
+                                                "data": (base, False), "version": 3}
+                col = torch.as_tensor(_View(), device="cuda")
+                col[torch.from_numpy(ids.astype(np.int64)).cuda()] = torch.from_numpy(rows).cuda()
+            else:
+                col = np.ctypeslib.as_array(ctypes.cast(base, ctypes.POINTER(ctypes.c_uint8)),
+                                            shape=(self.N, rb))
+                col[ids.astype(np.int64)] = rows
+            if self.mirror is not None:
+                self.mirror[c][ids.astype(np.int64)] = rows
+        torch.cuda.synchronize()
+        for k, g in enumerate(ids):
+            self.content[int(g)] = traj[k]
+
+    def commit(self, shard, ids, prio):
+        torch = self.torch
+        ids = np.asarray(ids, np.uint64)
+        prio = np.asarray(prio, np.float64)
+        self.t.commit(shard, torch.from_numpy(ids.view(np.int64)).cuda(),
+                      torch.from_numpy(prio).cuda())
+        torch.cuda.synchronize()
+        ost = self.o.commit(shard, ids, prio)
+        err, _ = self.t.sync()
+        assert err == oracle_bits_to_gear(ost), (err, ost)
+        return ost
 
     def check_state(self):
         key, seq, gen = self.t.read_state()
