@@ -356,8 +356,10 @@ gear_status gear_table_load(gear_table* t, const char* path);
  *                   rescans only the tiles whose keys changed since that CDF
  *                   buffer was last built (incremental, no look-back);
  *                   1 = one flat prefix sum per shard rebuilt whole by the
- *                   decoupled look-back scan.  The sampled ids
- *                   are identical (synchronises the device).
+ *                   decoupled look-back scan, only when the
+ *                   host saw a writer call since the last build (so writers
+ *                   replayed from a CUDA graph need cdf_levels 2).  The
+ *                   sampled ids are identical (synchronises the device).
  * Initial values also come from the environment (GEAR_COLLECT_IMPL=lsu|tma,
  * GEAR_COLLECT_CHUNK, GEAR_TMA_CHUNK).  INVALID_ARG for an unknown key or
  * value. */

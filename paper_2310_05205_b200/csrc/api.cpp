@@ -169,7 +169,7 @@ void destroy_table(gear_table* t) {
   dfree(t->n_stale); dfree(t->err); dfree(t->d_epoch); dfree(t->d_seed); dfree(t->d_xep);
   dfree(t->col_idx.p);
   dfree(t->d_meta); dfree(t->d_ord); dfree(t->d_out); dfree(t->d_rows);
-  dfree(t->d_prio_ins); dfree(t->d_alloc);
+  dfree(t->d_prio_ins); dfree(t->d_alloc); dfree(t->ins_bad);
   if (t->h_prio) cudaFreeHost(t->h_prio);
   if (t->h_out) cudaFreeHost(t->h_out);
   if (t->staging_ev) cudaEventDestroy(t->staging_ev);
@@ -442,6 +442,8 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_CUDA(cudaHostAlloc((void**)&t->h_out, MB * sizeof(uint64_t), cudaHostAllocDefault));
   GEAR_TRY(dalloc(&t->d_prio_ins, MB));
   GEAR_TRY(dalloc(&t->d_alloc, t->R));
+  GEAR_TRY(dalloc(&t->ins_bad, 1));
+  GEAR_CUDA(cudaMemset(t->ins_bad, 0, 4));
   {
     std::vector<AllocState> a0(t->R);
     for (auto& a : a0) a = AllocState{0, 1, 0, 0};  // free queue full, seq counter at 1
@@ -581,16 +583,21 @@ gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* c
     return set_error(GEAR_ERR_INVALID_ARG, "col_src / prio is NULL");
   for (size_t c = 0; c < t->cols.size(); ++c)
     if (col_src[c] == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "col_src[%zu] is NULL", c);
-  // Priorities are validated on the host before anything is inserted.
-  std::vector<double> p(n);
-  if (mem_kind(prio) == MemKind::Device)
-    GEAR_CUDA(cudaMemcpy(p.data(), prio, n * sizeof(double), cudaMemcpyDeviceToHost));
-  else
-    std::memcpy(p.data(), prio, n * sizeof(double));
-  for (uint32_t k = 0; k < n; ++k)
-    if (!(p[k] >= 0.0) || std::isinf(p[k]))
-      return set_error(GEAR_ERR_BAD_PRIORITY, "prio[%u] = %g is not a finite non-negative number", k, p[k]);
-
+  // Host priorities are validated here before anything is inserted (error
+  // returned); device priorities by a kernel (BAD_PRIORITY latched, nothing
+  // inserted), so a call with device sources and priorities never blocks the
+  // host and can be captured in a CUDA graph.
+  const bool dev_prio = mem_kind(prio) == MemKind::Device;
+  std::vector<double> p;
+  if (!dev_prio) {
+    p.assign(prio, prio + n);
+    for (uint32_t k = 0; k < n; ++k)
+      if (!(p[k] >= 0.0) || std::isinf(p[k]))
+        return set_error(GEAR_ERR_BAD_PRIORITY, "prio[%u] = %g is not a finite non-negative number",
+                         k, p[k]);
+  } else {
+    GEAR_CUDA(launch_validate_prio(prio, n, t->ins_bad, t->err, s));
+  }
   const uint32_t ls = shard % t->R;
   uint64_t row_total = 0;
   for (auto& c : t->cols) row_total += c.rb;
@@ -600,17 +607,23 @@ gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* c
   std::vector<MemKind> kinds(t->cols.size());
   for (size_t c = 0; c < t->cols.size(); ++c) kinds[c] = mem_kind(col_src[c]);
 
+  bool staging = !dev_prio;  // pinned host staging in use (reused per call)
+  for (auto k : kinds) staging = staging || k == MemKind::HostPageable;
   for (uint32_t k0 = 0; k0 < n; k0 += chunk_rows) {
     const uint32_t m = std::min(chunk_rows, n - k0);
-    GEAR_CUDA(cudaEventSynchronize(t->staging_ev));  // staging buffers free again
+    if (staging) GEAR_CUDA(cudaEventSynchronize(t->staging_ev));  // staging buffers free again
     // The allocator runs on the device (kernels/alloc.cu): slots, ring
     // positions, seq and generation counts of the m rows in one launch.
-    std::memcpy(t->h_prio, p.data() + k0, m * sizeof(double));
-    GEAR_CUDA(cudaMemcpyAsync(t->d_prio_ins, t->h_prio, m * sizeof(double),
-                              cudaMemcpyHostToDevice, s));
+    const double* d_p = prio + k0;
+    if (!dev_prio) {
+      std::memcpy(t->h_prio, p.data() + k0, m * sizeof(double));
+      GEAR_CUDA(cudaMemcpyAsync(t->d_prio_ins, t->h_prio, m * sizeof(double),
+                                cudaMemcpyHostToDevice, s));
+      d_p = t->d_prio_ins;
+    }
     GEAR_CUDA(launch_insert_plan(t->d_alloc, ls, shard, t->Cs, t->removal == GEAR_REMOVE_LIFO, m,
-                                 t->d_prio_ins, t->ord, t->d_meta, t->d_ord, t->d_out, t->err,
-                                 s));
+                                 d_p, t->ord, dev_prio ? t->ins_bad : nullptr, t->d_meta,
+                                 t->d_ord, t->d_out, t->err, s));
     const uint32_t n_meta = m, n_ord = m;  // rows a later row overrides are skipped
     // Row sources: device / pinned host are read in place; pageable host is
     // staged into device memory first.
@@ -662,7 +675,7 @@ gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* c
         std::memcpy(out_idx + k0, t->h_out, m * 8);
       }
     }
-    GEAR_CUDA(cudaEventRecord(t->staging_ev, s));
+    if (staging) GEAR_CUDA(cudaEventRecord(t->staging_ev, s));
   }
   t->dirty = true;
   return GEAR_OK;
@@ -825,7 +838,10 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     if (xchg) GEAR_CUDA(launch_epoch_bump(t->d_xep + 2, s));
   } else {
     const int mode = strategy == GEAR_UNIFORM ? 1 : 0;
-    if (t->dirty || t->cdf_mode != mode) {
+    // Two-level CDF: always launched -- it rescans only tiles the device-side
+    // dirty bits name, so writers replayed from a CUDA graph (which the host
+    // does not see) are picked up; a clean table costs one short launch.
+    if (t->cdf_levels == 2 || t->dirty || t->cdf_mode != mode) {
       // Rebuild into the buffer peers are not reading (device-resident parity).
       if (t->cdf_levels == 2)  // incremental: only tiles changed since this buffer's build
         GEAR_CUDA(launch_scan2(t->key, t->cdf[0], t->cdf[1], t->Cs, t->R, mode, t->d_xep + 3,

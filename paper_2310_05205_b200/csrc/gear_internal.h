@@ -339,10 +339,14 @@ cudaError_t launch_insert_meta(const InsMeta* meta, uint32_t m, const OrdRec* or
                                uint32_t* ord, cudaStream_t s);
 
 // NEXT-1: device-resident allocator (kernels/alloc.cu).
+// Device priorities of gear_insert: *bad = any invalid (all or nothing).
+cudaError_t launch_validate_prio(const double* prio, uint32_t n, uint32_t* bad, uint32_t* err,
+                                 cudaStream_t s);
+// abort_flag != null: plan nothing when *abort_flag (the validation failed).
 cudaError_t launch_insert_plan(AllocState* st, uint32_t ls, uint32_t shard, uint64_t Cs, int lifo,
-                               uint32_t m, const double* prio, const uint32_t* ord, InsMeta* meta,
-                               OrdRec* ord_recs, uint64_t* out_idx, uint32_t* err,
-                               cudaStream_t s);
+                               uint32_t m, const double* prio, const uint32_t* ord,
+                               const uint32_t* abort_flag, InsMeta* meta, OrdRec* ord_recs,
+                               uint64_t* out_idx, uint32_t* err, cudaStream_t s);
 cudaError_t launch_allocate(AllocState* st, uint32_t ls, uint32_t shard, uint64_t Cs, int lifo,
                             uint32_t n, const uint32_t* ord, uint64_t* key, uint64_t* seq,
                             uint32_t* gen, TileDirty td, uint64_t* out_idx, uint32_t* err,

@@ -56,21 +56,40 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* s_warp
   return before + incl - x;
 }
 
+// Device-side priority check of a whole gear_insert call (all or nothing):
+// *bad = 1 (and BAD_PRIORITY latched) if any p is NaN, infinite or negative.
+__global__ void __launch_bounds__(kThreads)
+    validate_prio_kernel(const double* __restrict__ prio, uint32_t n, uint32_t* bad,
+                         uint32_t* err) {
+  bool b = false;
+  for (uint32_t k = threadIdx.x; k < n; k += kThreads) {
+    const double p = prio[k];
+    b |= !(p >= 0.0) || isinf(p);
+  }
+  const int any = __syncthreads_or(b);
+  if (threadIdx.x == 0) {
+    *bad = any ? 1u : 0u;
+    if (any) atomicOr(err, kErrBadPriority);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads)
     insert_plan_kernel(AllocState* st, uint32_t ls, uint32_t shard, uint64_t Cs, int lifo,
                        uint32_t m, const double* __restrict__ prio, const uint32_t* __restrict__ ord,
-                       InsMeta* __restrict__ meta, OrdRec* __restrict__ ord_recs,
-                       uint64_t* __restrict__ out_idx, uint32_t* err) {
+                       const uint32_t* abort_flag, InsMeta* __restrict__ meta,
+                       OrdRec* __restrict__ ord_recs, uint64_t* __restrict__ out_idx,
+                       uint32_t* err) {
   const AllocState a = st[ls];
   const uint64_t F = Cs - a.next_free, L = a.len, C = F + L;
   const uint64_t base = (uint64_t)ls * Cs;
-  if (C == 0) {  // every slot is ongoing
+  const bool aborted = abort_flag != nullptr && *abort_flag != 0;  // a bad priority
+  if (C == 0 || aborted) {  // every slot is ongoing, or the call is rejected
     for (uint32_t k = threadIdx.x; k < m; k += kThreads) {
       meta[k].local = kIdxNone;
       ord_recs[k].pos = 0xffffffffu;
       out_idx[k] = kIdxNone;
     }
-    if (threadIdx.x == 0) atomicOr(err, kErrFull);
+    if (threadIdx.x == 0 && !aborted) atomicOr(err, kErrFull);
     return;
   }
   auto old_ring = [&](uint64_t i) -> uint32_t {  // i-th entry from the oldest
@@ -236,14 +255,21 @@ __global__ void __launch_bounds__(kThreads)
 
 }  // namespace
 
+cudaError_t launch_validate_prio(const double* prio, uint32_t n, uint32_t* bad, uint32_t* err,
+                                 cudaStream_t s) {
+  count_launch();
+  validate_prio_kernel<<<1, kThreads, 0, s>>>(prio, n, bad, err);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_insert_plan(AllocState* st, uint32_t ls, uint32_t shard, uint64_t Cs, int lifo,
-                               uint32_t m, const double* prio, const uint32_t* ord, InsMeta* meta,
-                               OrdRec* ord_recs, uint64_t* out_idx, uint32_t* err,
-                               cudaStream_t s) {
+                               uint32_t m, const double* prio, const uint32_t* ord,
+                               const uint32_t* abort_flag, InsMeta* meta, OrdRec* ord_recs,
+                               uint64_t* out_idx, uint32_t* err, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   count_launch();
-  insert_plan_kernel<<<1, kThreads, 0, s>>>(st, ls, shard, Cs, lifo, m, prio, ord, meta, ord_recs,
-                                            out_idx, err);
+  insert_plan_kernel<<<1, kThreads, 0, s>>>(st, ls, shard, Cs, lifo, m, prio, ord, abort_flag,
+                                            meta, ord_recs, out_idx, err);
   return cudaGetLastError();
 }
 

@@ -163,6 +163,7 @@ struct gear_table {
   gear::AllocState* d_alloc = nullptr;  // [R]
   double* h_prio = nullptr;         // pinned [max_batch]
   double* d_prio_ins = nullptr;     // [max_batch]
+  uint32_t* ins_bad = nullptr;      // device priorities of the current insert invalid
   uint64_t* h_out = nullptr;        // pinned
   gear::InsMeta* d_meta = nullptr;
   gear::OrdRec* d_ord = nullptr;

@@ -117,3 +117,75 @@ def test_full_shard(torch_cuda):
     idx = P.check_sample(G.GEAR_FIFO, 64, 0)
     P.check_collect(idx)
     P.close()
+
+
+def test_device_priorities_rejected_on_device(torch_cuda):
+    """gear_insert with device priorities validates them on the device: a NaN
+    latches BAD_PRIORITY and nothing is inserted."""
+    torch = torch_cuda
+    cols = [synth.ColSpec("x", "u8", (4,))]
+    P = _pair(capacity=64, seq_len=1, colspecs=cols, R=1)
+    P.insert(0, np.ones(10))
+    src = [torch.zeros((3, P.rb[0]), dtype=torch.uint8, device="cuda")]
+    prio = torch.tensor([1.0, float("nan"), 2.0], dtype=torch.float64, device="cuda")
+    out = torch.empty(3, dtype=torch.int64, device="cuda")
+    P.t.insert(0, src, prio, out)
+    err, _ = P.t.sync()
+    assert err & G.GEAR_DEVERR_BAD_PRIORITY
+    assert np.all(out.cpu().numpy().view(np.uint64) == np.uint64(G.GEAR_IDX_NONE))
+    P.check_state()
+    P.insert(0, np.ones(5))            # the allocator state was not touched
+    P.check_state()
+    P.close()
+
+
+@pytest.mark.parametrize("removal", [0, 1])
+def test_writer_calls_captured_in_a_graph(torch_cuda, removal):
+    """gear_insert (device rows and priorities) and gear_allocate -> gear_commit
+    (ids flowing through device memory) captured once in a CUDA graph and
+    replayed: every replay runs the allocator again on the device state and
+    equals the oracle doing the same calls."""
+    torch = torch_cuda
+    import oracle
+    cols = [synth.ColSpec("obs", "f32", (5,)), synth.ColSpec("act", "i32", ())]
+    Cs, B, A = 200, 48, 30
+    P = _pair(capacity=Cs, seq_len=2, colspecs=cols, R=1, removal=removal)
+    P.insert(0, synth.priorities(120, seed=1))
+    traj = np.arange(50_000, 50_000 + B)
+    rows = [synth.row_bytes_of(c, traj, rb) for c, rb in enumerate(P.rb)]
+    srcs = [torch.from_numpy(r).cuda() for r in rows]
+    p_ins = synth.priorities(B, seed=2)
+    p_com = synth.priorities(A, seed=3)
+    d_pins = torch.from_numpy(p_ins).cuda()
+    d_pcom = torch.from_numpy(p_com).cuda()
+    out_ins = torch.empty(B, dtype=torch.int64, device="cuda")
+    out_al = torch.empty(A, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+        G.gear_insert(P.t.handle, 0, B, srcs, d_pins, out_ins, s)
+        G.gear_allocate(P.t.handle, 0, A, out_al, s)
+        G.gear_commit(P.t.handle, 0, A, out_al, d_pcom, s)
+    torch.cuda.synchronize()
+    P.check_state()                    # capturing ran nothing
+    for rep in range(6):
+        with torch.cuda.stream(s):
+            g.replay()
+        torch.cuda.synchronize()
+        st, oids = P.o.insert(0, p_ins)
+        assert st == 0
+        for c in range(len(P.rb)):
+            P.mirror[c][oids.astype(np.int64)] = rows[c]
+        st, aids = P.o.allocate(0, A)
+        assert st == 0
+        assert P.o.commit(0, aids, p_com) == 0
+        assert np.array_equal(out_ins.cpu().numpy().view(np.uint64), oids)
+        assert np.array_equal(out_al.cpu().numpy().view(np.uint64), aids)
+        P.t.sync()
+        P.check_state()
+        for strat in (G.GEAR_FIFO, G.GEAR_LIFO, G.GEAR_PRIORITIZED):
+            idx = P.check_sample(strat, 64, rep)
+            P.check_collect(idx)
+    assert oracle.OK == 0
+    P.close()
