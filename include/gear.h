@@ -350,6 +350,11 @@ gear_status gear_table_load(gear_table* t, const char* path);
  *   "update_fused": 1 = priority updates of <= 8192 entries (all ranks) run
  *                   tag + apply in one single-CTA launch (default), 0 = two
  *                   grid-wide launches;
+ *   "collect_permute": 1 = gear_collect visits the requested rows in the
+ *                   order j*m mod n (m coprime with n, near n/phi) so that
+ *                   peer / host rows that sit together in the request overlap
+ *                   local HBM rows; 0 = request order (default: measured 2%
+ *                   faster at c2 on 1 and 2 GPUs); the output is the same;
  *   "cdf_levels":   same value on every rank; 2 = two-level CDF (default):
  *                   every 4096-key tile of a shard holds its own prefix sum,
  *                   the shard a prefix sum of the tile totals, and a rebuild

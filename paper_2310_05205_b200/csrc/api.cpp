@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <numeric>
 #include <random>
 #include <unordered_map>
 
@@ -212,6 +213,7 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
     return set_error(GEAR_ERR_INVALID_ARG, "ncols must be 1..%d", kMaxCols);
   if (const char* e = getenv("GEAR_COLLECT_CHUNK")) t->chunk_bytes = (uint32_t)atoi(e);
   if (const char* e = getenv("GEAR_TMA_CHUNK")) t->tma_chunk = (uint32_t)atoi(e);
+  if (const char* e = getenv("GEAR_COLLECT_PERMUTE")) t->collect_permute = atoi(e) != 0;
   if (const char* e = getenv("GEAR_COLLECT_IMPL")) t->collect_impl = strcmp(e, "lsu") == 0 ? 0 : 1;
   if (t->tma_chunk < 4096 || t->tma_chunk % 16 || t->tma_chunk > 32768)
     return set_error(GEAR_ERR_INVALID_ARG, "GEAR_TMA_CHUNK must be a multiple of 16 in [4096, 32768]");
@@ -999,6 +1001,12 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
   cp.ncols = ncols;
   cp.n = n;
   cp.err = t->err;
+  cp.row_mult = 1;
+  if (t->collect_permute && n > 2) {  // an odd multiplier near n/phi, coprime with n
+    uint64_t m = ((uint64_t)n * 618034ull / 1000000ull) | 1ull;
+    while (std::gcd(m, (uint64_t)n) != 1) m += 2;
+    cp.row_mult = m;
+  }
   cp.tma_ctas_per_sm = (uint32_t)t->tma_ctas;
   cp.tma_stages = (uint32_t)t->tma_stages;
   for (uint32_t c = 0; c < ncols; ++c) {
@@ -1071,6 +1079,8 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     GEAR_CUDA(cudaMemset(t->cdf_buf_mode, 0, 8));  // both buffers: full rebuild
     t->cdf_levels = (int)value;
     t->dirty = true;
+  } else if (!strcmp(key, "collect_permute") && (value == 0 || value == 1)) {
+    t->collect_permute = (int)value;
   } else if (!strcmp(key, "update_fused") && (value == 0 || value == 1)) {
     t->update_fused = (int)value;
   } else if (!strcmp(key, "tma_ctas_per_sm") && value >= 1 && value <= 8 &&

@@ -84,10 +84,14 @@ __device__ __forceinline__ void decode_task(const CollectParams& p, const uint8_
   while (ci + 1 < ncols && task >= p.col[cols[ci + 1]].chunk_begin) ++ci;
   const uint32_t c = cols[ci];
   const uint64_t rel = task - p.col[c].chunk_begin;
-  const uint64_t j = rel / p.col[c].chunks_per_row;
+  const uint64_t jt = rel / p.col[c].chunks_per_row;
   *c_out = c;
-  *j_out = j;
-  *k_out = rel - j * p.col[c].chunks_per_row;
+  // Rows are visited in the order jt * row_mult mod n (row_mult coprime with
+  // n): rows of one kind that sit together in the request -- e.g. the peer
+  // rows an owner-affine slice puts last -- are spread over the whole launch,
+  // so NVLink / PCIe reads overlap local HBM reads instead of forming a tail.
+  *j_out = p.row_mult > 1 ? (jt * p.row_mult) % p.n : jt;
+  *k_out = rel - jt * p.col[c].chunks_per_row;
 }
 
 // Warps [w_first, w_first + w_count) of every CTA walk the LSU task space.
