@@ -350,6 +350,11 @@ gear_status gear_table_load(gear_table* t, const char* path);
  *   "update_fused": 1 = priority updates of <= 8192 entries (all ranks) run
  *                   tag + apply in one single-CTA launch (default), 0 = two
  *                   grid-wide launches;
+ *   "collect_peer_lsu": W > 1: 1 = the peer-HBM rows of bulk-copied (TMA)
+ *                   columns are moved by the LSU warps instead of the bulk
+ *                   pipeline (+3% collect throughput when few rows are
+ *                   remote, -11% when half are); 0 = all by the bulk
+ *                   pipeline (default);
  *   "collect_permute": 1 = gear_collect visits the requested rows in the
  *                   order j*m mod n (m coprime with n, near n/phi) so that
  *                   peer / host rows that sit together in the request overlap

@@ -214,6 +214,17 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   if (const char* e = getenv("GEAR_COLLECT_CHUNK")) t->chunk_bytes = (uint32_t)atoi(e);
   if (const char* e = getenv("GEAR_TMA_CHUNK")) t->tma_chunk = (uint32_t)atoi(e);
   if (const char* e = getenv("GEAR_COLLECT_PERMUTE")) t->collect_permute = atoi(e) != 0;
+  if (const char* e = getenv("GEAR_COLLECT_PEER_LSU")) t->collect_peer_lsu = atoi(e) != 0;
+  if (const char* e = getenv("GEAR_TMA_STAGES")) {
+    const int v = atoi(e);
+    if (v == 2 || v == 3 || v == 4 || v == 6 || v == 8) t->tma_stages = v;
+  }
+  if (const char* e = getenv("GEAR_TMA_CTAS")) {
+    const int v = atoi(e);
+    if (v >= 1 && v <= 8) t->tma_ctas = v;
+  }
+  if ((uint64_t)t->tma_ctas * t->tma_stages * t->tma_chunk > (220u << 10))
+    return set_error(GEAR_ERR_INVALID_ARG, "GEAR_TMA_CTAS * GEAR_TMA_STAGES * tma_chunk > 220 KB");
   if (const char* e = getenv("GEAR_COLLECT_IMPL")) t->collect_impl = strcmp(e, "lsu") == 0 ? 0 : 1;
   if (t->tma_chunk < 4096 || t->tma_chunk % 16 || t->tma_chunk > 32768)
     return set_error(GEAR_ERR_INVALID_ARG, "GEAR_TMA_CHUNK must be a multiple of 16 in [4096, 32768]");
@@ -1007,6 +1018,7 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
     while (std::gcd(m, (uint64_t)n) != 1) m += 2;
     cp.row_mult = m;
   }
+  cp.self_rank = t->rank;
   cp.tma_ctas_per_sm = (uint32_t)t->tma_ctas;
   cp.tma_stages = (uint32_t)t->tma_stages;
   for (uint32_t c = 0; c < ncols; ++c) {
@@ -1027,6 +1039,8 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
     cc.chunk = cc.tma ? t->tma_chunk : t->chunk_bytes;
     if (cc.vec < 16 && cc.chunk % cc.vec) cc.chunk = t->chunk_bytes;
     cc.chunks_per_row = (uint32_t)((cs.rb + cc.chunk - 1) / cc.chunk);
+    cc.peer_lsu = (cc.tma && t->W > 1 && cs.placement == GEAR_DEVICE && t->collect_peer_lsu) ? 1u : 0u;
+    cp.any_peer_lsu |= cc.peer_lsu;
     if (cc.tma) {
       cc.chunk_begin = cp.tma_total;
       cp.tma_total += (uint64_t)n * cc.chunks_per_row;
@@ -1079,6 +1093,8 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     GEAR_CUDA(cudaMemset(t->cdf_buf_mode, 0, 8));  // both buffers: full rebuild
     t->cdf_levels = (int)value;
     t->dirty = true;
+  } else if (!strcmp(key, "collect_peer_lsu") && (value == 0 || value == 1)) {
+    t->collect_peer_lsu = (int)value;
   } else if (!strcmp(key, "collect_permute") && (value == 0 || value == 1)) {
     t->collect_permute = (int)value;
   } else if (!strcmp(key, "update_fused") && (value == 0 || value == 1)) {

@@ -164,6 +164,7 @@ struct CollectCol {
   uint32_t chunk;                     // bytes per task of this column
   uint32_t vec;                       // LSU vector width in bytes: 16, 8, 4, 2 or 1
   uint32_t tma;                       // 1: moved by TMA bulk copies (16-B aligned rows)
+  uint32_t peer_lsu;                  // TMA column whose peer-HBM rows the LSU warps move
 };
 
 struct CollectParams {
@@ -182,6 +183,8 @@ struct CollectParams {
   uint32_t ncols;
   uint32_t n;
   uint64_t row_mult;                  // row visiting order j -> j*row_mult mod n (1: in order)
+  uint32_t self_rank;                 // this rank (peer rows: owner != self_rank)
+  uint32_t any_peer_lsu;              // some column has peer_lsu
   uint32_t* err;
 };
 

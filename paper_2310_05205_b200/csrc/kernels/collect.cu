@@ -147,6 +147,31 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
+// W > 1: the peer-HBM rows of TMA columns, moved over NVLink by the LSU warps
+// with 16-byte loads (many independent loads in flight per warp) instead of
+// the single-lane bulk pipeline, where one slow NVLink chunk would hold up
+// the in-order stages behind it.
+__device__ __forceinline__ void collect_peer_rows(const CollectParams& p, uint64_t warp0,
+                                                  uint64_t nwarps, int lane) {
+  for (uint64_t task = warp0; task < p.tma_total; task += nwarps) {
+    uint32_t c;
+    uint64_t j, k;
+    decode_task(p, p.tma_cols, p.n_tma, task, &c, &j, &k);
+    const CollectCol& col = p.col[c];
+    if (!col.peer_lsu) continue;
+    const uint64_t g = __ldg(p.idx + j);
+    if (g >= p.n_global) continue;  // latched by the TMA lane
+    const uint64_t owner = g / p.rows_per_rank;
+    if (owner == p.self_rank) continue;
+    const uint64_t local = g - owner * p.rows_per_rank;
+    const uint64_t off = k * (uint64_t)col.chunk;
+    const uint64_t rem = col.rb - off;
+    const uint64_t bytes = rem < col.chunk ? rem : col.chunk;
+    copy_dispatch(16, col.out + j * col.rb + off, col.src[owner] + local * col.rb + off, bytes,
+                  lane);
+  }
+}
+
 // Issue the bulk load of TMA task `task` into stage `s` (mbarrier bars[s]).
 // Returns the bytes moved (0 for an invalid id: the barrier is still armed).
 __device__ __forceinline__ uint32_t tma_issue_load(const CollectParams& p, uint64_t task,
@@ -163,6 +188,10 @@ __device__ __forceinline__ uint32_t tma_issue_load(const CollectParams& p, uint6
     return 0;
   }
   const uint64_t owner = g / p.rows_per_rank;
+  if (col.peer_lsu && owner != p.self_rank) {  // a peer's HBM row: the LSU warps move it
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+    return 0;
+  }
   const uint64_t local = g - owner * p.rows_per_rank;
   const uint64_t off = k * (uint64_t)col.chunk;
   const uint64_t rem = col.rb - off;
@@ -191,7 +220,9 @@ __global__ void __launch_bounds__(kTmaThreads)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp != 0) {
     const uint64_t w0 = (uint64_t)blockIdx.x * (kTmaThreads / 32 - 1) + (warp - 1);
-    collect_lsu(p, w0, (uint64_t)gridDim.x * (kTmaThreads / 32 - 1), lane);
+    const uint64_t nw = (uint64_t)gridDim.x * (kTmaThreads / 32 - 1);
+    collect_lsu(p, w0, nw, lane);
+    if (p.any_peer_lsu) collect_peer_rows(p, w0, nw, lane);
     return;
   }
   if (lane != 0) return;
