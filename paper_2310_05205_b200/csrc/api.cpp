@@ -215,6 +215,7 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   if (const char* e = getenv("GEAR_TMA_CHUNK")) t->tma_chunk = (uint32_t)atoi(e);
   if (const char* e = getenv("GEAR_COLLECT_PERMUTE")) t->collect_permute = atoi(e) != 0;
   if (const char* e = getenv("GEAR_COLLECT_PEER_LSU")) t->collect_peer_lsu = atoi(e) != 0;
+  if (const char* e = getenv("GEAR_TMA_OOO")) t->tma_ooo = atoi(e) != 0;
   if (const char* e = getenv("GEAR_TMA_STAGES")) {
     const int v = atoi(e);
     if (v == 2 || v == 3 || v == 4 || v == 6 || v == 8) t->tma_stages = v;
@@ -1021,6 +1022,7 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
   cp.self_rank = t->rank;
   cp.tma_ctas_per_sm = (uint32_t)t->tma_ctas;
   cp.tma_stages = (uint32_t)t->tma_stages;
+  cp.tma_ooo = (uint32_t)t->tma_ooo;
   for (uint32_t c = 0; c < ncols; ++c) {
     if (col_ids[c] >= t->cols.size()) return set_error(GEAR_ERR_INVALID_ARG, "bad column id %u", col_ids[c]);
     if (out[c] == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "out[%u] is NULL", c);
@@ -1093,6 +1095,8 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     GEAR_CUDA(cudaMemset(t->cdf_buf_mode, 0, 8));  // both buffers: full rebuild
     t->cdf_levels = (int)value;
     t->dirty = true;
+  } else if (!strcmp(key, "tma_ooo") && (value == 0 || value == 1)) {
+    t->tma_ooo = (int)value;
   } else if (!strcmp(key, "collect_peer_lsu") && (value == 0 || value == 1)) {
     t->collect_peer_lsu = (int)value;
   } else if (!strcmp(key, "collect_permute") && (value == 0 || value == 1)) {

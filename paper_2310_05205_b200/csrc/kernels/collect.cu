@@ -212,7 +212,79 @@ __device__ __forceinline__ uint32_t tma_issue_load(const CollectParams& p, uint6
 // flight while task n is stored; the stage of task n-1 is refilled (task
 // n-1+kStages) once its store has finished reading shared memory
 // (wait_group.read 1: only the store of task n may still be reading).
+// Waits until at most n of this thread's bulk groups are still reading
+// shared memory (the PTX operand must be an immediate).
+__device__ __forceinline__ void bulk_wait_read(uint32_t n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.bulk.wait_group.read 5;" ::: "memory"); break;
+    case 6: asm volatile("cp.async.bulk.wait_group.read 6;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group.read 7;" ::: "memory"); break;
+  }
+}
+
+// Out-of-order variant of the issuing lane's ring (tuning "tma_ooo"): a stage
+// is stored as soon as ITS load lands, whichever stage that is, so one slow
+// chunk (a peer row over NVLink, a far DRAM page) no longer holds up the
+// stages behind it.  Stages whose store was issued are recycled in store
+// order: wait_group.read (pending - 1) frees the oldest.
 template <int kStages>
+__device__ __forceinline__ void tma_lane_ooo(const CollectParams& p, uint32_t base,
+                                             uint64_t* bars, uint32_t stage_bytes) {
+  const uint64_t first = blockIdx.x, step = gridDim.x;
+  const uint64_t ntask = p.tma_total > first ? (p.tma_total - first + step - 1) / step : 0;
+  uint8_t* dst[kStages] = {};
+  uint32_t nbytes[kStages] = {};
+  uint32_t phase = 0, loading = 0;  // bit s: stage s has a load in flight
+  int fifo[kStages];                // stages with a store pending, oldest first
+  uint32_t fh = 0, fn = 0;
+  uint64_t next = 0, done = 0;
+  uint32_t free_mask = (1u << kStages) - 1u;
+  while (done < ntask) {
+    // refill: a free stage, else the stage of the oldest pending store
+    while (next < ntask && (free_mask || fn)) {
+      int s;
+      if (free_mask) {
+        s = __ffs(free_mask) - 1;
+        free_mask &= free_mask - 1;
+      } else {
+        bulk_wait_read(fn - 1);  // the oldest store has read its stage
+        s = fifo[fh];
+        fh = (fh + 1) % kStages;
+        --fn;
+      }
+      nbytes[s] = tma_issue_load(p, first + next * step, base + (uint32_t)s * stage_bytes,
+                                 smem_u32(&bars[s]), &dst[s]);
+      loading |= 1u << s;
+      ++next;
+    }
+    // store every stage whose load has landed
+    for (int s = 0; s < kStages; ++s) {
+      if (!((loading >> s) & 1u)) continue;
+      if (!mbar_try_wait(smem_u32(&bars[s]), (phase >> s) & 1u)) continue;
+      phase ^= 1u << s;
+      loading &= ~(1u << s);
+      ++done;
+      if (nbytes[s]) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst[s]),
+                     "r"(base + (uint32_t)s * stage_bytes), "r"(nbytes[s])
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        fifo[(fh + fn) % kStages] = s;
+        ++fn;
+      } else {
+        free_mask |= 1u << s;
+      }
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <int kStages, bool kOoo>
 __global__ void __launch_bounds__(kTmaThreads)
     collect_tma_kernel(const __grid_constant__ CollectParams p, uint32_t stage_bytes) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -230,6 +302,10 @@ __global__ void __launch_bounds__(kTmaThreads)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[s])) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if constexpr (kOoo) {
+    tma_lane_ooo<kStages>(p, smem_u32(smem), bars, stage_bytes);
+    return;
+  }
   const uint64_t first = blockIdx.x, step = gridDim.x;
   const uint64_t ntask = p.tma_total > first ? (p.tma_total - first + step - 1) / step : 0;
   const uint32_t base = smem_u32(smem);
@@ -315,13 +391,13 @@ int grid_for(K kernel, uint64_t tasks) {
 
 // kStages stages of tma_chunk bytes per CTA, ctas CTAs per SM (192 KB of
 // shared memory per SM either way).
-template <int kStages>
+template <int kStages, bool kOoo>
 cudaError_t launch_tma(const CollectParams& p, int ctas, cudaStream_t s) {
   const uint32_t stage_bytes = p.col[p.tma_cols[0]].chunk;
   const size_t smem = (size_t)kStages * stage_bytes;
   static size_t configured = 0;
   if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(collect_tma_kernel<kStages>,
+    cudaError_t e = cudaFuncSetAttribute(collect_tma_kernel<kStages, kOoo>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = smem;
@@ -330,8 +406,19 @@ cudaError_t launch_tma(const CollectParams& p, int ctas, cudaStream_t s) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   count_launch();
-  collect_tma_kernel<kStages><<<sms * ctas, kTmaThreads, smem, s>>>(p, stage_bytes);
+  collect_tma_kernel<kStages, kOoo><<<sms * ctas, kTmaThreads, smem, s>>>(p, stage_bytes);
   return cudaGetLastError();
+}
+
+template <bool kOoo>
+cudaError_t launch_tma_stages(const CollectParams& p, int ctas, cudaStream_t s) {
+  switch (p.tma_stages) {
+    case 2: return launch_tma<2, kOoo>(p, ctas, s);
+    case 3: return launch_tma<3, kOoo>(p, ctas, s);
+    case 4: return launch_tma<4, kOoo>(p, ctas, s);
+    case 6: return launch_tma<6, kOoo>(p, ctas, s);
+    default: return launch_tma<8, kOoo>(p, ctas, s);
+  }
 }
 
 cudaError_t launch_collect(const CollectParams& p, cudaStream_t s) {
@@ -342,13 +429,7 @@ cudaError_t launch_collect(const CollectParams& p, cudaStream_t s) {
     return cudaGetLastError();
   }
   const int ctas = (int)p.tma_ctas_per_sm;
-  switch (p.tma_stages) {
-    case 2: return launch_tma<2>(p, ctas, s);
-    case 3: return launch_tma<3>(p, ctas, s);
-    case 4: return launch_tma<4>(p, ctas, s);
-    case 6: return launch_tma<6>(p, ctas, s);
-    default: return launch_tma<8>(p, ctas, s);
-  }
+  return p.tma_ooo ? launch_tma_stages<true>(p, ctas, s) : launch_tma_stages<false>(p, ctas, s);
 }
 
 cudaError_t launch_scatter(const ScatterParams& p, cudaStream_t s) {

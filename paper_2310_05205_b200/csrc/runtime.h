@@ -177,6 +177,7 @@ struct gear_table {
   int tma_ctas = 2;                 // TMA collect CTAs per SM
   int tma_stages = 3;               // shared-memory stages per TMA CTA
   int collect_impl = 1;             // 1: TMA bulk copies for large aligned rows, 0: LSU only
+  int tma_ooo = 0;                  // TMA ring stored in completion order
   int collect_peer_lsu = 0;         // W > 1: peer-HBM rows of TMA columns via LSU warps
   int collect_permute = 0;          // visit rows in a coprime-stride order (measured slower)
 };
