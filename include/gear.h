@@ -350,6 +350,9 @@ gear_status gear_table_load(gear_table* t, const char* path);
  *   "update_fused": 1 = priority updates of <= 8192 entries (all ranks) run
  *                   tag + apply in one single-CTA launch (default), 0 = two
  *                   grid-wide launches;
+ *   "tma_ooo":      1 = the bulk pipeline stores its stages in completion
+ *                   order instead of ring order (measured 2% slower at c2;
+ *                   default 0);
  *   "collect_peer_lsu": W > 1: 1 = the peer-HBM rows of bulk-copied (TMA)
  *                   columns are moved by the LSU warps instead of the bulk
  *                   pipeline (+3% collect throughput when few rows are
