@@ -389,3 +389,43 @@ def test_collect_large_rows_tma_and_lsu(torch_cuda, impl, placement):
     with pytest.raises(G.GearError):
         G.gear_table_set_tuning(P.t.handle, "tma_chunk", 100)
     P.close()
+
+
+@pytest.mark.parametrize("levels", [2, 1])
+@pytest.mark.parametrize("R", [1, 3, 8])
+def test_adversarial_keys(torch_cuda, R, levels):
+    """SURVEY.md §8 d.1 extras: every key at q_max (the total just below 2^62),
+    one dominant q_max key among keys of 1, and a single selectable slot --
+    sampled ids, q/T and IS weights equal the oracle's on both CDF layouts."""
+    cols = [synth.ColSpec("x", "u8", (2,))]
+    Cs = 4096 + 123                                    # two tiles per shard, ragged
+    N = Cs * R
+    P = _pair(capacity=N, seq_len=1, colspecs=cols, R=R)
+    G.gear_table_set_tuning(P.t.handle, "cdf_levels", levels)
+    P.fill(np.full(N, 1e300))                          # all keys q_max: T = N*q_max < 2^62
+    qmax = G.gear_table_info_get(P.t.handle)["q_max"]
+    assert int(P.o.key.astype(object).sum()) == N * qmax < (1 << 62)
+    for strat in (G.GEAR_PRIORITIZED, G.GEAR_WEIGHTED, G.GEAR_UNIFORM):
+        P.check_sample(strat, 2048, 11, beta=0.7)
+    ids = np.arange(N, dtype=np.uint64)
+
+    def update_all(v):                                 # in max_batch chunks
+        for k0 in range(0, N, 4096):
+            P.update(ids[k0:k0 + 4096], np.full(min(4096, N - k0), v))
+
+    update_all(2.0 ** -32)                             # every key 1 ...
+    P.update(np.array([N // 2 + 7], np.uint64), [1e300])   # ... but one at q_max
+    P.check_state()
+    idx = P.check_sample(G.GEAR_PRIORITIZED, 2048, 12, beta=0.4)
+    assert np.mean(idx == N // 2 + 7) > 0.9
+    update_all(0.0)                                    # nothing selectable but one
+    P.update(np.array([N - 1], np.uint64), [3.0])
+    for strat in (G.GEAR_PRIORITIZED, G.GEAR_UNIFORM, G.GEAR_FIFO, G.GEAR_TOPK):
+        if strat in (G.GEAR_FIFO, G.GEAR_TOPK):
+            idx = P.check_sample(strat, 1, 0)
+        else:
+            idx = P.check_sample(strat, 512, 13)
+        assert np.all(idx == N - 1)
+    P.update(np.array([N - 1], np.uint64), [0.0])      # nothing selectable: EMPTY
+    assert P.check_sample(G.GEAR_PRIORITIZED, 64, 14) is None
+    P.close()
