@@ -330,23 +330,25 @@ def run_gpu(args):
     # sample(i-1) and reads its host buffers) while step i runs.  Host buffers
     # are double buffered.
     barrier()
-    h_idx2 = [h_idx, torch.empty(B, dtype=torch.int64, pin_memory=True)]
-    h_w2 = [h_w, torch.empty(B, dtype=torch.float32, pin_memory=True)]
-    ev_hs = [torch.cuda.Event() for _ in range(2)]
+    LAG = 2                       # the host reads step i-LAG while steps i-LAG+1..i run
+    NH = 2 * LAG                  # host buffers
+    h_idx2 = [h_idx] + [torch.empty(B, dtype=torch.int64, pin_memory=True) for _ in range(NH - 1)]
+    h_w2 = [h_w] + [torch.empty(B, dtype=torch.float32, pin_memory=True) for _ in range(NH - 1)]
+    ev_hs = [torch.cuda.Event() for _ in range(NH)]
     np_idx2 = [x.numpy() for x in h_idx2]   # host views of the pinned buffers
     np_w2 = [x.numpy() for x in h_w2]
     consumed = 0.0
 
     def step_e2e(i):
-        b = i % 2
+        b, hb = i % 2, i % NH
         if i >= 2:
             stream.wait_event(ev_collected[b])   # collect(i-2) has read idx2[b]
         gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + 7919 + i, cfg.beta,
-                         idx2[b], h_w2[b], None, None, stream)
+                         idx2[b], h_w2[hb], None, None, stream)
         ev_sampled[b].record(stream)
         with torch.cuda.stream(stream):
-            h_idx2[b].copy_(idx2[b], non_blocking=True)
-        ev_hs[b].record(stream)
+            h_idx2[hb].copy_(idx2[b], non_blocking=True)
+        ev_hs[hb].record(stream)
         if cfg.update:
             gear.gear_update_priorities(t.handle, B, idx2[b], h_prio[i % 16], gear.GEAR_F64,
                                         None, stream)
@@ -362,11 +364,13 @@ def run_gpu(args):
     cstream.wait_event(e2)
     for i in range(args.steps):
         step_e2e(i)
-        if i >= 1:   # the host reads step i-1's result while step i runs
-            ev_hs[(i - 1) % 2].synchronize()
-            consumed += float(np_w2[(i - 1) % 2][0]) + float(np_idx2[(i - 1) % 2][B - 1])
-    ev_hs[(args.steps - 1) % 2].synchronize()
-    consumed += float(np_w2[(args.steps - 1) % 2][0])
+        if i >= LAG:   # the host reads step i-LAG's result while later steps run
+            hb = (i - LAG) % NH
+            ev_hs[hb].synchronize()
+            consumed += float(np_w2[hb][0]) + float(np_idx2[hb][B - 1])
+    for i in range(max(0, args.steps - LAG), args.steps):
+        ev_hs[i % NH].synchronize()
+        consumed += float(np_w2[i % NH][0]) + float(np_idx2[i % NH][B - 1])
     stream.wait_stream(cstream)
     e3.record(stream)
     barrier()
@@ -446,7 +450,7 @@ def run_gpu(args):
                 "d2h_bytes_per_step": e2e_d2h,
                 "path": ("C-ABI; priorities from pinned host memory, ids and IS weights to "
                          "pinned host memory, batch in HBM; pipelined (collect on a 2nd stream), "
-                         "the host reads each step's ids and weights one step behind")},
+                         "the host reads every step's ids and weights two steps behind")},
         "gpu_launches": int(launches),
         "clocks": clk,
     }

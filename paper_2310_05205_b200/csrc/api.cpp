@@ -475,12 +475,26 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
 }
 
 // Make `n` elements at `user` available on the device: device pointers pass
-// through, host pointers are copied into `scratch` on the stream.
+// through, host pointers are copied into `scratch` on the stream -- except
+// pinned host memory with `zero_copy`, which the kernel reads in place over
+// PCIe through its mapped address (for arrays every element of which is read
+// once: no copy-engine operation on the step, same stream-order lifetime rule
+// as an async copy).
 template <class T>
-gear_status stage_in(const T* user, size_t n, T* scratch, cudaStream_t s, const T** out) {
-  if (n == 0 || mem_kind(user) == MemKind::Device) {
+gear_status stage_in(const T* user, size_t n, T* scratch, cudaStream_t s, const T** out,
+                     bool zero_copy = false) {
+  const MemKind k = n == 0 ? MemKind::Device : mem_kind(user);
+  if (k == MemKind::Device) {
     *out = user;
     return GEAR_OK;
+  }
+  if (zero_copy && k == MemKind::HostPinned) {
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, const_cast<T*>(user), 0) == cudaSuccess) {
+      *out = static_cast<const T*>(dp);
+      return GEAR_OK;
+    }
+    cudaGetLastError();  // not mapped: copy instead
   }
   GEAR_CUDA(cudaMemcpyAsync(scratch, user, n * sizeof(T), cudaMemcpyHostToDevice, s));
   *out = scratch;
@@ -711,17 +725,17 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
   const void* d_prio = prio;
   const uint32_t* d_gen = gen;
   if (n > 0) {
-    GEAR_TRY(stage_in(idx, n, t->upd_idx, s, &d_idx));
+    GEAR_TRY(stage_in(idx, n, t->upd_idx, s, &d_idx, true));
     if (prio_dtype == GEAR_F64) {
       const double* dp = nullptr;
-      GEAR_TRY(stage_in((const double*)prio, n, t->upd_prio, s, &dp));
+      GEAR_TRY(stage_in((const double*)prio, n, t->upd_prio, s, &dp, true));
       d_prio = dp;
     } else {
       const float* dp = nullptr;
-      GEAR_TRY(stage_in((const float*)prio, n, (float*)t->upd_prio, s, &dp));
+      GEAR_TRY(stage_in((const float*)prio, n, (float*)t->upd_prio, s, &dp, true));
       d_prio = dp;
     }
-    if (gen) GEAR_TRY(stage_in(gen, n, t->upd_gen, s, &d_gen));
+    if (gen) GEAR_TRY(stage_in(gen, n, t->upd_gen, s, &d_gen, true));
   }
   // PER exponent: the update kernels quantise p^alpha computed here first
   Quant qz = quant(t);

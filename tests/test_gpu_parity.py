@@ -429,3 +429,33 @@ def test_adversarial_keys(torch_cuda, R, levels):
     P.update(np.array([N - 1], np.uint64), [0.0])      # nothing selectable: EMPTY
     assert P.check_sample(G.GEAR_PRIORITIZED, 64, 14) is None
     P.close()
+
+
+def test_update_from_pinned_and_pageable_host(torch_cuda):
+    """gear_update_priorities reads pinned host ids / priorities / generations
+    in place (zero-copy) and copies pageable ones; both equal the oracle."""
+    torch = torch_cuda
+    cols = [synth.ColSpec("x", "u8", (4,))]
+    P = _pair(capacity=512, seq_len=1, colspecs=cols, R=2)
+    P.fill(np.ones(512))
+    rng = np.random.default_rng(3)
+    for kind in ("pinned", "pageable"):
+        for fused in (1, 0):
+            G.gear_table_set_tuning(P.t.handle, "update_fused", fused)
+            ids = rng.integers(0, 512, 300).astype(np.uint64)
+            p = rng.lognormal(0, 1, 300)
+            gen = P.o.gen[ids.astype(np.int64)].copy()
+            gen[::5] += 1                                   # some stale
+            if kind == "pinned":
+                h_ids = torch.from_numpy(ids.view(np.int64)).pin_memory()
+                h_p = torch.from_numpy(p).pin_memory()
+                h_g = torch.from_numpy(gen.view(np.int32)).pin_memory()
+            else:
+                h_ids, h_p, h_g = ids, p, gen
+            G.gear_update_priorities(P.t.handle, 300, h_ids, h_p, G.GEAR_F64, h_g)
+            torch.cuda.synchronize()
+            ost, ons = P.o.update(ids, p, gen)
+            err, ns = P.t.sync()
+            assert ns == ons
+            P.check_state()
+    P.close()
