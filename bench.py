@@ -324,11 +324,10 @@ def run_gpu(args):
     # step.  Every step: gear_sample writes the IS weights straight to pinned
     # host memory (D2H inside the call) and the ids to HBM, from where they are
     # copied to pinned host memory for the host; gear_update_priorities reads
-    # that step's f64 priorities from pinned host memory (H2D inside the call);
+    # that step's f64 priorities from pinned host memory (in place, over PCIe);
     # gear_collect (collect stream) gathers the rows into HBM.  The host
-    # consumes each step's ids and weights one step behind (waits for
-    # sample(i-1) and reads its host buffers) while step i runs.  Host buffers
-    # are double buffered.
+    # consumes every step's ids and weights LAG steps behind (waits for
+    # sample(i-LAG) and reads its host buffers) while later steps run.
     barrier()
     LAG = 2                       # the host reads step i-LAG while steps i-LAG+1..i run
     NH = 2 * LAG                  # host buffers
