@@ -501,6 +501,24 @@ gear_status stage_in(const T* user, size_t n, T* scratch, cudaStream_t s, const 
   return GEAR_OK;
 }
 
+// Where a kernel writes an output the caller passed: device memory as is,
+// pinned host memory through its mapped address, pageable host memory into
+// `scratch` (*copy_back = true: copied to the caller at the end).
+template <class T>
+T* out_device(T* user, T* scratch, bool* copy_back) {
+  *copy_back = false;
+  if (user == nullptr) return nullptr;
+  const MemKind k = mem_kind(user);
+  if (k == MemKind::Device) return user;
+  if (k == MemKind::HostPinned) {
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, user, 0) == cudaSuccess) return static_cast<T*>(dp);
+    cudaGetLastError();
+  }
+  *copy_back = true;
+  return scratch;
+}
+
 uint32_t vec_width(uint64_t rb, uint32_t chunk, std::initializer_list<uintptr_t> ptrs) {
   for (uint32_t v : {16u, 8u, 4u, 2u}) {
     bool ok = rb % v == 0 && chunk % v == 0;
@@ -805,14 +823,14 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
   if (out_idx == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "out_idx is NULL");
   if (!std::isfinite(beta)) return set_error(GEAR_ERR_INVALID_ARG, "beta is not finite");
   // Outputs: device pointers are written in place, host ones via scratch.
-  const bool h_idx = mem_kind(out_idx) != MemKind::Device;
-  const bool h_w = out_w && mem_kind(out_w) != MemKind::Device;
-  const bool h_p = out_p && mem_kind(out_p) != MemKind::Device;
-  const bool h_gen = out_gen && mem_kind(out_gen) != MemKind::Device;
-  uint64_t* d_idx = h_idx ? t->tmp_idx : out_idx;
-  float* d_w = out_w ? (h_w ? t->tmp_w : out_w) : nullptr;
-  double* d_p = out_p ? (h_p ? t->tmp_p : out_p) : nullptr;
-  uint32_t* d_gen = out_gen ? (h_gen ? t->tmp_gen : out_gen) : nullptr;
+  // Outputs: device and pinned host buffers are written in place by the
+  // kernels (pinned ones through their mapped address, over PCIe); pageable
+  // host buffers through device scratch and a copy at the end.
+  bool h_idx = false, h_w = false, h_p = false, h_gen = false;
+  uint64_t* d_idx = out_device(out_idx, t->tmp_idx, &h_idx);
+  float* d_w = out_device(out_w, t->tmp_w, &h_w);
+  double* d_p = out_device(out_p, t->tmp_p, &h_p);
+  uint32_t* d_gen = out_device(out_gen, t->tmp_gen, &h_gen);
 
   if (strategy == GEAR_FIFO || strategy == GEAR_LIFO || strategy == GEAR_TOPK) {
     const uint32_t K = t->W * B;

@@ -459,3 +459,37 @@ def test_update_from_pinned_and_pageable_host(torch_cuda):
             assert ns == ons
             P.check_state()
     P.close()
+
+
+@pytest.mark.parametrize("strat", ["prioritized", "fifo"])
+def test_sample_into_pinned_and_pageable_host(torch_cuda, strat):
+    """gear_sample writes pinned host outputs in place (mapped, zero-copy) and
+    pageable ones through scratch + copy; both equal the device outputs and
+    the oracle."""
+    torch = torch_cuda
+    import oracle
+    cols = [synth.ColSpec("x", "u8", (4,))]
+    P = _pair(capacity=600, seq_len=1, colspecs=cols, R=3)
+    P.fill(synth.priorities(600, seed=8, zero_frac=0.1))
+    S = G.GEAR_PRIORITIZED if strat == "prioritized" else G.GEAR_FIFO
+    B = 200
+    st, oi, ow, op = P.o.sample(oracle.PRIORITIZED if strat == "prioritized" else oracle.FIFO,
+                                1, 0, B, 77, 0.4)
+    assert st == 0
+    pin = [torch.empty(B, dtype=d).pin_memory() for d in (torch.int64, torch.float32,
+                                                          torch.float64, torch.int32)]
+    G.gear_sample(P.t.handle, S, B, 77, 0.4, *pin)
+    torch.cuda.synchronize()
+    pag = [np.empty(B, np.uint64), np.empty(B, np.float32), np.empty(B, np.float64),
+           np.empty(B, np.uint32)]
+    G.gear_sample(P.t.handle, S, B, 77, 0.4, *pag)
+    torch.cuda.synchronize()
+    for out in (pin, pag):
+        idx = out[0].numpy().view(np.uint64) if hasattr(out[0], "numpy") else out[0]
+        w = out[1].numpy() if hasattr(out[1], "numpy") else out[1]
+        p = out[2].numpy() if hasattr(out[2], "numpy") else out[2]
+        assert np.array_equal(idx, oi)
+        np.testing.assert_allclose(w, ow, rtol=1e-6, atol=0)
+        assert np.array_equal(p, op)
+    assert P.t.sync()[0] == 0
+    P.close()
