@@ -672,13 +672,10 @@ gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* c
                                  t->d_ord, t->d_out, t->err, s));
     const uint32_t n_meta = m, n_ord = m;  // rows a later row overrides are skipped
     // Row sources: device / pinned host are read in place; pageable host is
-    // staged into device memory first.
-    ScatterParams sp{};
-    sp.meta = t->d_meta;
-    sp.ncols = (uint32_t)t->cols.size();
-    sp.m = n_meta;
-    sp.chunk_bytes = t->chunk_bytes;
-    uint64_t chunks = 0, stage_off = 0, stage_need = 0;
+    // staged into device memory first.  The rows move with the collect
+    // engine in scatter mode (source row -> table slot): TMA bulk copies for
+    // 16-byte aligned rows of >= 4 KB, warp LSU copies otherwise.
+    uint64_t stage_off = 0, stage_need = 0;
     for (size_t c = 0; c < t->cols.size(); ++c)
       if (kinds[c] == MemKind::HostPageable) stage_need += (uint64_t)m * t->cols[c].rb;
     if (stage_need > t->d_rows_bytes) {
@@ -686,11 +683,24 @@ gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* c
       GEAR_TRY(dalloc(&t->d_rows, stage_need));
       t->d_rows_bytes = stage_need;
     }
+    CollectParams cp{};
+    cp.meta = t->d_meta;
+    cp.rows_per_rank = t->Clocal;
+    cp.n_global = t->N;
+    cp.ncols = (uint32_t)t->cols.size();
+    cp.n = n_meta;
+    cp.err = t->err;
+    cp.row_mult = 1;
+    cp.self_rank = t->rank;
+    cp.tma_ctas_per_sm = (uint32_t)t->tma_ctas;
+    cp.tma_stages = (uint32_t)t->tma_stages;
+    cp.tma_ooo = (uint32_t)t->tma_ooo;
     for (size_t c = 0; c < t->cols.size(); ++c) {
       ColumnState& cs = t->cols[c];
       const uint8_t* src = (const uint8_t*)col_src[c] + (uint64_t)k0 * cs.rb;
       if (kinds[c] == MemKind::HostPageable) {
-        GEAR_CUDA(cudaMemcpyAsync(t->d_rows + stage_off, src, (uint64_t)m * cs.rb, cudaMemcpyHostToDevice, s));
+        GEAR_CUDA(cudaMemcpyAsync(t->d_rows + stage_off, src, (uint64_t)m * cs.rb,
+                                  cudaMemcpyHostToDevice, s));
         src = t->d_rows + stage_off;
         stage_off += (uint64_t)m * cs.rb;
       } else if (kinds[c] == MemKind::HostPinned) {
@@ -698,18 +708,26 @@ gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* c
         GEAR_CUDA(cudaHostGetDevicePointer(&dp, (void*)src, 0));
         src = (const uint8_t*)dp;
       }
-      uint8_t* dst = (uint8_t*)cs.view[t->rank];
-      ScatterCol& sc = sp.col[c];
-      sc.dst = dst;
-      sc.src = src;
-      sc.rb = cs.rb;
-      sc.chunks_per_row = (uint32_t)((cs.rb + t->chunk_bytes - 1) / t->chunk_bytes);
-      sc.chunk_begin = chunks;
-      sc.vec = vec_width(cs.rb, t->chunk_bytes, {(uintptr_t)dst, (uintptr_t)src});
-      chunks += (uint64_t)n_meta * sc.chunks_per_row;
+      CollectCol& cc = cp.col[c];
+      cc.out = (uint8_t*)cs.view[t->rank];  // the table column (destination)
+      cc.src[0] = src;                      // the caller's rows (source)
+      cc.rb = cs.rb;
+      cc.vec = vec_width(cs.rb, 512, {(uintptr_t)cc.out | (uintptr_t)src});
+      cc.tma = (t->collect_impl == 1 && cc.vec == 16 && cs.rb >= 4096) ? 1u : 0u;
+      cc.chunk = cc.tma ? t->tma_chunk : t->chunk_bytes;
+      if (cc.vec < 16 && cc.chunk % cc.vec) cc.chunk = t->chunk_bytes;
+      cc.chunks_per_row = (uint32_t)((cs.rb + cc.chunk - 1) / cc.chunk);
+      if (cc.tma) {
+        cc.chunk_begin = cp.tma_total;
+        cp.tma_total += (uint64_t)n_meta * cc.chunks_per_row;
+        cp.tma_cols[cp.n_tma++] = (uint8_t)c;
+      } else {
+        cc.chunk_begin = cp.lsu_total;
+        cp.lsu_total += (uint64_t)n_meta * cc.chunks_per_row;
+        cp.lsu_cols[cp.n_lsu++] = (uint8_t)c;
+      }
     }
-    sp.total_chunks = chunks;
-    GEAR_CUDA(launch_scatter(sp, s));
+    GEAR_CUDA(launch_collect(cp, s));
     GEAR_CUDA(launch_insert_meta(t->d_meta, n_meta, t->d_ord, n_ord, quant(t), t->key,
                                  tile_dirty(t), t->seq, t->gen, t->ord, s));
     if (out_idx) {

@@ -170,6 +170,9 @@ struct CollectCol {
 struct CollectParams {
   CollectCol col[kMaxCols];
   const uint64_t* idx;                // [n] global ids (device)
+  const InsMeta* meta;                // non-null: insert scatter -- row j of the source
+                                      // (col.src[0], row meta[j].src_row) goes to table slot
+                                      // meta[j].local of col.out; kIdxNone rows are skipped
   uint64_t rows_per_rank;             // R * C_s
   uint64_t n_global;                  // N
   uint64_t lsu_total;                 // tasks of the LSU (warp-copy) space

@@ -102,6 +102,16 @@ __device__ __forceinline__ void collect_lsu(const CollectParams& p, uint64_t war
     uint64_t j, k;
     decode_task(p, p.lsu_cols, p.n_lsu, task, &c, &j, &k);
     const CollectCol& col = p.col[c];
+    const uint64_t off = k * (uint64_t)col.chunk;
+    const uint64_t rem = col.rb - off;
+    const uint64_t bytes = rem < col.chunk ? rem : col.chunk;
+    if (p.meta) {  // insert scatter: source row -> table slot
+      const uint64_t local = p.meta[j].local;
+      if (local == kIdxNone) continue;
+      copy_dispatch(col.vec, col.out + local * col.rb + off,
+                    col.src[0] + (uint64_t)p.meta[j].src_row * col.rb + off, bytes, lane);
+      continue;
+    }
     const uint64_t g = __ldg(p.idx + j);
     if (g >= p.n_global) {
       if (lane == 0 && k == 0) atomicOr(p.err, kErrIndexRange);
@@ -109,9 +119,6 @@ __device__ __forceinline__ void collect_lsu(const CollectParams& p, uint64_t war
     }
     const uint64_t owner = g / p.rows_per_rank;
     const uint64_t local = g - owner * p.rows_per_rank;
-    const uint64_t off = k * (uint64_t)col.chunk;
-    const uint64_t rem = col.rb - off;
-    const uint64_t bytes = rem < col.chunk ? rem : col.chunk;
     copy_dispatch(col.vec, col.out + j * col.rb + off, col.src[owner] + local * col.rb + off,
                   bytes, lane);
   }
@@ -181,6 +188,25 @@ __device__ __forceinline__ uint32_t tma_issue_load(const CollectParams& p, uint6
   uint64_t j, k;
   decode_task(p, p.tma_cols, p.n_tma, task, &c, &j, &k);
   const CollectCol& col = p.col[c];
+  if (p.meta) {  // insert scatter: source row -> table slot
+    const uint64_t local = p.meta[j].local;
+    if (local == kIdxNone) {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+      return 0;
+    }
+    const uint64_t off = k * (uint64_t)col.chunk;
+    const uint64_t rem = col.rb - off;
+    const uint32_t bytes = (uint32_t)(rem < col.chunk ? rem : col.chunk);
+    *dst = col.out + local * col.rb + off;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            stage_addr),
+        "l"(col.src[0] + (uint64_t)p.meta[j].src_row * col.rb + off), "r"(bytes), "r"(bar)
+        : "memory");
+    return bytes;
+  }
   const uint64_t g = __ldg(p.idx + j);
   if (g >= p.n_global) {
     if (k == 0) atomicOr(p.err, kErrIndexRange);
