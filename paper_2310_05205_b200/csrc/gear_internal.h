@@ -192,25 +192,6 @@ struct CollectParams {
   uint32_t* err;
 };
 
-// Insert-side row scatter: dst row slot[j] <- src row src_row[j].
-struct ScatterCol {
-  uint8_t* dst;
-  const uint8_t* src;
-  uint64_t rb;
-  uint64_t chunk_begin;
-  uint32_t chunks_per_row;
-  uint32_t vec;
-};
-
-struct ScatterParams {
-  ScatterCol col[kMaxCols];
-  const InsMeta* meta;                // [m]
-  uint64_t total_chunks;
-  uint32_t ncols;
-  uint32_t m;
-  uint32_t chunk_bytes;
-};
-
 struct SampleParams {
   const ShardTotals* totals;          // [S] (ignored when xchg: taken from the mailbox)
   const ShardTotals* totals_local;    // [R] this rank's totals (xchg)
@@ -340,7 +321,6 @@ cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_i
 
 // K5: collect (gather) and the insert-side scatter.
 cudaError_t launch_collect(const CollectParams& p, cudaStream_t s);
-cudaError_t launch_scatter(const ScatterParams& p, cudaStream_t s);
 cudaError_t launch_insert_meta(const InsMeta* meta, uint32_t m, const OrdRec* ord_recs,
                                uint32_t n_ord, Quant qz,
                                uint64_t* key, TileDirty td, uint64_t* seq, uint32_t* gen,

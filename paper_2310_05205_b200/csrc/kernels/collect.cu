@@ -1,5 +1,6 @@
 // collect.cu -- K5: gather the selected rows of several columns into
-// contiguous batches, and the insert-side scatter.
+// contiguous batches; the same engine in scatter mode
+// (CollectParams::meta) writes inserted rows into their table slots.
 //
 // The paper launches "one CUDA kernel per table" that reads pinned host
 // memory zero-copy; here ONE launch covers every requested
@@ -361,27 +362,6 @@ __global__ void __launch_bounds__(kTmaThreads)
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(kThreads) scatter_kernel(const __grid_constant__ ScatterParams p) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const uint64_t nwarps = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t task = warp0; task < p.total_chunks; task += nwarps) {
-    uint32_t c = 0;
-    while (c + 1 < p.ncols && task >= p.col[c + 1].chunk_begin) ++c;
-    const ScatterCol& col = p.col[c];
-    const uint64_t rel = task - col.chunk_begin;
-    const uint64_t j = rel / col.chunks_per_row;
-    const uint64_t k = rel - j * col.chunks_per_row;
-    const InsMeta m = p.meta[j];
-    if (m.local == kIdxNone) continue;  // a later row of the call owns this slot
-    const uint64_t off = k * (uint64_t)p.chunk_bytes;
-    const uint64_t rem = col.rb - off;
-    const uint64_t bytes = rem < p.chunk_bytes ? rem : p.chunk_bytes;
-    copy_dispatch(col.vec, col.dst + m.local * col.rb + off,
-                  col.src + (uint64_t)m.src_row * col.rb + off, bytes, lane);
-  }
-}
-
 __global__ void __launch_bounds__(kThreads)
     insert_meta_kernel(const InsMeta* __restrict__ meta, uint32_t m,
                        const OrdRec* __restrict__ ord_recs, uint32_t n_ord, Quant qz,
@@ -456,13 +436,6 @@ cudaError_t launch_collect(const CollectParams& p, cudaStream_t s) {
   }
   const int ctas = (int)p.tma_ctas_per_sm;
   return p.tma_ooo ? launch_tma_stages<true>(p, ctas, s) : launch_tma_stages<false>(p, ctas, s);
-}
-
-cudaError_t launch_scatter(const ScatterParams& p, cudaStream_t s) {
-  if (p.total_chunks == 0) return cudaSuccess;
-  count_launch();
-  scatter_kernel<<<grid_for(scatter_kernel, p.total_chunks), kThreads, 0, s>>>(p);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_insert_meta(const InsMeta* meta, uint32_t m, const OrdRec* ord_recs,
