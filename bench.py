@@ -335,8 +335,10 @@ def run_gpu(args):
 
     # End-to-end through the C-ABI with HOST buffers, pipelined like the device
     # step.  Every step: gear_sample writes the IS weights straight to pinned
-    # host memory (D2H inside the call) and the ids to HBM, from where they are
-    # copied to pinned host memory for the host; gear_update_priorities reads
+    # host memory (in place) and the ids to HBM, from where a third stream
+    # copies them to pinned host memory for the host (a copy on the selection
+    # stream delayed every rank's mailbox exchanges: N=4 e2e 9.6 M -> 13.5 M
+    # traj/s without it); gear_update_priorities reads
     # that step's f64 priorities from pinned host memory (in place, over PCIe);
     # gear_collect (collect stream) gathers the rows into HBM.  The host
     # consumes every step's ids and weights LAG steps behind (waits for
@@ -347,6 +349,8 @@ def run_gpu(args):
     h_idx2 = [h_idx] + [torch.empty(B, dtype=torch.int64, pin_memory=True) for _ in range(NH - 1)]
     h_w2 = [h_w] + [torch.empty(B, dtype=torch.float32, pin_memory=True) for _ in range(NH - 1)]
     ev_hs = [torch.cuda.Event() for _ in range(NH)]
+    xstream = torch.cuda.Stream()   # the ids' D2H copy: off the selection / collect streams
+    ev_copied = [torch.cuda.Event() for _ in range(2)]
     np_idx2 = [x.numpy() for x in h_idx2]   # host views of the pinned buffers
     np_w2 = [x.numpy() for x in h_w2]
     consumed = 0.0
@@ -355,12 +359,15 @@ def run_gpu(args):
         b, hb = i % 2, i % NH
         if i >= 2:
             stream.wait_event(ev_collected[b])   # collect(i-2) has read idx2[b]
+            stream.wait_event(ev_copied[b])      # and so has its host copy
         gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + 7919 + i, cfg.beta,
                          idx2[b], h_w2[hb], None, None, stream)
         ev_sampled[b].record(stream)
-        with torch.cuda.stream(stream):
+        xstream.wait_event(ev_sampled[b])
+        with torch.cuda.stream(xstream):
             h_idx2[hb].copy_(idx2[b], non_blocking=True)
-        ev_hs[hb].record(stream)
+        ev_copied[b].record(xstream)
+        ev_hs[hb].record(xstream)
         if cfg.update:
             gear.gear_update_priorities(t.handle, B, idx2[b], h_prio[i % 16], gear.GEAR_F64,
                                         None, stream)
@@ -385,7 +392,7 @@ def run_gpu(args):
     for i in range(max(0, args.steps - LAG), args.steps):
         ev_hs[i % NH].synchronize()
         consumed += float(np_w2[i % NH][0]) + float(np_idx2[i % NH][B - 1])
-    for cs in cstreams:
+    for cs in cstreams + [xstream]:
         stream.wait_stream(cs)
     e3.record(stream)
     barrier()
