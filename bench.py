@@ -167,6 +167,10 @@ def run_gpu(args):
     strategy = gear.STRATEGIES[cfg.strategy]
     if args.assign == "owner":
         strategy |= gear.GEAR_SAMPLE_OWNER_AFFINE
+        if world > 1 and "GEAR_COLLECT_PEER_LSU" not in os.environ:
+            # the application knows its batches are ~95% local: the few peer
+            # rows go through the LSU warps (profiles/r01m, r01n: +1.7% at N=4)
+            gear.gear_table_set_tuning(t.handle, "collect_peer_lsu", 1)
     B = cfg.batch
     ncols = len(t.row_bytes)
     col_ids = list(range(ncols))
