@@ -270,6 +270,10 @@ def run_gpu(args):
         err, _ = t.sync()
         assert err == 0, f"device error bits {err} in the timed region"
         coll = float(np.mean([a.elapsed_time(b) for a, b in zip(*ev)]))
+        # per-step distribution: intervals between consecutive collect ends
+        iv = [ev[1][i - 1].elapsed_time(ev[1][i]) for i in range(1, args.steps)]
+        pct = ({f"p{q}": float(np.percentile(iv, q)) for q in (10, 50, 90)} if iv else {})
+        timed.percentiles = pct
         return e0.elapsed_time(e1), coll, launches, clk
 
     def timed_graph():
@@ -322,6 +326,7 @@ def run_gpu(args):
         return e0.elapsed_time(e1), per_graph * (args.steps // S), S
 
     ms, coll_ms_p, launches, clk = timed(step_pipe)
+    step_pct = dict(timed.percentiles)
     ms_serial, coll_ms_s, _, clk_s = timed(step_serial)
     graph = None
     if args.graph:
@@ -471,6 +476,8 @@ def run_gpu(args):
         "serial": {"value": traj / (ms_serial / 1e3), "ms_per_step": ms_serial / args.steps,
                    "collect_avg_ms": coll_serial,
                    "note": "sample -> collect -> update on one stream, same K steps"},
+        "step_ms_percentiles": {**step_pct, "from": ("eager pipelined run, rank 0: intervals "
+                                                     "between consecutive collect completions")},
         "roofline": roof,
         "e2e": {"value": traj / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": e2e_h2d,
                 "d2h_bytes_per_step": e2e_d2h,

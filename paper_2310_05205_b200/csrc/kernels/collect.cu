@@ -130,6 +130,13 @@ __global__ void __launch_bounds__(kThreads) collect_kernel(const __grid_constant
   collect_lsu(p, warp0, (uint64_t)gridDim.x * kWarps, threadIdx.x & 31);
 }
 
+// The same engine in scatter mode (gear_insert), under its own name so that
+// profiles tell the writer's launches from the collector's.
+__global__ void __launch_bounds__(kThreads) insert_rows_kernel(const __grid_constant__ CollectParams p) {
+  const uint64_t warp0 = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  collect_lsu(p, warp0, (uint64_t)gridDim.x * kWarps, threadIdx.x & 31);
+}
+
 // ---- TMA bulk-copy variant -------------------------------------------------
 // One CTA per SM.  Lane 0 of warp 0 runs a kStages-deep ring of shared-memory
 // stages: cp.async.bulk global->shared completes on the stage's mbarrier,
@@ -312,8 +319,7 @@ __device__ __forceinline__ void tma_lane_ooo(const CollectParams& p, uint32_t ba
 }
 
 template <int kStages, bool kOoo>
-__global__ void __launch_bounds__(kTmaThreads)
-    collect_tma_kernel(const __grid_constant__ CollectParams p, uint32_t stage_bytes) {
+__device__ __forceinline__ void tma_body(const CollectParams& p, uint32_t stage_bytes) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[kStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -393,6 +399,18 @@ int grid_for(K kernel, uint64_t tasks) {
   return (int)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
+template <int kStages, bool kOoo>
+__global__ void __launch_bounds__(kTmaThreads)
+    collect_tma_kernel(const __grid_constant__ CollectParams p, uint32_t stage_bytes) {
+  tma_body<kStages, kOoo>(p, stage_bytes);
+}
+
+template <int kStages, bool kOoo>
+__global__ void __launch_bounds__(kTmaThreads)
+    insert_rows_tma_kernel(const __grid_constant__ CollectParams p, uint32_t stage_bytes) {
+  tma_body<kStages, kOoo>(p, stage_bytes);
+}
+
 }  // namespace
 
 // kStages stages of tma_chunk bytes per CTA, ctas CTAs per SM (192 KB of
@@ -401,18 +419,20 @@ template <int kStages, bool kOoo>
 cudaError_t launch_tma(const CollectParams& p, int ctas, cudaStream_t s) {
   const uint32_t stage_bytes = p.col[p.tma_cols[0]].chunk;
   const size_t smem = (size_t)kStages * stage_bytes;
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(collect_tma_kernel<kStages, kOoo>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = p.meta ? insert_rows_tma_kernel<kStages, kOoo> : collect_tma_kernel<kStages, kOoo>;
+  static size_t configured[2] = {0, 0};
+  size_t& conf = configured[p.meta ? 1 : 0];
+  if (smem > conf) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
+    conf = smem;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   count_launch();
-  collect_tma_kernel<kStages, kOoo><<<sms * ctas, kTmaThreads, smem, s>>>(p, stage_bytes);
+  kern<<<sms * ctas, kTmaThreads, smem, s>>>(p, stage_bytes);
   return cudaGetLastError();
 }
 
@@ -431,7 +451,10 @@ cudaError_t launch_collect(const CollectParams& p, cudaStream_t s) {
   if (p.lsu_total + p.tma_total == 0) return cudaSuccess;
   if (p.tma_total == 0) {
     count_launch();
-    collect_kernel<<<grid_for(collect_kernel, p.lsu_total), kThreads, 0, s>>>(p);
+    if (p.meta)
+      insert_rows_kernel<<<grid_for(insert_rows_kernel, p.lsu_total), kThreads, 0, s>>>(p);
+    else
+      collect_kernel<<<grid_for(collect_kernel, p.lsu_total), kThreads, 0, s>>>(p);
     return cudaGetLastError();
   }
   const int ctas = (int)p.tma_ctas_per_sm;
