@@ -1,11 +1,10 @@
 // api.cpp -- the C-ABI of include/gear.h: argument validation, table memory,
 // peer mappings and the orchestration of the sm_100a kernels.
 //
-// Every step of the hot path runs on the GPU: this file only validates,
-// allocates, stages small host arrays and enqueues kernels / NCCL calls on the
-// caller's stream.  The only host-side algorithm is the per-shard ring
-// allocator of gear_insert, which the paper also keeps in
-// the host-resident index manager.
+// Every step of the hot path runs on the GPU, the block allocator of the
+// writers included (kernels/alloc.cu): this file only validates, allocates,
+// stages small host arrays and enqueues kernels / NCCL calls on the caller's
+// stream.
 #include <fcntl.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
@@ -17,7 +16,6 @@
 #include <cstring>
 #include <numeric>
 #include <random>
-#include <unordered_map>
 
 #include "runtime.h"
 
