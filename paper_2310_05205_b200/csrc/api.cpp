@@ -861,7 +861,7 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
     // the FIFO-exchange epoch advances after the merge (and assignment)
     mb.epoch_dev = t->d_xep + 2;
     if (topk)
-      GEAR_CUDA(launch_topk_local(t->key, t->Cs, t->R, t->rank * t->R, K, t->topk_tmp,
+      GEAR_CUDA(launch_topk_local(t->key, t->Cs, t->qmax, t->R, t->rank * t->R, K, t->topk_tmp,
                                   t->cand_local,
                                   t->fifo_totals_local, t->topk_state, t->topk_cnt,
                                   xchg ? &mb : nullptr, s));

@@ -364,7 +364,8 @@ cudaError_t launch_assign(const AssignParams& p, cudaStream_t s);
 // TopK local selection (kernels/topk.cu): sorted top-K of each local shard;
 // merged by launch_fifo_merge with lifo == 2.  K <= topk_max_k().
 uint32_t topk_max_k();
-cudaError_t launch_topk_local(const uint64_t* key, uint64_t shard_cap, uint32_t n_shards_local,
+cudaError_t launch_topk_local(const uint64_t* key, uint64_t shard_cap, uint64_t q_max,
+                              uint32_t n_shards_local,
                               uint32_t first_shard, uint32_t K, Cand* cand_tmp, Cand* cand_out,
                               ShardTotals* totals_out, TopkState* state, uint32_t* cnt,
                               const Mbox* mbox, cudaStream_t s);

@@ -362,7 +362,8 @@ __global__ void __launch_bounds__(kSortThreads)
 
 uint32_t topk_max_k() { return 8192; }
 
-cudaError_t launch_topk_local(const uint64_t* key, uint64_t shard_cap, uint32_t n_shards_local,
+cudaError_t launch_topk_local(const uint64_t* key, uint64_t shard_cap, uint64_t q_max,
+                              uint32_t n_shards_local,
                               uint32_t first_shard, uint32_t K, Cand* cand_tmp, Cand* cand_out,
                               ShardTotals* totals_out, TopkState* state, uint32_t* cnt,
                               const Mbox* mbox, cudaStream_t s) {
@@ -376,9 +377,13 @@ cudaError_t launch_topk_local(const uint64_t* key, uint64_t shard_cap, uint32_t 
   G = (uint64_t)G > max_g ? (uint32_t)max_g : G;
   G = G > kTopkMaxCtas ? kTopkMaxCtas : G;
   const dim3 grid(G, n_shards_local);
-  count_launch(12);
+  // Every key is <= q_max: the select never needs more passes than q_max has
+  // bytes (6 at c2); the passes after an early exit are no-op launches.
+  int passes = 1;
+  while (passes < 8 && (q_max >> (8 * passes)) != 0) ++passes;
+  count_launch(4 + passes);
   stats_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, K, state);
-  for (int pass = 0; pass < 8; ++pass)  // one per key byte; no-ops once selected
+  for (int pass = 0; pass < passes; ++pass)  // one per key byte from the top
     hist_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, state);
   count_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, state, cnt);
   write_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, K, first_shard, state, cnt, cand_tmp,

@@ -15,4 +15,7 @@ run --config c2 --assign contiguous > $out/bench_c2_contig.json; echo "bench c2 
 run --config c3 > $out/bench_c3.json; echo "bench c3 exit $?"
 run --config c4 > $out/bench_c4.json; echo "bench c4 exit $?"
 run --config c4 --strategy fifo > $out/bench_c4_fifo.json; echo "bench c4 fifo exit $?"
+run --config c2 --strategy topk > $out/bench_c2_topk.json; echo "bench c2 topk exit $?"
+run --config c2 --strategy fifo > $out/bench_c2_fifo.json; echo "bench c2 fifo exit $?"
 run --config c5 > $out/bench_c5.json; echo "bench c5 exit $?"
+run --impl reference --steps 3 --warmup 3 > $out/bench_reference.json; echo "reference exit $?"
