@@ -350,6 +350,9 @@ gear_status gear_table_load(gear_table* t, const char* path);
  *   "update_fused": 1 = priority updates of <= 8192 entries (all ranks) run
  *                   tag + apply in one single-CTA launch (default), 0 = two
  *                   grid-wide launches;
+ *   "collect_dynamic": 1 = the bulk pipeline claims its tasks from a counter
+ *                   (dynamic load balance) instead of a static stride
+ *                   (measured 1-3% slower; default 0);
  *   "tma_ooo":      1 = the bulk pipeline stores its stages in completion
  *                   order instead of ring order (measured 2% slower at c2;
  *                   default 0);

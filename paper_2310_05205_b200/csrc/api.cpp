@@ -168,7 +168,7 @@ void destroy_table(gear_table* t) {
   dfree(t->n_stale); dfree(t->err); dfree(t->d_epoch); dfree(t->d_seed); dfree(t->d_xep);
   dfree(t->col_idx.p);
   dfree(t->d_meta); dfree(t->d_ord); dfree(t->d_out); dfree(t->d_rows);
-  dfree(t->d_prio_ins); dfree(t->d_alloc); dfree(t->ins_bad);
+  dfree(t->d_prio_ins); dfree(t->d_alloc); dfree(t->ins_bad); dfree(t->dyn_pool);
   if (t->h_prio) cudaFreeHost(t->h_prio);
   if (t->h_out) cudaFreeHost(t->h_out);
   if (t->staging_ev) cudaEventDestroy(t->staging_ev);
@@ -214,6 +214,7 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   if (const char* e = getenv("GEAR_COLLECT_PERMUTE")) t->collect_permute = atoi(e) != 0;
   if (const char* e = getenv("GEAR_COLLECT_PEER_LSU")) t->collect_peer_lsu = atoi(e) != 0;
   if (const char* e = getenv("GEAR_TMA_OOO")) t->tma_ooo = atoi(e) != 0;
+  if (const char* e = getenv("GEAR_COLLECT_DYNAMIC")) t->collect_dynamic = atoi(e) != 0;
   if (const char* e = getenv("GEAR_TMA_STAGES")) {
     const int v = atoi(e);
     if (v == 2 || v == 3 || v == 4 || v == 6 || v == 8) t->tma_stages = v;
@@ -455,6 +456,8 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_TRY(dalloc(&t->d_prio_ins, MB));
   GEAR_TRY(dalloc(&t->d_alloc, t->R));
   GEAR_TRY(dalloc(&t->ins_bad, 1));
+  GEAR_TRY(dalloc(&t->dyn_pool, 2 * gear_table::kDynSlots));
+  GEAR_CUDA(cudaMemset(t->dyn_pool, 0, 2 * gear_table::kDynSlots * 8));
   GEAR_CUDA(cudaMemset(t->ins_bad, 0, 4));
   {
     std::vector<AllocState> a0(t->R);
@@ -1068,6 +1071,9 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
     cp.row_mult = m;
   }
   cp.self_rank = t->rank;
+  if (t->collect_dynamic) {  // a counter pair per launch, rotating (concurrent collects differ)
+    cp.dyn_ctr = t->dyn_pool + 2 * (t->dyn_slot++ % gear_table::kDynSlots);
+  }
   cp.tma_ctas_per_sm = (uint32_t)t->tma_ctas;
   cp.tma_stages = (uint32_t)t->tma_stages;
   cp.tma_ooo = (uint32_t)t->tma_ooo;
@@ -1143,6 +1149,8 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     GEAR_CUDA(cudaMemset(t->cdf_buf_mode, 0, 8));  // both buffers: full rebuild
     t->cdf_levels = (int)value;
     t->dirty = true;
+  } else if (!strcmp(key, "collect_dynamic") && (value == 0 || value == 1)) {
+    t->collect_dynamic = (int)value;
   } else if (!strcmp(key, "tma_ooo") && (value == 0 || value == 1)) {
     t->tma_ooo = (int)value;
   } else if (!strcmp(key, "collect_peer_lsu") && (value == 0 || value == 1)) {

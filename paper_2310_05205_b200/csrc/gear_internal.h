@@ -184,6 +184,7 @@ struct CollectParams {
   uint32_t tma_ctas_per_sm;           // CTAs of the TMA kernel per SM
   uint32_t tma_stages;                // 2, 3, 4, 6 or 8 shared-memory stages per CTA
   uint32_t tma_ooo;                   // 1: stages stored in completion order
+  unsigned long long* dyn_ctr;        // non-null: TMA tasks claimed from this counter pair
   uint32_t ncols;
   uint32_t n;
   uint64_t row_mult;                  // row visiting order j -> j*row_mult mod n (1: in order)

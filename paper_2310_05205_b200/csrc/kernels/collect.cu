@@ -318,6 +318,61 @@ __device__ __forceinline__ void tma_lane_ooo(const CollectParams& p, uint32_t ba
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Dynamic variant of the issuing lane's in-order ring: each refill claims the
+// next task from a per-launch counter instead of the static stride, so CTAs
+// slowed by co-resident kernels (the next step's selection) or by slow chunks
+// take fewer tasks.  The last CTA to finish re-arms the counter (graph-safe).
+template <int kStages>
+__device__ __forceinline__ void tma_lane_dynamic(const CollectParams& p, uint32_t base,
+                                                 uint64_t* bars, uint32_t stage_bytes) {
+  unsigned long long* ctr = p.dyn_ctr;  // [0] next task, [1] CTAs done
+  uint8_t* dst[kStages] = {};
+  uint32_t nbytes[kStages] = {};
+  uint32_t phase = 0;
+  int inflight = 0;
+  bool more = true;
+  for (int s = 0; s < kStages; ++s) {
+    const uint64_t task = atomicAdd(ctr, 1ull);
+    if (task >= p.tma_total) {
+      more = false;
+      break;
+    }
+    nbytes[s] = tma_issue_load(p, task, base + (uint32_t)s * stage_bytes, smem_u32(&bars[s]),
+                               &dst[s]);
+    ++inflight;
+  }
+  for (uint64_t n = 0; inflight > 0; ++n) {
+    const int s = (int)(n % kStages);
+    while (!mbar_try_wait(smem_u32(&bars[s]), (phase >> s) & 1u)) {
+    }
+    phase ^= 1u << s;
+    --inflight;
+    if (nbytes[s])
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst[s]),
+                   "r"(base + (uint32_t)s * stage_bytes), "r"(nbytes[s])
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (n >= 1 && more) {  // refill the previous stage (cyclic order is kept)
+      const int sp = (int)((n - 1) % kStages);
+      const uint64_t task = atomicAdd(ctr, 1ull);
+      if (task < p.tma_total) {
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        nbytes[sp] = tma_issue_load(p, task, base + (uint32_t)sp * stage_bytes,
+                                    smem_u32(&bars[sp]), &dst[sp]);
+        ++inflight;
+      } else {
+        more = false;
+      }
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __threadfence();
+  if (atomicAdd(ctr + 1, 1ull) == gridDim.x - 1) {  // every CTA has stopped claiming
+    ctr[0] = 0;
+    ctr[1] = 0;
+  }
+}
+
 template <int kStages, bool kOoo>
 __device__ __forceinline__ void tma_body(const CollectParams& p, uint32_t stage_bytes) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -337,6 +392,10 @@ __device__ __forceinline__ void tma_body(const CollectParams& p, uint32_t stage_
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if constexpr (kOoo) {
     tma_lane_ooo<kStages>(p, smem_u32(smem), bars, stage_bytes);
+    return;
+  }
+  if (p.dyn_ctr != nullptr) {  // tuning "collect_dynamic": tasks claimed from a counter
+    tma_lane_dynamic<kStages>(p, smem_u32(smem), bars, stage_bytes);
     return;
   }
   const uint64_t first = blockIdx.x, step = gridDim.x;

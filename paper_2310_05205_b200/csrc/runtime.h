@@ -178,6 +178,10 @@ struct gear_table {
   int tma_stages = 3;               // shared-memory stages per TMA CTA
   int collect_impl = 1;             // 1: TMA bulk copies for large aligned rows, 0: LSU only
   int tma_ooo = 0;                  // TMA ring stored in completion order
+  int collect_dynamic = 0;          // TMA tasks claimed from a counter
+  static constexpr uint32_t kDynSlots = 8;
+  unsigned long long* dyn_pool = nullptr;  // [kDynSlots][2] task counters
+  uint64_t dyn_slot = 0;
   int collect_peer_lsu = 0;         // W > 1: peer-HBM rows of TMA columns via LSU warps
   int collect_permute = 0;          // visit rows in a coprime-stride order (measured slower)
 };
