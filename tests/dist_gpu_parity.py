@@ -29,6 +29,23 @@ OS = {gear.GEAR_FIFO: oracle.FIFO, gear.GEAR_LIFO: oracle.LIFO, gear.GEAR_UNIFOR
       gear.GEAR_TOPK: oracle.TOPK}
 
 
+def write_rows_in_place(t, c, placement, local, rows, nrows, rb):
+    """Rows of rank-local slots `local` of column c, written at gear_column_base."""
+    import ctypes
+    base = t.column_base(c)
+    if placement == gear.GEAR_DEVICE:
+        class _View:
+            __cuda_array_interface__ = {"shape": (nrows, rb), "typestr": "|u1",
+                                        "data": (base, False), "version": 3}
+        col = torch.as_tensor(_View(), device="cuda")
+        col[torch.from_numpy(local).cuda()] = torch.from_numpy(rows).cuda()
+    else:
+        col = np.ctypeslib.as_array(ctypes.cast(base, ctypes.POINTER(ctypes.c_uint8)),
+                                    shape=(nrows, rb))
+        col[local] = rows
+    torch.cuda.synchronize()
+
+
 def run_case(comm, W, rank, R, placements, removal, Cs=700, B=40, steps=3, xchg=1):
     dt = [gear.GEAR_F32, gear.GEAR_U8, gear.GEAR_I32]
     shapes = [(5,), (3,), ()]
@@ -64,6 +81,36 @@ def run_case(comm, W, rank, R, placements, removal, Cs=700, B=40, steps=3, xchg=
     dist.barrier()
     key, seq, gen = t.read_state()
     lo, hi = rank * R * Cs, (rank + 1) * R * Cs
+    assert np.array_equal(key, o.key[lo:hi]) and np.array_equal(seq, o.seq[lo:hi])
+    assert np.array_equal(gen, o.gen[lo:hi])
+
+    # split writer API (reading Q21): every rank allocates in its own shards,
+    # writes the rows in place at gear_column_base, then commits
+    for s in range(S):
+        n = 30
+        st, oids = o.allocate(s, n)
+        assert st == 0
+        traj = np.arange(10 ** 7 + 1000 * s, 10 ** 7 + 1000 * s + n)
+        content[oids.astype(np.int64)] = traj
+        pc = synth.priorities(n, seed=77 + s)
+        assert o.commit(s, oids, pc) == 0
+        if s // R != rank:
+            continue
+        ids = torch.empty(n, dtype=torch.int64, device="cuda")
+        t.allocate(s, n, ids)
+        torch.cuda.synchronize()
+        gids = ids.cpu().numpy().view(np.uint64)
+        assert np.array_equal(gids, oids), "allocated slots differ"
+        local = (gids - np.uint64(lo)).astype(np.int64)
+        for c in range(len(cols)):
+            rows = synth.row_bytes_of(c, traj, rb[c])
+            write_rows_in_place(t, c, placements[c], local, rows, R * Cs, rb[c])
+        t.commit(s, ids, torch.from_numpy(pc).cuda())
+    torch.cuda.synchronize()
+    dist.barrier()
+    err, _ = t.sync()
+    assert err == 0, err
+    key, seq, gen = t.read_state()
     assert np.array_equal(key, o.key[lo:hi]) and np.array_equal(seq, o.seq[lo:hi])
     assert np.array_equal(gen, o.gen[lo:hi])
 
