@@ -224,7 +224,12 @@ gear_status gear_column_row_bytes(const gear_table* t, uint32_t col, uint64_t* o
  * seq = the shard's next counter value (starting at 1), gen += 1, and
  * key = Q_F(prio[k]).
  *   col_src[c]: n rows of column c, [n][row_bytes_c], host or device.
- *   prio:       HOST array of n f64 priorities (0 = stored, not selectable).
+ *   prio:       n f64 priorities (0 = stored, not selectable), host or
+ *               device.  Host priorities are validated before anything is
+ *               inserted (BAD_PRIORITY returned); device priorities by a
+ *               kernel (GEAR_DEVERR_BAD_PRIORITY latched, nothing inserted),
+ *               so a call with device rows and priorities and a device (or
+ *               NULL) out_idx never blocks the host and can be captured.
  *   out_idx:    n u64 global ids (host or device), may be NULL.
  * Each row is allocated and committed before the next (victims are
  * committed slots only -- never ongoing ones of gear_allocate).  If two of
@@ -280,10 +285,13 @@ gear_status gear_column_base(const gear_table* t, uint32_t col, void** out);
  * prio_dtype (GEAR_F32 or GEAR_F64); gen: optional u32 generations (entries
  * whose generation differs from the slot's are skipped as stale, as are
  * never-inserted slots and allocated but uncommitted ones).  The
- * priority becomes key = Q_F(p): p == 0 -> 0 (not selectable), else
- * clamp(round_half_even(p * 2^F), 1, q_max).  Entries of all ranks are
- * applied in (rank, position) order -- the last writer wins.  Device-side
- * errors (id >= N, bad p, stale) skip the entry and are latched. */
+ * priority becomes key = Q_F(v), v = RN(p^alpha) (v = p for alpha 1):
+ * p == 0 -> 0 (not selectable), else clamp(round_half_even(v * 2^F), 1,
+ * q_max).  Entries of all ranks are applied in (rank, position) order -- the
+ * last writer wins.  idx / prio / gen may be device memory, pinned host
+ * memory (read in place by the kernel over PCIe) or pageable host memory
+ * (copied).  Device-side errors (id >= N, bad p, stale) skip the entry and
+ * are latched.  n <= max_batch. */
 gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* idx,
                                    const void* prio, gear_dtype prio_dtype, const uint32_t* gen,
                                    gear_stream stream);
@@ -299,8 +307,14 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
  *    smallest / largest (seq, shard), in that order.
  *  out_idx: u64[B] global ids (required).  out_w: f32[B] importance weights
  *  (PRIORITIZED: (q_min/q)^beta in f64 rounded to f32; otherwise 1).
- *  out_p: f64[B] selection probability q/T (FIFO/LIFO: 1).  out_gen: u32[B]
- *  generation of each selected slot.  Optional outputs may be NULL.
+ *  out_p: f64[B] selection probability q/T (FIFO/LIFO/TOPK: 1).  out_gen:
+ *  u32[B] generation of each selected slot.  Optional outputs may be NULL.
+ *  Outputs may be device memory or pinned host memory (written in place by
+ *  the kernels through the mapped address, stream-ordered) or pageable host
+ *  memory (copied at the end of the call).
+ *  TOPK: the W*B selectable trajectories with the largest keys, ties by the
+ *  smaller global id, in that order (reading Q20; W*B <= 8192).
+ *  Flags OR-ed into `strategy`: GEAR_SAMPLE_OWNER_AFFINE, GEAR_SAMPLE_DEVICE_SEED.
  *  Nothing selectable: outputs get GEAR_IDX_NONE and EMPTY is latched. */
 gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint64_t seed,
                         double beta, uint64_t* out_idx, float* out_w, double* out_p,
