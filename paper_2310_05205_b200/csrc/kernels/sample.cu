@@ -10,8 +10,10 @@
 //        each round the 32 lanes probe 32 evenly spaced pivots of the live
 //        range and a ballot keeps the first bin that can hold the answer, so
 //        a shard of C_s keys takes ceil(log32 C_s) dependent rounds instead
-//        of ceil(log2 C_s).  cdf_s may live in a peer GPU's HBM (read over
-//        NVLink through a CUDA-IPC mapping).
+//        of ceil(log2 C_s).  With the two-level CDF (default) the search runs
+//        first over the shard's tile prefixes, then inside the chosen tile.
+//        cdf_s may live in a peer GPU's HBM (read over NVLink through a
+//        CUDA-IPC mapping).
 //   g  = s*C_s + i,  q = cdf_s[i] - cdf_s[i-1]
 // The IS weights (q_min/q)^beta need the min over the whole slice; the last
 // block to finish (threadfence + counter) computes them and re-arms the
