@@ -19,6 +19,7 @@ launching stream, barrier + synchronize on both sides, max over ranks.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -111,6 +112,22 @@ def scaled_capacity(cfg, n_ranks: int) -> tuple[int, str]:
             note = f"capacity scaled {cfg.capacity} -> {N} to fit {int(frac * 100)}% of {mem >> 30} GiB host RAM"
     N -= N % n_ranks
     return N, note
+
+
+def _cudart():
+    """The CUDA runtime library (for cudaEventRecordWithFlags), or None."""
+    import glob
+    import torch
+    for path in sorted(glob.glob(os.path.join(os.path.dirname(torch.__file__), "lib",
+                                              "libcudart*.so*"))) + \
+            sorted(glob.glob("/usr/local/cuda/lib64/libcudart.so*")):
+        try:
+            lib = ctypes.CDLL(path)
+            lib.cudaEventRecordWithFlags.restype = ctypes.c_int
+            return lib
+        except OSError:
+            continue
+    return None
 
 
 def build_table(cfg, comm, n_ranks: int, rank: int, capacity: int, stream):
@@ -286,7 +303,22 @@ def run_gpu(args):
         gear.gear_table_set_tuning(t.handle, "device_seed", synth.SAMPLE_SEED_BASE + 100000)
         gstrat = strategy | gear.GEAR_SAMPLE_DEVICE_SEED
 
-        def gstep(i):
+        # timing events around every collect of the captured steps: each
+        # replay re-records them, so after the timed replays they hold the
+        # collect launch times of the last replay (the headline's kernels)
+        gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(S)]
+        for a, z in gev:  # create the events before capture
+            a.record(stream)
+            z.record(stream)
+        cudart = _cudart()
+
+        def rec(ev, st):  # an external event node: keeps its timing inside the graph
+            if cudart is None or cudart.cudaEventRecordWithFlags(
+                    ctypes.c_void_p(ev.cuda_event), ctypes.c_void_p(st.cuda_stream), 1) != 0:
+                raise RuntimeError("cudaEventRecordWithFlags(External) failed")
+
+        def gstep(i, timing=False):
             b = i % 2
             if i >= 2:
                 stream.wait_event(ev_collected[b])
@@ -297,7 +329,11 @@ def run_gpu(args):
                                             stream)
             cs = cstreams[b % len(cstreams)]
             cs.wait_event(ev_sampled[b])
+            if timing:
+                rec(gev[i][0], cs)
             gear.gear_collect(t.handle, B, idx2[b], col_ids, outs2[b % len(cstreams)], cs)
+            if timing:
+                rec(gev[i][1], cs)
             ev_collected[b].record(cs)
 
         for i in range(args.warmup):
@@ -311,6 +347,18 @@ def run_gpu(args):
             for cs in cstreams:
                 stream.wait_stream(cs)
         per_graph = gear.gear_kernel_launches() - l0
+        # a second capture of the same steps with timing events around each
+        # collect, replayed after the timed region: the collect launch time of
+        # the graph-replayed step (the events perturb the graph a little, so
+        # the headline is timed on the plain graph)
+        timing = cudart is not None
+        if timing:
+            gi = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gi, stream=stream, capture_error_mode="thread_local"):
+                for i in range(S):
+                    gstep(i, timing=True)
+                for cs in cstreams:
+                    stream.wait_stream(cs)
         barrier()
         with torch.cuda.stream(stream):  # replay() launches on the current stream
             g.replay()  # warm replay
@@ -323,9 +371,22 @@ def run_gpu(args):
         barrier()
         err, _ = t.sync()
         assert err == 0, f"device error bits {err} in the graph replays"
+        timed_graph.collect_ms = None
+        if timing:
+            with torch.cuda.stream(stream):
+                for _ in range(2):
+                    gi.replay()
+            barrier()
+            try:
+                timed_graph.collect_ms = float(np.mean([a.elapsed_time(z) for a, z in gev]))
+            except RuntimeError:  # timing events not usable inside this graph
+                pass
+            err, _ = t.sync()
+            assert err == 0, f"device error bits {err} in the instrumented replays"
         return e0.elapsed_time(e1), per_graph * (args.steps // S), S
 
     ms, coll_ms_p, launches, clk = timed(step_pipe)
+    coll_src = "eager pipelined run (events on the collect stream around each launch)"
     step_pct = dict(timed.percentiles)
     ms_serial, coll_ms_s, _, clk_s = timed(step_serial)
     graph = None
@@ -339,8 +400,13 @@ def run_gpu(args):
                  "steps_per_graph": S_g, "gpu_launches": launches_g}
         if ms_g < ms:  # the graph-replayed pipelined step is the headline when faster
             graph["eager_pipelined"] = {"value": world * B * args.steps / (ms / 1e3),
-                                        "ms_per_step": ms / args.steps}
+                                        "ms_per_step": ms / args.steps,
+                                        "collect_avg_ms": coll_ms_p}
             ms, launches = ms_g, launches_g
+            if timed_graph.collect_ms is not None:  # the headline's own collect launches
+                coll_ms_p = timed_graph.collect_ms
+                coll_src = ("graph replay (events captured around each collect of an "
+                            "instrumented copy of the step graph, replayed after the timed region)")
 
     # End-to-end through the C-ABI with HOST buffers, pipelined like the device
     # step.  Every step: gear_sample writes the IS weights straight to pinned
@@ -442,6 +508,7 @@ def run_gpu(args):
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["kernel"] = "collect_tma_kernel" if max(t.row_bytes) >= 4096 else "collect_kernel"
     roof["avg_launch_ms"] = coll_avg
+    roof["launch_timing"] = coll_src
     roof["algorithmic_bytes_per_launch"] = alg
     roof["remote_fraction"] = f_remote
     roof["traffic"] = args.traffic
