@@ -101,6 +101,7 @@ struct Cand {
 // Per-shard state of the multi-CTA TopK radix select (kernels/topk.cu);
 // zero-initialised once, re-armed by the kernels themselves.
 constexpr uint32_t kTopkMaxCtas = 512;  // CTAs per shard
+constexpr uint32_t kTopkEqMax = 2048;   // extra candidates beyond K the sort may rank
 struct TopkState {
   unsigned long long max_key;  // stats: largest key
   uint64_t prefix;             // select: key bits fixed so far (== T* when done)
@@ -110,7 +111,7 @@ struct TopkState {
   int shift;          // next byte to resolve; < 0 when done
   uint32_t all;       // n_sel <= K: take every selectable key
   uint32_t ctr;       // last-CTA counter
-  uint32_t pad;
+  uint32_t eq_all;    // select stopped on a small bin: take all of it, the sort keeps K
   uint32_t hist[256];
 };
 

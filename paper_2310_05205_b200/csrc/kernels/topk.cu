@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(kThreads)
     const uint64_t mxk = *(volatile unsigned long long*)&S.max_key;
     const uint32_t n = *(volatile uint32_t*)&S.n_sel;
     S.all = n <= K;
+    S.eq_all = 0;
     S.k_remain = K;
     S.prefix = 0;
     S.mask = 0;
@@ -147,21 +148,28 @@ __global__ void __launch_bounds__(kThreads)
   for (int w = 0; w < warp; ++w) suf += s_hist[w];
   if (suf >= kk && suf - h < kk) {  // exactly one thread
     const uint32_t v = 255 - t;
+    const uint32_t need = kk - (suf - h);
     S.prefix = prefix | ((uint64_t)v << shift);
     S.mask = mask | (255ull << shift);
-    S.k_remain = kk - (suf - h);
-    // done after the last byte, or as soon as every key of the bin is needed
-    // (then the keys > T* and == T* are those above / in the bin, ties moot)
-    S.shift = h == kk - (suf - h) ? -1 : shift - 8;
+    S.k_remain = need;
+    // Done after the last byte, or as soon as the boundary bin is small: then
+    // every key of the bin becomes a candidate (at most kTopkEqMax beyond the
+    // K) and the rank sort keeps the first K by (key desc, slot asc).  After
+    // the last byte with a large bin the bin holds equal keys: the first
+    // `need` in slot order are taken.
+    const bool small = h - need <= kTopkEqMax;
+    S.eq_all = small ? 1u : 0u;
+    S.shift = (small || shift == 0) ? -1 : shift - 8;
   }
   __syncthreads();  // every thread has read the histogram
   for (int b = threadIdx.x; b < 256; b += kThreads) S.hist[b] = 0;
 }
 
-// Keys taken: all selectable ones (all), or the keys whose resolved bytes
-// (x & mask) exceed the prefix plus the first k_remain keys whose resolved
-// bytes equal it, in slot order.  With every byte resolved the prefix is the
-// K-th largest key T* itself and this is "key > T*, then ties by slot".
+// Candidates: all selectable keys (all), or the keys whose resolved bytes
+// (x & mask) exceed the prefix plus those whose resolved bytes equal it --
+// all of them (eq_all: a bin of at most K + kTopkEqMax keys, ranked by the
+// sort) or the first k_remain in slot order (every byte resolved: the prefix
+// is the K-th largest key T* itself, "key > T*, then ties by slot").
 __device__ __forceinline__ void classify(const TopkState& S, uint64_t x, bool* gt, bool* eq) {
   if (S.all) {
     *gt = x > 0;
@@ -215,7 +223,8 @@ __global__ void __launch_bounds__(kThreads)
   const uint32_t ls = blockIdx.y;
   const TopkState& S = st[ls];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t need = S.all ? 0u : S.k_remain;
+  const uint32_t need = S.all ? 0u : (S.eq_all ? 0xffffffffu : S.k_remain);
+  const uint32_t cap = K + kTopkEqMax;  // candidate slots per shard
   __shared__ uint32_t s_tg, s_te;
   if (tid == 0) s_base_gt = s_base_eq = s_tg = s_te = 0;
   __syncthreads();
@@ -244,7 +253,7 @@ __global__ void __launch_bounds__(kThreads)
       atomicAdd(&s_te, te);
     }
     __syncthreads();
-    if (tid == 0) s_tot = min(K, s_tg + min(need, s_te));
+    if (tid == 0) s_tot = min(cap, s_tg + min(need, s_te));
     __syncthreads();
   }
   const uint32_t base_gt = s_base_gt;
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(kThreads)
   uint32_t taken = base_gt + min(need, eq_seen);
   const Slice sl = cta_slice(shard_cap, G, blockIdx.x);
   const uint64_t* k = key + (uint64_t)ls * shard_cap;
-  Cand* out = cand_out + (uint64_t)ls * K;
+  Cand* out = cand_out + (uint64_t)ls * cap;
   for (uint64_t i0 = sl.begin; i0 < sl.end; i0 += kThreads) {
     const uint64_t i = i0 + tid;
     const uint64_t x = i < sl.end ? k[i] : 0;
@@ -281,16 +290,16 @@ __global__ void __launch_bounds__(kThreads)
       c.shard = first_shard + ls;
       c.slot = (uint32_t)i;
       const uint32_t pos = taken + gt_before + __popc(mg & lt) + eq_taken_before;
-      if (pos < K) out[pos] = c;  // always true when the selection invariant holds
+      if (pos < cap) out[pos] = c;  // always true when the selection invariant holds
     }
     taken += gt_total + (min(need, eq_seen + eq_total) - min(need, eq_seen));
     eq_seen += eq_total;
     __syncthreads();
   }
-  if (blockIdx.x == 0 && tid == 0) {
+  if (blockIdx.x == 0 && tid == 0) {  // candidates for the sort, list length for the merge
     ShardTotals t;
-    t.total_and_parity = 0;
-    t.aux = s_tot;
+    t.total_and_parity = s_tot;
+    t.aux = min(s_tot, K);
     totals_out[ls] = t;
   }
 }
@@ -313,7 +322,8 @@ __global__ void __launch_bounds__(kSortThreads)
   const Mbox m = xchg ? mbox_at_next_epoch(m0) : m0;  // the FIFO/TopK epoch advances later
   const uint32_t ls = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31;
-  const uint32_t n = (uint32_t)totals[ls].aux;
+  const uint32_t n = (uint32_t)totals[ls].total_and_parity;  // candidates (write_kernel)
+  const uint32_t n_out = n < K ? n : K;
   const uint32_t i = blockIdx.x * kSortWarps + (tid >> 5);
   const uint32_t shard = first_shard + ls;
   if (blockIdx.x == 0 && tid == 0) {  // re-arm this shard's selection state for the next call
@@ -322,15 +332,15 @@ __global__ void __launch_bounds__(kSortThreads)
     S.max_key = 0;
   }
   if (i < n) {
-    const Cand* in = unsorted + (uint64_t)ls * K;
+    const Cand* in = unsorted + (uint64_t)ls * (K + kTopkEqMax);
     const Cand me = in[i];
     uint32_t rank = 0;
 #pragma unroll 4
     for (uint32_t j = lane; j < n; j += 32) rank += before(in[j], me);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) rank += __shfl_xor_sync(kFull, rank, d);
-    if (lane == 0) sorted[(uint64_t)ls * K + rank] = me;
-    if (xchg && lane < m.W) {  // W > 1: straight into every peer's mailbox as well
+    if (rank < K && lane == 0) sorted[(uint64_t)ls * K + rank] = me;
+    if (rank < K && xchg && lane < m.W) {  // W > 1: straight into every peer's mailbox too
       const MboxLayout L = mbox_layout(m.W, m.S, m.MB);
       const uint32_t b = mbox_buf(m);
       mbox_at<Cand>(m, lane, L.cand)[((uint64_t)b * m.S + shard) * K + rank] = me;
@@ -351,7 +361,7 @@ __global__ void __launch_bounds__(kSortThreads)
   const uint32_t b = mbox_buf(m);
   ShardTotals t;
   t.total_and_parity = 0;
-  t.aux = n;
+  t.aux = n_out;
   for (uint32_t r = 0; r < m.W; ++r) mbox_at<ShardTotals>(m, r, L.ccnt)[b * m.S + shard] = t;
   __threadfence_system();
   for (uint32_t r = 0; r < m.W; ++r)
@@ -388,7 +398,7 @@ cudaError_t launch_topk_local(const uint64_t* key, uint64_t shard_cap, uint64_t 
   count_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, state, cnt);
   write_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, K, first_shard, state, cnt, cand_tmp,
                                          totals_out);
-  const dim3 sgrid((K + kSortWarps - 1) / kSortWarps, n_shards_local);
+  const dim3 sgrid((K + kTopkEqMax + kSortWarps - 1) / kSortWarps, n_shards_local);
   sort_kernel<<<sgrid, kSortThreads, 0, s>>>(K, first_shard, cand_tmp, cand_out, totals_out,
                                                 state, mbox ? *mbox : Mbox{}, mbox != nullptr);
   return cudaGetLastError();

@@ -140,7 +140,7 @@ struct gear_table {
   uint32_t* glob_slot = nullptr;
   gear::Cand* cand_local = nullptr;  // [R * W*max_batch]
   gear::TopkState* topk_state = nullptr;  // [R]
-  gear::Cand* topk_tmp = nullptr;         // [R * W*max_batch] unsorted TopK lists
+  gear::Cand* topk_tmp = nullptr;         // [R * (W*max_batch + kTopkEqMax)] TopK candidates
   uint32_t* topk_cnt = nullptr;           // [R][kTopkMaxCtas][2]
   gear::Cand* cand_all = nullptr;    // [S * W*max_batch]
 
