@@ -166,7 +166,7 @@ void destroy_table(gear_table* t) {
   dfree(t->glob_shard); dfree(t->glob_slot);
   dfree(t->upd_local); dfree(t->upd_all); dfree(t->upd_idx); dfree(t->upd_prio); dfree(t->upd_pow); dfree(t->upd_gen);
   dfree(t->n_stale); dfree(t->err); dfree(t->d_epoch); dfree(t->d_seed); dfree(t->d_xep);
-  dfree(t->col_idx.p);
+  for (auto& b : t->col_idx) dfree(b.p);
   dfree(t->d_meta); dfree(t->d_ord); dfree(t->d_out); dfree(t->d_rows);
   dfree(t->d_prio_ins); dfree(t->d_alloc); dfree(t->ins_bad); dfree(t->dyn_pool);
   if (t->h_prio) cudaFreeHost(t->h_prio);
@@ -1049,13 +1049,14 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
   if (ncols > (uint32_t)kMaxCols) return set_error(GEAR_ERR_INVALID_ARG, "ncols > %d", kMaxCols);
   const uint64_t* d_idx = idx;
   if (mem_kind(idx) != MemKind::Device) {
-    if (t->col_idx.n < n) {
-      dfree(t->col_idx.p);
-      GEAR_TRY(dalloc(&t->col_idx.p, n));
-      t->col_idx.n = n;
+    DevBuf<uint64_t>& buf = t->col_idx[t->col_idx_next++ % 4];
+    if (buf.n < n) {
+      dfree(buf.p);
+      GEAR_TRY(dalloc(&buf.p, n));
+      buf.n = n;
     }
-    GEAR_CUDA(cudaMemcpyAsync(t->col_idx.p, idx, n * 8ull, cudaMemcpyHostToDevice, s));
-    d_idx = t->col_idx.p;
+    GEAR_CUDA(cudaMemcpyAsync(buf.p, idx, n * 8ull, cudaMemcpyHostToDevice, s));
+    d_idx = buf.p;
   }
   CollectParams cp{};
   cp.idx = d_idx;

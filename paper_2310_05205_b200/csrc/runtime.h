@@ -157,7 +157,8 @@ struct gear_table {
   uint32_t* err = nullptr;
 
   // collect scratch (host-resident id lists)
-  gear::DevBuf<uint64_t> col_idx;
+  gear::DevBuf<uint64_t> col_idx[4];  // rotating: collects on different streams do not share one
+  uint32_t col_idx_next = 0;
 
   // block allocator (device-resident, kernels/alloc.cu) and insert staging
   gear::AllocState* d_alloc = nullptr;  // [R]
