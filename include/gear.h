@@ -20,8 +20,14 @@
  *    returned by gear_table_sync().
  *  - Small per-call arrays (ids, priorities, generations, sample outputs) may
  *    be DEVICE or HOST pointers; the library detects which.  Pinned host
- *    memory keeps the call asynchronous; pageable host memory makes the copy
- *    synchronous.  Collect outputs must be device memory (or mapped pinned).
+ *    memory keeps the call asynchronous (update inputs and sample outputs are
+ *    read / written in place by the kernels through their mapped address);
+ *    pageable host memory goes through per-table scratch with a synchronous
+ *    copy, so calls with pageable arrays must be ordered among themselves
+ *    (one stream).  Collect outputs must be device memory (or mapped pinned).
+ *  - Streams: sample and update of a table must be issued in one order (they
+ *    share the keys and, at W > 1, the exchange epochs); collects and writers
+ *    may run on other streams ordered by events, as bench.py does.
  *  - The caller owns every argument buffer and must keep it alive until the
  *    stream has reached the call.  The table owns its columns, keys, CDFs and
  *    scratch.
