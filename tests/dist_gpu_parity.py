@@ -240,6 +240,105 @@ def run_graph_case(comm, W, rank, R=2, Cs=500, B=48, reps=4):
     t.close()
 
 
+def run_fuzz_case(comm, W, rank, R=2, Cs=400, steps=150, seed=11):
+    """Random collective operation sequences (inserts, allocate / commit,
+    updates, samples of every strategy plain and owner-affine, collects), the
+    same sequence on every rank, each result compared with the oracle --
+    exercises the mailbox epochs across arbitrary interleavings."""
+    cols = [gear.Column("a", gear.GEAR_F32, (3,), gear.GEAR_DEVICE),
+            gear.Column("b", gear.GEAR_U8, (5,), gear.GEAR_HOST)]
+    S = W * R
+    N = S * Cs
+    t = gear.Table(N, 2, cols, comm, shards_per_rank=R, max_batch=256)
+    o = oracle.Table(Cs, S)
+    rb = t.row_bytes
+    content = np.full(N, -1, np.int64)
+    rng = np.random.default_rng(seed)            # identical on every rank
+    lo, hi = rank * R * Cs, (rank + 1) * R * Cs
+    next_traj = 0
+    strategies = [gear.GEAR_UNIFORM, gear.GEAR_WEIGHTED, gear.GEAR_PRIORITIZED, gear.GEAR_FIFO,
+                  gear.GEAR_LIFO, gear.GEAR_TOPK]
+    for step in range(steps):
+        op = int(rng.integers(0, 5))
+        if op == 0:                              # every shard gets an insert
+            for s in range(S):
+                n = int(rng.integers(1, 150))
+                p = synth.priorities(n, seed=1000 * step + s, zero_frac=0.1)
+                traj = np.arange(next_traj, next_traj + n)
+                next_traj += n
+                st, oidx = o.insert(s, p)
+                content[oidx.astype(np.int64)] = traj
+                if s // R == rank:
+                    rows = [torch.from_numpy(synth.row_bytes_of(c, traj, rb[c])).cuda()
+                            for c in range(len(cols))]
+                    out = np.zeros(n, np.uint64)
+                    t.insert(s, rows, p, out)
+                    assert np.array_equal(out, oidx), "insert slots differ"
+        elif op == 1:                            # allocate -> rows in place -> commit
+            for s in range(S):
+                n = int(rng.integers(1, 20))
+                st, oids = o.allocate(s, n)
+                if st != 0:
+                    continue
+                traj = np.arange(next_traj, next_traj + n)
+                next_traj += n
+                content[oids.astype(np.int64)] = traj
+                pc = synth.priorities(n, seed=7 * step + s)
+                o.commit(s, oids, pc)
+                if s // R == rank:
+                    ids = torch.empty(n, dtype=torch.int64, device="cuda")
+                    t.allocate(s, n, ids)
+                    torch.cuda.synchronize()
+                    assert np.array_equal(ids.cpu().numpy().view(np.uint64), oids)
+                    local = (oids - np.uint64(lo)).astype(np.int64)
+                    for c in range(len(cols)):
+                        write_rows_in_place(t, c, cols[c].placement, local,
+                                            synth.row_bytes_of(c, traj, rb[c]), R * Cs, rb[c])
+                    t.commit(s, ids, torch.from_numpy(pc).cuda())
+        elif op == 2:                            # collective update of random ids
+            n = int(rng.integers(1, 200))
+            lists = [(rng.integers(0, N, n).astype(np.uint64), rng.lognormal(0, 1, n))
+                     for _ in range(W)]
+            ids, p = lists[rank]
+            gear.gear_update_priorities(t.handle, n, torch.from_numpy(ids.view(np.int64)).cuda(),
+                                        torch.from_numpy(p).cuda(), gear.GEAR_F64)
+            for r in range(W):
+                o.update(lists[r][0], lists[r][1])
+            torch.cuda.synchronize()
+            err, _ = t.sync()                    # never-inserted / ongoing ids: stale
+            assert err & ~gear.GEAR_DEVERR_STALE == 0, err
+        else:                                    # sample (+ collect)
+            strat = strategies[int(rng.integers(0, len(strategies)))]
+            affine = bool(rng.integers(0, 2))
+            B = int(rng.integers(1, 100))
+            sd = int(rng.integers(0, 1 << 30))
+            idx = torch.empty(B, dtype=torch.int64, device="cuda")
+            w = torch.empty(B, dtype=torch.float32, device="cuda")
+            t.sample(strat | (gear.GEAR_SAMPLE_OWNER_AFFINE if affine else 0), B, sd, 0.4, idx, w)
+            torch.cuda.synchronize()
+            st, oi, ow, _ = o.sample(OS[strat], W, rank, B, sd, 0.4, owner_affine=affine)
+            gi = idx.cpu().numpy().view(np.uint64)
+            err, _ = t.sync()
+            if st == oracle.EMPTY:
+                assert err & gear.GEAR_DEVERR_EMPTY
+                continue
+            assert st == 0 and err == 0, (st, err)
+            assert np.array_equal(gi, oi), f"step {step} strategy {strat}: ids differ"
+            np.testing.assert_allclose(w.cpu().numpy(), ow, rtol=1e-6)
+            outs = [torch.empty((B, r), dtype=torch.uint8, device="cuda") for r in rb]
+            t.collect(idx, list(range(len(cols))), outs)
+            torch.cuda.synchronize()
+            for c in range(len(cols)):
+                want = synth.row_bytes_of(c, content[oi.astype(np.int64)], rb[c])
+                assert np.array_equal(outs[c].cpu().numpy(), want), f"step {step} column {c}"
+        torch.cuda.synchronize()
+        dist.barrier()
+        key, sq, gen = t.read_state()
+        assert np.array_equal(key, o.key[lo:hi]) and np.array_equal(sq, o.seq[lo:hi])
+        assert np.array_equal(gen, o.gen[lo:hi])
+    t.close()
+
+
 def main():
     W = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
@@ -259,6 +358,10 @@ def main():
     dist.barrier()
     if rank == 0:
         print("case graph replay (owner-affine, device seed): ok", flush=True)
+    run_fuzz_case(comm, W, rank)
+    dist.barrier()
+    if rank == 0:
+        print("case random collective sequences: ok", flush=True)
     gear.gear_comm_destroy(comm)
     dist.destroy_process_group()
     print(f"rank {rank}: all multi-GPU parity cases ok", flush=True)
