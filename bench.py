@@ -506,6 +506,9 @@ def run_gpu(args):
                             "nvlink": "probe: cudaMemcpyPeer pull (profiles/r01_probe_2gpu.jsonl)",
                             "pcie": "probe: pinned H2D cudaMemcpy (profiles/r01_probe_2gpu.jsonl)"}[bound]}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    if roof["frac"] < 0.2:  # e.g. c1: a few hundred KB per launch
+        roof["note"] = ("latency-bound: %.0f KB per collect launch, far below what saturates %s"
+                        % (alg / 1e3, bound.upper()))
     roof["kernel"] = "collect_tma_kernel" if max(t.row_bytes) >= 4096 else "collect_kernel"
     roof["avg_launch_ms"] = coll_avg
     roof["launch_timing"] = coll_src
