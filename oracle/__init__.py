@@ -2,7 +2,7 @@
 
 This package is the plain, slow, single-threaded definition of what the CUDA
 path computes (see gear_oracle.h for the per-function citations into
-PAPER.md and the readings Q1..Q16 in DESIGN.md §3).  Only ``tests/``,
+PAPER.md and the readings Q1..Q21 in DESIGN.md §3).  Only ``tests/``,
 ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` / ``--impl
 reference`` legs may import it.  It shares no code with
 ``paper_2310_05205_b200`` and never imports it.

@@ -4,7 +4,10 @@
  * A plain, slow, single-threaded CPU oracle for the GEAR (arXiv 2310.05205)
  * replay hot path: quantised priority update, CDF, Philox draw, inverse-CDF
  * search, uniform/weighted/prioritized sampling with importance weights,
- * FIFO/LIFO selection, index translation, collection and insertion.
+ * FIFO/LIFO/TopK selection (plain and owner-affine), index translation,
+ * collection, insertion and the split allocate / commit writer.  The PER
+ * exponent (RN(p^alpha), reading Q7) is applied by oracle/__init__.py with
+ * mpmath before the priorities reach this code.
  *
  * It treats the W shards as ONE concatenated global table (global id order),
  * which is the plain definition of what the sharded GPU path must reproduce
