@@ -1,4 +1,6 @@
 #!/bin/bash
+# The ncu part of run_bench_suite.sh alone (launch list + full captures).
+# usage: tools/run_ncu_suite.sh <outdir>
 out=gpurun_out/${1:-suite}
 mkdir -p $out
 K='collect|sample_kernel|scan2_kernel|scan_kernel|assign_kernel|fused_kernel|alpha_kernel'
