@@ -35,6 +35,7 @@ sys.path.insert(0, ROOT)
 os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep stdout to the one JSON line:
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # (WARN still prints the version line)
 
+L2_BYTES = 126 << 20   # B200 L2
 METRIC = "sampled+collected trajectories/sec and collect GB/s vs HBM/PCIe roofline, 1/2/4/8 B200"
 UNIT = "trajectories/s"
 PCIE_H2D_GBS = 55.62     # profiles/r01_probe_2gpu.jsonl: pinned cudaMemcpy H2D, 1 GiB, best of 5
@@ -159,6 +160,36 @@ def build_table(cfg, comm, n_ranks: int, rank: int, capacity: int, stream):
     return t, prio_all
 
 
+def effective_cfg(args):
+    """The config with the --strategy override applied (both arms)."""
+    import dataclasses
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    if args.strategy:
+        cfg = dataclasses.replace(cfg, strategy=args.strategy,
+                                  update=cfg.update and args.strategy == "prioritized")
+    return cfg
+
+
+def workload_config(cfg, capacity, world, args, cap_note):
+    """The `config` object of the JSON line, identical for both arms."""
+    import synth
+    row_total = sum(synth.row_bytes(cfg, c) for c in cfg.cols)
+    payload = cfg.batch * row_total
+    return {"workload": cfg.name, "capacity": capacity, "seq_len": cfg.seq_len,
+            "row_bytes": row_total, "strategy": cfg.strategy, "batch_per_rank": cfg.batch,
+            "global_batch": world * cfg.batch, "update_per_step": cfg.update,
+            "table_bytes": capacity * row_total,
+            "l2": ("inputs larger than L2: random rows of a %.1f GB table, %.0f MB batch per rank"
+                   % (capacity * row_total / 1e9, payload / 1e6)
+                   if capacity * row_total > L2_BYTES else
+                   "L2-resident table (%.1f MB < %d MB L2), not flushed: a latency case, "
+                   "not a bandwidth measurement" % (capacity * row_total / 1e6, L2_BYTES >> 20)),
+            "parallelism": f"dp{world} (table sharded by trajectory id, 1 shard per GPU)",
+            "assignment": args.assign,
+            **({"note": cap_note} if cap_note else {})}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -173,11 +204,7 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     gear.load()
     comm = gear.comm_from_torch_distributed(local) if world > 1 else None
-    cfg = synth.CONFIGS[args.config]
-    if args.strategy:
-        import dataclasses
-        cfg = dataclasses.replace(cfg, strategy=args.strategy,
-                                  update=cfg.update and args.strategy == "prioritized")
+    cfg = effective_cfg(args)
     capacity, cap_note = scaled_capacity(cfg, world)
     stream = torch.cuda.Stream()
     t, prio_all = build_table(cfg, comm, world, rank, capacity, stream)
@@ -530,15 +557,7 @@ def run_gpu(args):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (seeded splitmix64 row bytes, lognormal priorities)",
-        "config": {"workload": cfg.name, "capacity": capacity, "seq_len": cfg.seq_len,
-                   "row_bytes": row_total, "strategy": cfg.strategy, "batch_per_rank": B,
-                   "global_batch": world * B, "update_per_step": cfg.update,
-                   "table_bytes": capacity * row_total,
-                   "l2": "inputs larger than L2: random rows of a %.1f GB table, %.0f MB batch per rank"
-                         % (capacity * row_total / 1e9, payload / 1e6),
-                   "parallelism": f"dp{world} (table sharded by trajectory id, 1 shard per GPU)",
-                   "assignment": args.assign,
-                   **({"note": cap_note} if cap_note else {})},
+        "config": workload_config(cfg, capacity, world, args, cap_note),
         "collect_gbps": payload / (coll_avg / 1e3) / 1e9,
         "step": ("pipelined: collect(i) on a 2nd stream overlaps update(i) + sample(i+1)"
                  + ("; CUDA-graph replay" if graph and "eager_pipelined" in graph else "")),
@@ -625,7 +644,7 @@ def run_reference(args):
     if rank != 0:
         return
     import synth
-    cfg = synth.CONFIGS[args.config]
+    cfg = effective_cfg(args)
     capacity, note = scaled_capacity(cfg, world)
     if cfg.prio == "tasks":
         prio_all = synth.task_weights(capacity, zero_frac=cfg.zero_frac)
@@ -637,8 +656,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": cfg.name, "capacity": capacity, "batch_per_rank": cfg.batch,
-                   "strategy": cfg.strategy, **({"note": note} if note else {})},
+        "config": workload_config(cfg, capacity, world, args, note),
         "cpu_baseline": cb,
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
