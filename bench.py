@@ -547,6 +547,12 @@ def run_gpu(args):
         # (unchanged since) from ncu --set full at this config
         roof["traffic"] = (433.055232 + 384.025856) * 1e6
         roof["traffic_source"] = "profiles/r01e/ncu_collect_tma_full_raw.csv (one launch)"
+    elif args.traffic is None and cfg.name == "c3_gato_db1" and world == 1 and args.strategy is None:
+        # PCIe-bound: the 4.2 MB batch stays in L2 (0 B reach DRAM), the rows
+        # come over PCIe; dram__bytes_read + write of one launch, ncu --set full
+        roof["traffic"] = 86.272e3 + 0.0
+        roof["traffic_source"] = ("profiles/r01s/ncu_collect_tma_c3_full_raw.csv (one launch; "
+                                  "DRAM bytes only, the binding PCIe read is in the same capture)")
     # The whole step against the same bound: the step's algorithmic bytes of
     # the binding resource over the (headline) time per step.
     roof["step_achieved"] = alg / (ms / args.steps / 1e3) / 1e9

@@ -74,6 +74,8 @@ void dfree(T*& p) {
 // memory.  shm_name empty: private anonymous memory (W = 1); otherwise a POSIX
 // shared-memory object (created if `create`), so every rank's GPU can map the
 // same pages.
+constexpr size_t kHostRegChunk = size_t(64) << 30;
+
 gear_status map_host(const std::string& shm_name, bool create, size_t bytes, void** out) {
   *out = nullptr;
   void* p = MAP_FAILED;
@@ -93,19 +95,37 @@ gear_status map_host(const std::string& shm_name, bool create, size_t bytes, voi
   }
   if (p == MAP_FAILED) return set_error(GEAR_ERR_OUT_OF_MEMORY, "mmap(%zu) failed", bytes);
   madvise(p, bytes, MADV_HUGEPAGE);
-  cudaError_t e = cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  // One registration per kHostRegChunk: a single cudaHostRegister of ~300 GB
+  // fails on the 4-GPU boxes ("OS call failed"), 64 GiB pieces do not.  The
+  // pieces form one contiguous device range because registered memory is
+  // mapped at its host address (checked below; UVA).
+  size_t done = 0;
+  cudaError_t e = cudaSuccess;
+  for (; done < bytes; done += kHostRegChunk) {
+    uint8_t* c = (uint8_t*)p + done;
+    size_t n = std::min(kHostRegChunk, bytes - done);
+    e = cudaHostRegister(c, n, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) break;
+    void* dp = nullptr;
+    if (cudaHostGetDevicePointer(&dp, c, 0) != cudaSuccess || dp != (void*)c) {
+      cudaHostUnregister(c);
+      e = cudaErrorNotSupported;
+      break;
+    }
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
+    for (size_t o = 0; o < done; o += kHostRegChunk) cudaHostUnregister((uint8_t*)p + o);
     munmap(p, bytes);
-    return set_error(GEAR_ERR_OUT_OF_MEMORY, "cudaHostRegister(%zu bytes): %s", bytes,
-                     cudaGetErrorString(e));
+    return set_error(GEAR_ERR_OUT_OF_MEMORY, "cudaHostRegister(%zu of %zu bytes at offset %zu): %s",
+                     std::min(kHostRegChunk, bytes - done), bytes, done, cudaGetErrorString(e));
   }
   *out = p;
   return GEAR_OK;
 }
 
 void unmap_host(void* p, size_t bytes) {
-  cudaHostUnregister(p);
+  for (size_t o = 0; o < bytes; o += kHostRegChunk) cudaHostUnregister((uint8_t*)p + o);
   munmap(p, bytes);
 }
 
