@@ -74,9 +74,20 @@ void dfree(T*& p) {
 // memory.  shm_name empty: private anonymous memory (W = 1); otherwise a POSIX
 // shared-memory object (created if `create`), so every rank's GPU can map the
 // same pages.
-constexpr size_t kHostRegChunk = size_t(64) << 30;
+constexpr size_t kHostRegChunkDefault = size_t(64) << 30;
 
-gear_status map_host(const std::string& shm_name, bool create, size_t bytes, void** out) {
+// GEAR_HOST_REG_CHUNK (bytes, a multiple of 2 MiB): a smaller piece size, so
+// tests cover rows that straddle two registrations.
+size_t host_reg_chunk() {
+  if (const char* e = getenv("GEAR_HOST_REG_CHUNK")) {
+    const size_t v = (size_t)strtoull(e, nullptr, 10);
+    if (v >= (size_t(2) << 20) && v % (size_t(2) << 20) == 0) return v;
+  }
+  return kHostRegChunkDefault;
+}
+
+gear_status map_host(const std::string& shm_name, bool create, size_t bytes, size_t piece,
+                     void** out) {
   *out = nullptr;
   void* p = MAP_FAILED;
   if (shm_name.empty()) {
@@ -95,15 +106,15 @@ gear_status map_host(const std::string& shm_name, bool create, size_t bytes, voi
   }
   if (p == MAP_FAILED) return set_error(GEAR_ERR_OUT_OF_MEMORY, "mmap(%zu) failed", bytes);
   madvise(p, bytes, MADV_HUGEPAGE);
-  // One registration per kHostRegChunk: a single cudaHostRegister of ~300 GB
+  // One registration per piece: a single cudaHostRegister of ~300 GB
   // fails on the 4-GPU boxes ("OS call failed"), 64 GiB pieces do not.  The
   // pieces form one contiguous device range because registered memory is
   // mapped at its host address (checked below; UVA).
   size_t done = 0;
   cudaError_t e = cudaSuccess;
-  for (; done < bytes; done += kHostRegChunk) {
+  for (; done < bytes; done += piece) {
     uint8_t* c = (uint8_t*)p + done;
-    size_t n = std::min(kHostRegChunk, bytes - done);
+    size_t n = std::min(piece, bytes - done);
     e = cudaHostRegister(c, n, cudaHostRegisterMapped | cudaHostRegisterPortable);
     if (e != cudaSuccess) break;
     void* dp = nullptr;
@@ -115,17 +126,17 @@ gear_status map_host(const std::string& shm_name, bool create, size_t bytes, voi
   }
   if (e != cudaSuccess) {
     cudaGetLastError();
-    for (size_t o = 0; o < done; o += kHostRegChunk) cudaHostUnregister((uint8_t*)p + o);
+    for (size_t o = 0; o < done; o += piece) cudaHostUnregister((uint8_t*)p + o);
     munmap(p, bytes);
     return set_error(GEAR_ERR_OUT_OF_MEMORY, "cudaHostRegister(%zu of %zu bytes at offset %zu): %s",
-                     std::min(kHostRegChunk, bytes - done), bytes, done, cudaGetErrorString(e));
+                     std::min(piece, bytes - done), bytes, done, cudaGetErrorString(e));
   }
   *out = p;
   return GEAR_OK;
 }
 
-void unmap_host(void* p, size_t bytes) {
-  for (size_t o = 0; o < bytes; o += kHostRegChunk) cudaHostUnregister((uint8_t*)p + o);
+void unmap_host(void* p, size_t bytes, size_t piece) {
+  for (size_t o = 0; o < bytes; o += piece) cudaHostUnregister((uint8_t*)p + o);
   munmap(p, bytes);
 }
 
@@ -164,7 +175,7 @@ void destroy_table(gear_table* t) {
   cudaDeviceSynchronize();
   for (auto& c : t->cols) {
     for (void* p : c.ipc_opened) cudaIpcCloseMemHandle(p);
-    for (auto& m : c.host_maps) unmap_host(m.first, m.second);
+    for (auto& m : c.host_maps) unmap_host(m.first, m.second, c.host_reg_chunk);
     if (c.placement == GEAR_DEVICE && c.local) cudaFree(c.local);
   }
   for (void* p : t->ipc_opened) cudaIpcCloseMemHandle(p);
@@ -307,6 +318,7 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
         cs.view[0] = cs.local;
       }
     } else {
+      cs.host_reg_chunk = host_reg_chunk();
       if (t->W == 1) {
         void* p = nullptr;
         // GEAR_HOST_SHM=1: use a shared-memory object even at W = 1 (to
@@ -317,7 +329,7 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
           snprintf(b, sizeof(b), "/gear_w1_%d_c%u", (int)getpid(), c);
           nm = b;
         }
-        GEAR_TRY(map_host(nm, true, cs.bytes_local, &p));
+        GEAR_TRY(map_host(nm, true, cs.bytes_local, cs.host_reg_chunk, &p));
         if (!nm.empty()) shm_unlink(nm.c_str());
         cs.host_maps.emplace_back(p, cs.bytes_local);
         cs.local = (uint8_t*)p;
@@ -329,7 +341,7 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
         snprintf(nm, sizeof(nm), "/gear_%016llx_c%u_r%u", (unsigned long long)tag, c, t->rank);
         cs.shm_name = nm;
         void* p = nullptr;
-        GEAR_TRY(map_host(cs.shm_name, true, cs.bytes_local, &p));
+        GEAR_TRY(map_host(cs.shm_name, true, cs.bytes_local, cs.host_reg_chunk, &p));
         cs.host_maps.emplace_back(p, cs.bytes_local);
         cs.local = (uint8_t*)p;
         GEAR_TRY(barrier(comm));
@@ -337,7 +349,7 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
           void* q = p;
           if (r != t->rank) {
             snprintf(nm, sizeof(nm), "/gear_%016llx_c%u_r%u", (unsigned long long)tag, c, r);
-            GEAR_TRY(map_host(nm, false, cs.bytes_local, &q));
+            GEAR_TRY(map_host(nm, false, cs.bytes_local, cs.host_reg_chunk, &q));
             cs.host_maps.emplace_back(q, cs.bytes_local);
           }
           void* dp = nullptr;

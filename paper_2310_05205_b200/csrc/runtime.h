@@ -65,6 +65,7 @@ struct ColumnState {
   const uint8_t* view[kMaxRanks] = {};  // device-accessible base of each rank's rows
   std::vector<void*> ipc_opened;        // peer device mappings to close
   std::vector<std::pair<void*, size_t>> host_maps;  // host mappings (own + peers) to unmap
+  size_t host_reg_chunk = 0;            // bytes per cudaHostRegister piece of those mappings
   std::string shm_name;                 // own shm object (W > 1 HOST columns)
 };
 

@@ -493,3 +493,23 @@ def test_sample_into_pinned_and_pageable_host(torch_cuda, strat):
         assert np.array_equal(p, op)
     assert P.t.sync()[0] == 0
     P.close()
+
+
+def test_host_rows_straddling_registration_pieces(torch_cuda, monkeypatch):
+    """Host columns are registered with CUDA in pieces (api.cpp map_host; 64 GiB
+    by default, 2 MiB here): rows that straddle two pieces are inserted and
+    collected byte-exactly, on the LSU path (3000-B rows) and the TMA bulk path
+    (12000-B rows)."""
+    monkeypatch.setenv("GEAR_HOST_REG_CHUNK", str(2 << 20))
+    cols = [synth.ColSpec("a", "u8", (1000,), "host"), synth.ColSpec("b", "i32", (1000,), "host")]
+    N = 1500
+    P = _pair(capacity=N, seq_len=3, colspecs=cols)
+    assert P.rb == [3000, 12000]
+    P.fill(synth.priorities(N, seed=5))
+    straddle = [g for g in range(N) for rb in P.rb
+                if (g * rb) // (2 << 20) != ((g + 1) * rb - 1) // (2 << 20)]
+    assert len(straddle) > 8
+    P.check_collect(np.asarray(sorted(set(straddle)), np.uint64))
+    P.check_collect(np.random.default_rng(3).permutation(N).astype(np.uint64))
+    P.check_collect(P.check_sample(G.GEAR_WEIGHTED, 1024, 77))
+    P.close()
