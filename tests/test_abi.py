@@ -72,3 +72,16 @@ def test_oracle_and_product_share_no_code():
             for dep in _imports_and_includes(os.path.join(odir, f)):
                 assert "paper_2310_05205_b200" not in dep and "gear.h" != dep \
                     and "synth" not in dep, (f, dep)
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    """No CPU fallback: without libgear.so every call raises instead of
+    computing anything on the host."""
+    import pytest
+    import paper_2310_05205_b200 as gear
+    monkeypatch.setattr(gear, "_lib", None)
+    monkeypatch.setattr(gear, "LIB_PATH", str(tmp_path / "libgear.so"))
+    with pytest.raises(ImportError, match="no CPU fallback"):
+        gear.load()
+    with pytest.raises(ImportError):
+        gear.gear_sample(1, gear.GEAR_PRIORITIZED, 4, 1, 0.4, 0, None, None, None, 0)
