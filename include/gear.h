@@ -185,7 +185,8 @@ const char* gear_version(void);
  * (diagnostics: bench.py reports the count inside its timed region). */
 uint64_t gear_kernel_launches(void);
 
-/* --- communicator (one per rank; wraps an NCCL communicator) ------------ */
+/* --- communicator (one per rank; wraps an NCCL communicator, or a host
+ *     all-gather callback: gear_comm_create_host) --------------------------- */
 
 /* Rank 0 creates the 128-byte unique id and the caller broadcasts it to the
  * other ranks by any means (the Python binding uses torch.distributed). */
@@ -195,6 +196,29 @@ gear_status gear_get_unique_id(uint8_t out[128]);
  * made current.  Peer access is enabled to every other rank's device. */
 gear_status gear_comm_create(int nranks, int rank, const uint8_t id[128], int device,
                              gear_comm** out);
+
+/* Host all-gather callback of gear_comm_create_host: gather `bytes` bytes of
+ * `send` from every rank into `recv` (nranks * bytes, rank order).  Host
+ * pointers.  Returns 0 on success.  Called only from the thread that makes
+ * the gear call, and only by calls every rank makes (create, destroy,
+ * barriers, the peer_xchg = 0 exchanges). */
+typedef int (*gear_allgather_fn)(void* ctx, const void* send, void* recv, size_t bytes);
+
+/* Collective over all nranks: a communicator bootstrapped WITHOUT NCCL, through
+ * the caller's host all-gather (the Python binding passes a torch.distributed
+ * gloo group).  Unlike gear_comm_create, several ranks may share one CUDA
+ * device (NCCL refuses that): every per-step exchange of the hot path is a
+ * peer-mailbox store through CUDA-IPC mappings, which work between processes
+ * on one device as between devices, so the multi-rank device path (totals /
+ * update / FIFO / TopK mailboxes, owner-CDF search, peer collect, shared host
+ * shards) runs unchanged -- kernels of different processes on one GPU are
+ * time-sliced, so it is a correctness vehicle, not a performance one.  The
+ * peer_xchg = 0 fallback exchanges go through the callback synchronously
+ * (device -> host copy, all-gather, host -> device copy; not capturable in a
+ * CUDA graph: UNSUPPORTED while the stream is capturing).  `fn` and `ctx`
+ * must stay valid until gear_comm_destroy. */
+gear_status gear_comm_create_host(int nranks, int rank, int device, gear_allgather_fn fn,
+                                  void* ctx, gear_comm** out);
 gear_status gear_comm_destroy(gear_comm* comm);
 
 /* --- table ------------------------------------------------------------- */

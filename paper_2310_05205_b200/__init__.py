@@ -94,6 +94,7 @@ SIGNATURES = {
     "gear_kernel_launches": ([], ctypes.c_uint64),
     "gear_get_unique_id": ([_P], _i32),
     "gear_comm_create": ([_i32, _i32, _P, _i32, _P], _i32),
+    "gear_comm_create_host": ([_i32, _i32, _i32, _P, _P, _P], _i32),
     "gear_comm_destroy": ([_P], _i32),
     "gear_table_create": ([_P, _P, _P], _i32),
     "gear_table_destroy": ([_P], _i32),
@@ -180,8 +181,55 @@ def gear_comm_create(nranks: int, rank: int, uid: bytes, device: int) -> int:
     return out.value
 
 
+# gear_allgather_fn: int (*)(void* ctx, const void* send, void* recv, size_t bytes)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                ctypes.c_size_t)
+_host_comms: dict[int, object] = {}   # comm handle -> callback (kept alive until destroy)
+
+
+def gear_comm_create_host(nranks: int, rank: int, device: int, allgather) -> int:
+    """gear_comm_create_host with a Python all-gather ``allgather(bytes) ->
+    list[bytes]`` (one entry per rank, rank order) as the host callback."""
+    def cb(_ctx, send, recv, nbytes):
+        try:
+            parts = allgather(ctypes.string_at(send, nbytes))
+            assert len(parts) == nranks and all(len(p) == nbytes for p in parts)
+            ctypes.memmove(recv, b"".join(parts), nbytes * nranks)
+            return 0
+        except Exception as e:  # noqa: BLE001 -- reported as a status by the library
+            print(f"gear host all-gather failed: {e!r}", flush=True)
+            return 1
+    fn = ALLGATHER_FN(cb)
+    out = ctypes.c_void_p()
+    _check("gear_comm_create_host",
+           load().gear_comm_create_host(nranks, rank, device, ctypes.cast(fn, ctypes.c_void_p),
+                                        None, ctypes.byref(out)))
+    _host_comms[out.value] = fn
+    return out.value
+
+
 def gear_comm_destroy(comm: int):
     _check("gear_comm_destroy", load().gear_comm_destroy(comm))
+    _host_comms.pop(comm, None)
+
+
+def comm_from_process_group(device: int, group=None) -> int | None:
+    """Create a gear comm bootstrapped through a torch.distributed group (any
+    backend -- gloo works -- with no NCCL communicator of its own), so several
+    ranks may share one CUDA device.  Returns None when the group has one
+    rank."""
+    import torch
+    import torch.distributed as dist
+    W = dist.get_world_size(group)
+    if W == 1:
+        return None
+
+    def allgather(b: bytes) -> list[bytes]:
+        t = torch.frombuffer(bytearray(b), dtype=torch.uint8)
+        out = [torch.empty_like(t) for _ in range(W)]
+        dist.all_gather(out, t, group=group)
+        return [o.numpy().tobytes() for o in out]
+    return gear_comm_create_host(W, dist.get_rank(group), device, allgather)
 
 
 def comm_from_torch_distributed(device: int) -> int | None:

@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "runtime.h"
 
@@ -49,18 +50,59 @@ MemKind mem_kind(const void* p) {
   }
 }
 
+// Host-callback all-gather: stream-ordered by synchronising the stream
+// (device buffers are staged through host memory).  Not graph-capturable.
+gear_status host_allgather(gear_comm* c, const void* send, void* recv, size_t bytes,
+                           cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  GEAR_CUDA(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone)
+    return set_error(GEAR_ERR_UNSUPPORTED,
+                     "a host-bootstrapped comm cannot run an all-gather inside stream capture "
+                     "(use peer_xchg = 1)");
+  GEAR_CUDA(cudaStreamSynchronize(s));
+  const bool dev_send = mem_kind(send) == MemKind::Device;
+  const bool dev_recv = mem_kind(recv) == MemKind::Device;
+  std::vector<uint8_t> hs, hr;
+  const void* sp = send;
+  void* rp = recv;
+  if (dev_send) {
+    hs.resize(bytes);
+    GEAR_CUDA(cudaMemcpy(hs.data(), send, bytes, cudaMemcpyDeviceToHost));
+    sp = hs.data();
+  }
+  if (dev_recv) {
+    hr.resize(bytes * (size_t)c->nranks);
+    rp = hr.data();
+  }
+  if (c->host_ag(c->host_ctx, sp, rp, bytes) != 0)
+    return set_error(GEAR_ERR_NCCL, "host all-gather callback failed (%zu bytes)", bytes);
+  if (dev_recv)
+    GEAR_CUDA(cudaMemcpy(recv, hr.data(), bytes * (size_t)c->nranks, cudaMemcpyHostToDevice));
+  return GEAR_OK;
+}
+
 gear_status allgather_bytes(gear_comm* c, const void* send, void* recv, size_t bytes,
                             cudaStream_t s) {
   if (c == nullptr || c->nranks == 1) {
     if (send != recv) GEAR_CUDA(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, s));
     return GEAR_OK;
   }
+  if (c->host_ag) return host_allgather(c, send, recv, bytes, s);
   GEAR_NCCL(ncclAllGather(send, recv, bytes, ncclUint8, c->nccl, s));
   return GEAR_OK;
 }
 
 gear_status barrier(gear_comm* c) {
   if (c == nullptr || c->nranks == 1) return GEAR_OK;
+  if (c->host_ag) {
+    GEAR_CUDA(cudaDeviceSynchronize());
+    uint8_t one = 1;
+    std::vector<uint8_t> all((size_t)c->nranks);
+    if (c->host_ag(c->host_ctx, &one, all.data(), 1) != 0)
+      return set_error(GEAR_ERR_NCCL, "host all-gather callback failed (barrier)");
+    return GEAR_OK;
+  }
   int* d = nullptr;
   GEAR_CUDA(cudaMallocAsync(&d, sizeof(int), c->stream));
   GEAR_CUDA(cudaMemsetAsync(d, 0, sizeof(int), c->stream));
@@ -114,6 +156,44 @@ gear_status gear_comm_create(int nranks, int rank, const uint8_t id[128], int de
     delete c;
     return gear::set_error(GEAR_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
   }
+  *out = c;
+  return GEAR_OK;
+}
+
+gear_status gear_comm_create_host(int nranks, int rank, int device, gear_allgather_fn fn,
+                                  void* ctx, gear_comm** out) {
+  gear::clear_error();
+  if (out == nullptr || fn == nullptr || nranks < 1 || nranks > gear::kMaxRanks || rank < 0 ||
+      rank >= nranks || device < 0)
+    return gear::set_error(GEAR_ERR_INVALID_ARG, "bad comm arguments (nranks=%d rank=%d)",
+                           nranks, rank);
+  GEAR_CUDA(cudaSetDevice(device));
+  auto* c = new gear_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  c->host_ag = fn;
+  c->host_ctx = ctx;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return gear::set_error(GEAR_ERR_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e));
+  }
+  // every rank agrees on nranks (a mismatch would hang the first exchange)
+  std::vector<int32_t> all((size_t)nranks);
+  int32_t mine = nranks;
+  if (fn(ctx, &mine, all.data(), sizeof(mine)) != 0) {
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return gear::set_error(GEAR_ERR_NCCL, "host all-gather callback failed (bootstrap)");
+  }
+  for (int r = 0; r < nranks; ++r)
+    if (all[r] != nranks) {
+      cudaStreamDestroy(c->stream);
+      delete c;
+      return gear::set_error(GEAR_ERR_INVALID_ARG, "rank %d passed nranks=%d, this rank %d", r,
+                             all[r], nranks);
+    }
   *out = c;
   return GEAR_OK;
 }

@@ -17,6 +17,10 @@ struct gear_comm {
   int rank = 0;
   int device = 0;
   cudaStream_t stream = nullptr;  // for create-time exchanges
+  // gear_comm_create_host: no NCCL; create-time plumbing and the peer_xchg = 0
+  // exchanges go through the caller's host all-gather
+  gear_allgather_fn host_ag = nullptr;
+  void* host_ctx = nullptr;
 };
 
 namespace gear {

@@ -343,9 +343,18 @@ def main():
     W = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
     local = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    comm = gear.comm_from_torch_distributed(local)
+    shared = os.environ.get("GEAR_SHARED_DEVICE", "0") == "1"
+    if shared:
+        # every rank on cuda:0, bootstrapped through gloo (NCCL refuses two
+        # ranks on one device): the same mailbox / IPC / shared-shm device path
+        local = 0
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+        comm = gear.comm_from_process_group(0)
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm = gear.comm_from_torch_distributed(local)
     D, H = gear.GEAR_DEVICE, gear.GEAR_HOST
     cases = [(1, [D, D, D], 0, 1), (2, [D, D, D], 1, 1), (1, [H, H, H], 0, 1),
              (2, [D, H, D], 0, 1), (1, [D, D, D], 0, 0), (2, [D, H, D], 1, 0)]
@@ -364,7 +373,8 @@ def main():
         print("case random collective sequences: ok", flush=True)
     gear.gear_comm_destroy(comm)
     dist.destroy_process_group()
-    print(f"rank {rank}: all multi-GPU parity cases ok", flush=True)
+    print(f"rank {rank}: all multi-GPU parity cases ok ({'shared device, host bootstrap' if shared else 'one GPU per rank, NCCL bootstrap'})",
+          flush=True)
 
 
 if __name__ == "__main__":

@@ -1,5 +1,17 @@
-"""Multi-GPU parity through torchrun (NCCL, NVLink P2P, shared host shards).
-Runs only where at least 2 GPUs are visible (gpurun --gpus 2|4)."""
+"""Multi-rank parity of the W > 1 device path through torchrun.
+
+* test_multi_gpu_parity: one GPU per rank, NCCL bootstrap (gear_comm_create);
+  runs where at least n GPUs are visible (gpurun --gpus 2|4).
+* test_shared_device_parity: n rank processes on the ONE visible GPU,
+  bootstrapped through a gloo group (gear_comm_create_host).  CUDA-IPC
+  mappings and POSIX shared memory work between processes on one device, so
+  the per-step mailbox exchanges (shard totals, update records, FIFO / TopK
+  candidates), the search of the owner's CDF through its IPC mapping, the
+  peer-HBM collect rows and the shared host shards all run the same code as
+  on n GPUs (kernels of different processes are time-sliced, so this is a
+  correctness run, not a performance one).  Both compare every rank's slice
+  with the unsharded CPU oracle.
+"""
 import os
 import subprocess
 import sys
@@ -18,13 +30,25 @@ def _ngpus():
         return 0
 
 
+def _run(n, port, env_extra):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tests", "dist_gpu_parity.py")]
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT, env=env)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0
+    assert r.stdout.count("all multi-GPU parity cases ok") == n
+
+
 @pytest.mark.parametrize("n", [2, 4])
 def test_multi_gpu_parity(n):
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "dist_gpu_parity.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
-    print(r.stdout[-4000:], r.stderr[-4000:])
-    assert r.returncode == 0
-    assert r.stdout.count("all multi-GPU parity cases ok") == n
+    _run(n, 29533 + n, {"GEAR_SHARED_DEVICE": "0"})
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_shared_device_parity(n):
+    if _ngpus() < 1:
+        pytest.skip("needs a GPU")
+    _run(n, 29543 + n, {"GEAR_SHARED_DEVICE": "1", "CUDA_VISIBLE_DEVICES": os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0]})
