@@ -106,7 +106,7 @@ typedef enum {
   GEAR_TOPK = 5
 } gear_strategy;
 
-/* Flag OR-ed into the strategy of gear_sample: owner-affine assignment of
+/* Bit of gear_sample's `flags`: owner-affine assignment of
  * the same global batch (Q19; data locality, "the
  * majority of the trajectories collected by the servers reside in local
  * memory").  Instead of the contiguous positions [r*B, (r+1)*B), rank r keeps
@@ -116,7 +116,7 @@ typedef enum {
  * each rank mostly collects rows from its own HBM instead of over NVLink. */
 #define GEAR_SAMPLE_OWNER_AFFINE 0x100
 
-/* Flag OR-ed into the strategy of gear_sample: the draw key is the table's
+/* Bit of gear_sample's `flags`: the draw key is the table's
  * device-resident seed counter instead of the `seed` argument, and the call
  * advances the counter on the device (set it with gear_table_set_tuning(t,
  * "device_seed", value)).  Consecutive calls use value, value+1, ... even when
@@ -147,7 +147,8 @@ typedef struct {
   gear_removal removal;        /* victim rule of gear_insert when a shard is full */
   uint32_t shards_per_rank;    /* R (0 -> 1); W*R <= 32.  R > 1 emulates a
                                   larger world on fewer GPUs (tests). */
-  uint32_t max_batch;          /* upper bound of B and of per-call n (0 -> 4096) */
+  uint32_t max_batch;          /* upper bound of B and of per-call n (0 -> 4096);
+                                  W * max_batch < 2^24 */
   double priority_alpha;       /* PER exponent alpha (Schaul et al.; Q7):
                                   every priority p of gear_insert and
                                   gear_update_priorities becomes the key
@@ -344,11 +345,12 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
  *  memory (copied at the end of the call).
  *  TOPK: the W*B selectable trajectories with the largest keys, ties by the
  *  smaller global id, in that order (reading Q20; W*B <= 8192).
- *  Flags OR-ed into `strategy`: GEAR_SAMPLE_OWNER_AFFINE, GEAR_SAMPLE_DEVICE_SEED.
+ *  flags: 0 or GEAR_SAMPLE_OWNER_AFFINE | GEAR_SAMPLE_DEVICE_SEED (other
+ *  bits: INVALID_ARG); same value on every rank.
  *  Nothing selectable: outputs get GEAR_IDX_NONE and EMPTY is latched. */
 gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint64_t seed,
                         double beta, uint64_t* out_idx, float* out_w, double* out_p,
-                        uint32_t* out_gen, gear_stream stream);
+                        uint32_t* out_gen, uint32_t flags, gear_stream stream);
 
 /* Gather rows of ncols columns for n global ids into contiguous batches,
  * rows in request order.  out[c] is a device buffer of
@@ -394,22 +396,11 @@ gear_status gear_table_load(gear_table* t, const char* path);
  *   "update_fused": 1 = priority updates of <= 8192 entries (all ranks) run
  *                   tag + apply in one single-CTA launch (default), 0 = two
  *                   grid-wide launches;
- *   "collect_dynamic": 1 = the bulk pipeline claims its tasks from a counter
- *                   (dynamic load balance) instead of a static stride
- *                   (measured 1-3% slower; default 0);
- *   "tma_ooo":      1 = the bulk pipeline stores its stages in completion
- *                   order instead of ring order (measured 2% slower at c2;
- *                   default 0);
  *   "collect_peer_lsu": W > 1: 1 = the peer-HBM rows of bulk-copied (TMA)
  *                   columns are moved by the LSU warps instead of the bulk
  *                   pipeline (+3% collect throughput when few rows are
  *                   remote, -11% when half are); 0 = all by the bulk
  *                   pipeline (default);
- *   "collect_permute": 1 = gear_collect visits the requested rows in the
- *                   order j*m mod n (m coprime with n, near n/phi) so that
- *                   peer / host rows that sit together in the request overlap
- *                   local HBM rows; 0 = request order (default: measured 2%
- *                   faster at c2 on 1 and 2 GPUs); the output is the same;
  *   "cdf_levels":   same value on every rank; 2 = two-level CDF (default):
  *                   every 4096-key tile of a shard holds its own prefix sum,
  *                   the shard a prefix sum of the tile totals, and a rebuild

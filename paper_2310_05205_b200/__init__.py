@@ -106,7 +106,7 @@ SIGNATURES = {
     "gear_commit": ([_P, _u32, _u32, _P, _P, _P], _i32),
     "gear_column_base": ([_P, _u32, _P], _i32),
     "gear_update_priorities": ([_P, _u32, _P, _P, _i32, _P, _P], _i32),
-    "gear_sample": ([_P, _i32, _u32, _u64, _f64, _P, _P, _P, _P, _P], _i32),
+    "gear_sample": ([_P, _i32, _u32, _u64, _f64, _P, _P, _P, _P, _u32, _P], _i32),
     "gear_collect": ([_P, _u32, _P, _u32, _P, _P, _P], _i32),
     "gear_table_sync": ([_P, _P, _P], _i32),
     "gear_read_state": ([_P, _P, _P, _P], _i32),
@@ -152,6 +152,38 @@ def _ptr(x) -> int | None:
         assert x.is_contiguous(), "tensors must be contiguous"
         return x.data_ptr()
     raise TypeError(f"cannot take the address of {type(x)}")
+
+
+_I64 = ("int64", "uint64")
+_I32 = ("int32", "uint32")
+
+
+def _dtype_name(x) -> str:
+    return str(x.dtype).replace("torch.", "")
+
+
+def _arg(x, kinds, name: str, n: int = 0, fn: str = "") -> int | None:
+    """_ptr(x) after checking that a tensor / array argument has one of the
+    dtypes `kinds` and at least n elements (a wrong dtype would make the
+    kernels read or write past the buffer).  Raw integer addresses are the
+    caller's responsibility."""
+    if x is None or isinstance(x, int):
+        return _ptr(x)
+    dt = _dtype_name(x)
+    if dt not in kinds:
+        raise TypeError(f"{fn}: {name} must have dtype {' or '.join(kinds)}, got {dt}")
+    numel = x.numel() if hasattr(x, "numel") and callable(x.numel) else x.size
+    if numel < n:
+        raise ValueError(f"{fn}: {name} has {numel} elements, the call needs {n}")
+    return _ptr(x)
+
+
+def _nbytes(x) -> int | None:
+    if isinstance(x, int) or x is None:
+        return None
+    if hasattr(x, "element_size"):
+        return x.numel() * x.element_size()
+    return x.nbytes
 
 
 def _stream(stream) -> int | None:
@@ -302,19 +334,28 @@ def gear_column_row_bytes(t: int, col: int) -> int:
 
 
 def gear_insert(t: int, shard: int, n: int, col_src: Sequence, prio, out_idx=None, stream=None):
+    for c, src in enumerate(col_src):
+        nb = _nbytes(src)
+        if nb is not None and nb < n * gear_column_row_bytes(t, c):
+            raise ValueError(f"gear_insert: col_src[{c}] has {nb} bytes, {n} rows need "
+                             f"{n * gear_column_row_bytes(t, c)}")
     srcs = (ctypes.c_void_p * len(col_src))(*[_ptr(s) for s in col_src])
     prio = np.ascontiguousarray(prio, dtype=np.float64) if not hasattr(prio, "data_ptr") else prio
-    _check("gear_insert", load().gear_insert(t, shard, n, srcs, _ptr(prio), _ptr(out_idx),
+    _check("gear_insert", load().gear_insert(t, shard, n, srcs, _arg(prio, ("float64",), "prio", n, "gear_insert"),
+                                             _arg(out_idx, _I64, "out_idx", n, "gear_insert"),
                                              _stream(stream)))
 
 
 def gear_allocate(t: int, shard: int, n: int, out_idx, stream=None):
-    _check("gear_allocate", load().gear_allocate(t, shard, n, _ptr(out_idx), _stream(stream)))
+    _check("gear_allocate", load().gear_allocate(t, shard, n, _arg(out_idx, _I64, "out_idx", n, "gear_allocate"),
+                                                 _stream(stream)))
 
 
 def gear_commit(t: int, shard: int, n: int, idx, prio, stream=None):
     prio = np.ascontiguousarray(prio, dtype=np.float64) if not hasattr(prio, "data_ptr") else prio
-    _check("gear_commit", load().gear_commit(t, shard, n, _ptr(idx), _ptr(prio), _stream(stream)))
+    _check("gear_commit", load().gear_commit(t, shard, n, _arg(idx, _I64, "idx", n, "gear_commit"),
+                                             _arg(prio, ("float64",), "prio", n, "gear_commit"),
+                                             _stream(stream)))
 
 
 def gear_column_base(t: int, col: int) -> int:
@@ -324,22 +365,39 @@ def gear_column_base(t: int, col: int) -> int:
 
 
 def gear_update_priorities(t: int, n: int, idx, prio, prio_dtype: int, gen=None, stream=None):
-    _check("gear_update_priorities",
-           load().gear_update_priorities(t, n, _ptr(idx), _ptr(prio), prio_dtype, _ptr(gen),
-                                         _stream(stream)))
+    f = "gear_update_priorities"
+    pk = {GEAR_F64: ("float64",), GEAR_F32: ("float32",)}.get(prio_dtype)
+    pp = _arg(prio, pk, "prio", n, f) if pk else _ptr(prio)   # other dtypes: the C-ABI rejects them
+    _check(f, load().gear_update_priorities(t, n, _arg(idx, _I64, "idx", n, f), pp,
+                                            prio_dtype, _arg(gen, _I32, "gen", n, f), _stream(stream)))
 
 
 def gear_sample(t: int, strategy: int, B: int, seed: int, beta: float, out_idx, out_w=None,
-                out_p=None, out_gen=None, stream=None):
-    _check("gear_sample", load().gear_sample(t, strategy, B, seed, beta, _ptr(out_idx), _ptr(out_w),
-                                             _ptr(out_p), _ptr(out_gen), _stream(stream)))
+                out_p=None, out_gen=None, stream=None, flags: int = 0):
+    """strategy: GEAR_FIFO ... GEAR_TOPK; flags: GEAR_SAMPLE_* bits (for
+    compatibility, flag bits OR-ed into `strategy` are moved to `flags`)."""
+    f = "gear_sample"
+    flags |= strategy & ~0xFF
+    strategy &= 0xFF
+    _check(f, load().gear_sample(t, strategy, B, seed, beta, _arg(out_idx, _I64, "out_idx", B, f),
+                                 _arg(out_w, ("float32",), "out_w", B, f),
+                                 _arg(out_p, ("float64",), "out_p", B, f),
+                                 _arg(out_gen, _I32, "out_gen", B, f), flags, _stream(stream)))
 
 
 def gear_collect(t: int, n: int, idx, col_ids: Sequence[int], out: Sequence, stream=None):
+    f = "gear_collect"
+    if len(col_ids) != len(out):
+        raise ValueError(f"{f}: {len(col_ids)} column ids but {len(out)} outputs")
+    for c, o in zip(col_ids, out):
+        nb = _nbytes(o)
+        if nb is not None and nb < n * gear_column_row_bytes(t, c):
+            raise ValueError(f"{f}: output of column {c} has {nb} bytes, {n} rows need "
+                             f"{n * gear_column_row_bytes(t, c)}")
     ids = (ctypes.c_uint32 * len(col_ids))(*col_ids)
     outs = (ctypes.c_void_p * len(out))(*[_ptr(o) for o in out])
-    _check("gear_collect", load().gear_collect(t, n, _ptr(idx), len(col_ids), ids, outs,
-                                               _stream(stream)))
+    _check(f, load().gear_collect(t, n, _arg(idx, _I64, "idx", n, f), len(col_ids), ids, outs,
+                                  _stream(stream)))
 
 
 def gear_table_sync(t: int) -> tuple[int, int]:
@@ -409,11 +467,14 @@ class Table:
         return gear_column_base(self.handle, col)
 
     def update_priorities(self, idx, prio, gen=None, stream=None):
-        dt = GEAR_F64 if str(getattr(prio, "dtype", "")).endswith("float64") else GEAR_F32
+        dt = {"float64": GEAR_F64, "float32": GEAR_F32}.get(_dtype_name(prio))
+        if dt is None:
+            raise TypeError(f"priorities must be float32 or float64, got {_dtype_name(prio)}")
         gear_update_priorities(self.handle, len(idx), idx, prio, dt, gen, stream)
 
-    def sample(self, strategy, B, seed, beta, out_idx, out_w=None, out_p=None, out_gen=None, stream=None):
-        gear_sample(self.handle, strategy, B, seed, beta, out_idx, out_w, out_p, out_gen, stream)
+    def sample(self, strategy, B, seed, beta, out_idx, out_w=None, out_p=None, out_gen=None, stream=None,
+               flags=0):
+        gear_sample(self.handle, strategy, B, seed, beta, out_idx, out_w, out_p, out_gen, stream, flags)
 
     def collect(self, idx, col_ids, out, stream=None):
         gear_collect(self.handle, len(idx), idx, col_ids, out, stream)

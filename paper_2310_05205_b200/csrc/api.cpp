@@ -199,7 +199,7 @@ void destroy_table(gear_table* t) {
   dfree(t->n_stale); dfree(t->err); dfree(t->d_epoch); dfree(t->d_seed); dfree(t->d_xep);
   for (auto& b : t->col_idx) dfree(b.p);
   dfree(t->d_meta); dfree(t->d_ord); dfree(t->d_out); dfree(t->d_rows);
-  dfree(t->d_prio_ins); dfree(t->d_alloc); dfree(t->ins_bad); dfree(t->dyn_pool);
+  dfree(t->d_prio_ins); dfree(t->d_alloc); dfree(t->ins_bad);
   if (t->h_prio) cudaFreeHost(t->h_prio);
   if (t->h_out) cudaFreeHost(t->h_out);
   if (t->staging_ev) cudaEventDestroy(t->staging_ev);
@@ -237,15 +237,14 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   if (t->removal != GEAR_REMOVE_FIFO && t->removal != GEAR_REMOVE_LIFO)
     return set_error(GEAR_ERR_INVALID_ARG, "bad removal");
   t->max_batch = d->max_batch ? d->max_batch : 4096;
+  if ((uint64_t)t->W * t->max_batch >= (1ull << kTagLowBits))
+    return set_error(GEAR_ERR_INVALID_ARG, "W * max_batch must be < 2^%d", kTagLowBits);
   if (d->seq_len == 0) return set_error(GEAR_ERR_INVALID_ARG, "seq_len == 0");
   if (d->ncols == 0 || d->ncols > (uint32_t)kMaxCols || d->cols == nullptr)
     return set_error(GEAR_ERR_INVALID_ARG, "ncols must be 1..%d", kMaxCols);
   if (const char* e = getenv("GEAR_COLLECT_CHUNK")) t->chunk_bytes = (uint32_t)atoi(e);
   if (const char* e = getenv("GEAR_TMA_CHUNK")) t->tma_chunk = (uint32_t)atoi(e);
-  if (const char* e = getenv("GEAR_COLLECT_PERMUTE")) t->collect_permute = atoi(e) != 0;
   if (const char* e = getenv("GEAR_COLLECT_PEER_LSU")) t->collect_peer_lsu = atoi(e) != 0;
-  if (const char* e = getenv("GEAR_TMA_OOO")) t->tma_ooo = atoi(e) != 0;
-  if (const char* e = getenv("GEAR_COLLECT_DYNAMIC")) t->collect_dynamic = atoi(e) != 0;
   if (const char* e = getenv("GEAR_TMA_STAGES")) {
     const int v = atoi(e);
     if (v == 2 || v == 3 || v == 4 || v == 6 || v == 8) t->tma_stages = v;
@@ -287,6 +286,30 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
     cs.placement = cd.placement;
     cs.rb = elems * dtype_size(cd.dtype);
     cs.bytes_local = cs.rb * t->Clocal;
+  }
+  // schema hash (checkpoints): FNV-1a 64 over little-endian field encodings
+  t->seq_len = d->seq_len;
+  {
+    uint64_t h = 0xcbf29ce484222325ull;
+    auto mix = [&h](uint64_t v, int nbytes) {
+      for (int b = 0; b < nbytes; ++b) {
+        h ^= (v >> (8 * b)) & 0xff;
+        h *= 0x100000001b3ull;
+      }
+    };
+    mix(d->seq_len, 4);
+    mix(d->ncols, 4);
+    for (uint32_t c = 0; c < d->ncols; ++c) {
+      const gear_column_desc& cd = d->cols[c];
+      const size_t L = strlen(cd.name);
+      mix(L, 4);
+      for (size_t k = 0; k < L; ++k) mix((uint8_t)cd.name[k], 1);
+      mix((uint32_t)cd.dtype, 4);
+      mix(cd.ndim, 4);
+      for (uint32_t k = 0; k < cd.ndim; ++k) mix((uint64_t)cd.shape[k], 8);
+      mix((uint32_t)cd.placement, 4);
+    }
+    t->schema_hash = h;
   }
 
   // A per-table tag for shared-memory names (rank 0 draws it, all-gathered).
@@ -476,7 +499,7 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_TRY(dalloc(&t->d_xep, 4));
   GEAR_CUDA(cudaMemset(t->d_xep, 0, 32));
   GEAR_TRY(dalloc(&t->d_epoch, 1));
-  GEAR_CUDA(cudaMemset(t->d_epoch, 0, 4));
+  GEAR_CUDA(cudaMemset(t->d_epoch, 0, 8));
   GEAR_TRY(dalloc(&t->d_seed, 1));
   GEAR_CUDA(cudaMemset(t->d_seed, 0, 8));
   GEAR_TRY(dalloc(&t->n_stale, 1));
@@ -488,8 +511,6 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_TRY(dalloc(&t->d_prio_ins, MB));
   GEAR_TRY(dalloc(&t->d_alloc, t->R));
   GEAR_TRY(dalloc(&t->ins_bad, 1));
-  GEAR_TRY(dalloc(&t->dyn_pool, 2 * gear_table::kDynSlots));
-  GEAR_CUDA(cudaMemset(t->dyn_pool, 0, 2 * gear_table::kDynSlots * 8));
   GEAR_CUDA(cudaMemset(t->ins_bad, 0, 4));
   {
     std::vector<AllocState> a0(t->R);
@@ -723,11 +744,9 @@ gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* c
     cp.ncols = (uint32_t)t->cols.size();
     cp.n = n_meta;
     cp.err = t->err;
-    cp.row_mult = 1;
     cp.self_rank = t->rank;
     cp.tma_ctas_per_sm = (uint32_t)t->tma_ctas;
     cp.tma_stages = (uint32_t)t->tma_stages;
-    cp.tma_ooo = (uint32_t)t->tma_ooo;
     for (size_t c = 0; c < t->cols.size(); ++c) {
       ColumnState& cs = t->cols[c];
       const uint8_t* src = (const uint8_t*)col_src[c] + (uint64_t)k0 * cs.rb;
@@ -856,18 +875,18 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
 
 gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint64_t seed,
                         double beta, uint64_t* out_idx, float* out_w, double* out_p,
-                        uint32_t* out_gen, gear_stream stream) {
+                        uint32_t* out_gen, uint32_t flags, gear_stream stream) {
   clear_error();
   GEAR_TRY(check_table(t));
   GEAR_CUDA(cudaSetDevice(t->device));
   cudaStream_t s = (cudaStream_t)stream;
+  if (flags & ~(uint32_t)(GEAR_SAMPLE_OWNER_AFFINE | GEAR_SAMPLE_DEVICE_SEED))
+    return set_error(GEAR_ERR_INVALID_ARG, "unknown sample flags 0x%x", flags);
   // With one rank every entry is local: the owner-affine slice is the
   // contiguous one, so the assignment kernel is skipped.
-  const bool affine = ((uint32_t)strategy & GEAR_SAMPLE_OWNER_AFFINE) != 0 && t->W > 1;
-  const bool dseed = ((uint32_t)strategy & GEAR_SAMPLE_DEVICE_SEED) != 0;
-  strategy = (gear_strategy)((uint32_t)strategy &
-                             ~(uint32_t)(GEAR_SAMPLE_OWNER_AFFINE | GEAR_SAMPLE_DEVICE_SEED));
-  if (strategy < GEAR_FIFO || strategy > GEAR_TOPK)
+  const bool affine = (flags & GEAR_SAMPLE_OWNER_AFFINE) != 0 && t->W > 1;
+  const bool dseed = (flags & GEAR_SAMPLE_DEVICE_SEED) != 0;
+  if ((int)strategy < GEAR_FIFO || (int)strategy > GEAR_TOPK)
     return set_error(GEAR_ERR_INVALID_ARG, "bad strategy %d", (int)strategy);
   if (B > t->max_batch) return set_error(GEAR_ERR_INVALID_ARG, "B %u > max_batch %u", B, t->max_batch);
   if (B == 0) return GEAR_OK;
@@ -1097,19 +1116,9 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
   cp.ncols = ncols;
   cp.n = n;
   cp.err = t->err;
-  cp.row_mult = 1;
-  if (t->collect_permute && n > 2) {  // an odd multiplier near n/phi, coprime with n
-    uint64_t m = ((uint64_t)n * 618034ull / 1000000ull) | 1ull;
-    while (std::gcd(m, (uint64_t)n) != 1) m += 2;
-    cp.row_mult = m;
-  }
   cp.self_rank = t->rank;
-  if (t->collect_dynamic) {  // a counter pair per launch, rotating (concurrent collects differ)
-    cp.dyn_ctr = t->dyn_pool + 2 * (t->dyn_slot++ % gear_table::kDynSlots);
-  }
   cp.tma_ctas_per_sm = (uint32_t)t->tma_ctas;
   cp.tma_stages = (uint32_t)t->tma_stages;
-  cp.tma_ooo = (uint32_t)t->tma_ooo;
   for (uint32_t c = 0; c < ncols; ++c) {
     if (col_ids[c] >= t->cols.size()) return set_error(GEAR_ERR_INVALID_ARG, "bad column id %u", col_ids[c]);
     if (out[c] == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "out[%u] is NULL", c);
@@ -1182,14 +1191,8 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     GEAR_CUDA(cudaMemset(t->cdf_buf_mode, 0, 8));  // both buffers: full rebuild
     t->cdf_levels = (int)value;
     t->dirty = true;
-  } else if (!strcmp(key, "collect_dynamic") && (value == 0 || value == 1)) {
-    t->collect_dynamic = (int)value;
-  } else if (!strcmp(key, "tma_ooo") && (value == 0 || value == 1)) {
-    t->tma_ooo = (int)value;
   } else if (!strcmp(key, "collect_peer_lsu") && (value == 0 || value == 1)) {
     t->collect_peer_lsu = (int)value;
-  } else if (!strcmp(key, "collect_permute") && (value == 0 || value == 1)) {
-    t->collect_permute = (int)value;
   } else if (!strcmp(key, "update_fused") && (value == 0 || value == 1)) {
     t->update_fused = (int)value;
   } else if (!strcmp(key, "tma_ctas_per_sm") && value >= 1 && value <= 8 &&

@@ -23,6 +23,18 @@ constexpr uint32_t kErrEmpty = 8u;
 constexpr uint32_t kErrTimeout = 16u;
 constexpr uint32_t kErrFull = 32u;
 
+// Last-writer-wins tags of the update / commit passes (kernels/update.cu,
+// alloc.cu): tag = epoch << 24 | low, low = an entry's rank in its call
+// (< 2^24: create checks W * max_batch < 2^24).  The epoch is a 40-bit
+// device counter advanced once per update / commit call, so tags of earlier
+// calls compare smaller and the tag array never needs clearing; it wraps
+// after 2^40 calls (~4.8 years at 7,300 calls/s).
+constexpr int kTagLowBits = 24;
+constexpr uint32_t kTagLowMax = (1u << kTagLowBits) - 1;
+__host__ __device__ __forceinline__ unsigned long long make_tag(uint64_t epoch, uint32_t low) {
+  return ((unsigned long long)epoch << kTagLowBits) | (unsigned long long)low;
+}
+
 // Strategy codes (mirror gear_strategy).
 constexpr int kFifo = 0, kLifo = 1, kUniform = 2, kWeighted = 3, kPrioritized = 4;
 
@@ -184,11 +196,8 @@ struct CollectParams {
   uint32_t n_tma;
   uint32_t tma_ctas_per_sm;           // CTAs of the TMA kernel per SM
   uint32_t tma_stages;                // 2, 3, 4, 6 or 8 shared-memory stages per CTA
-  uint32_t tma_ooo;                   // 1: stages stored in completion order
-  unsigned long long* dyn_ctr;        // non-null: TMA tasks claimed from this counter pair
   uint32_t ncols;
   uint32_t n;
-  uint64_t row_mult;                  // row visiting order j -> j*row_mult mod n (1: in order)
   uint32_t self_rank;                 // this rank (peer rows: owner != self_rank)
   uint32_t any_peer_lsu;              // some column has peer_lsu
   uint32_t* err;
@@ -290,12 +299,12 @@ cudaError_t launch_update_quantize(const uint64_t* idx, const void* prio, int pr
                                    uint32_t* err, cudaStream_t s);
 cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                               uint64_t local_rows, const uint32_t* gen, const uint64_t* seq, unsigned long long* tag,
-                              uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err,
+                              uint64_t* epoch_dev, unsigned long long* n_stale, uint32_t* err,
                               cudaStream_t s);
 cudaError_t launch_update_apply(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                                 uint64_t local_rows, const uint32_t* gen,
                                const uint64_t* seq,
-                                const unsigned long long* tag, uint32_t* epoch_dev, uint64_t* key,
+                                const unsigned long long* tag, uint64_t* epoch_dev, uint64_t* key,
                                 TileDirty td, cudaStream_t s);
 
 // Single-launch update for m <= update_fused_max() entries (one CTA): raw
@@ -306,7 +315,7 @@ cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_
                                 uint64_t n_global, Quant qz,
                                 uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
                                const uint64_t* seq,
-                                unsigned long long* tag, uint32_t* epoch_dev,
+                                unsigned long long* tag, uint64_t* epoch_dev,
                                 unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                 TileDirty td, cudaStream_t s);
 
@@ -317,7 +326,7 @@ cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_i
                                Quant qz, const Mbox& mb,
                                uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
                                const uint64_t* seq,
-                               unsigned long long* tag, uint32_t* epoch_dev,
+                               unsigned long long* tag, uint64_t* epoch_dev,
                                unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                TileDirty td, cudaStream_t s);
 
@@ -344,7 +353,7 @@ cudaError_t launch_allocate(AllocState* st, uint32_t ls, uint32_t shard, uint64_
 cudaError_t launch_commit(AllocState* st, uint32_t ls, uint32_t shard, uint64_t Cs, uint32_t n,
                           const uint64_t* idx, const double* prio, Quant qz, uint64_t* key,
                           uint64_t* seq, const uint32_t* gen, uint32_t* ord,
-                          unsigned long long* tag, uint32_t* epoch_dev, TileDirty td,
+                          unsigned long long* tag, uint64_t* epoch_dev, TileDirty td,
                           uint32_t* err, cudaStream_t s);
 
 // K4: FIFO/LIFO local selection and merge (ring state read from `alloc`).

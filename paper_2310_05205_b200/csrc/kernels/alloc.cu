@@ -190,11 +190,11 @@ __global__ void __launch_bounds__(kThreads)
     commit_kernel(AllocState* st, uint32_t ls, uint32_t shard, uint64_t Cs, uint32_t n,
                   const uint64_t* __restrict__ idx, const double* __restrict__ prio, Quant qz,
                   uint64_t* key, uint64_t* seq, const uint32_t* __restrict__ gen, uint32_t* ord,
-                  unsigned long long* tag, uint32_t* epoch_dev, TileDirty td, uint32_t* err) {
+                  unsigned long long* tag, uint64_t* epoch_dev, TileDirty td, uint32_t* err) {
   __shared__ uint32_t s_warp[kThreads / 32];
   __shared__ uint32_t s_err;
   const AllocState a = st[ls];
-  const uint32_t epoch = *epoch_dev + 1;  // shares the update's tag epochs
+  const uint64_t epoch = *epoch_dev + 1;  // shares the update's tag epochs
   const uint64_t base = (uint64_t)ls * Cs;
   const uint64_t g0 = (uint64_t)shard * Cs;
   if (threadIdx.x == 0) s_err = 0;
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kThreads)
     if (g < g0 || g >= g0 + Cs) continue;
     const uint64_t local = base + (g - g0);
     if (gen[local] == 0 || seq[local] != 0) continue;
-    atomicMax(tag + local, ((unsigned long long)epoch << 32) | (0xffffffffu - k));
+    atomicMax(tag + local, make_tag(epoch, kTagLowMax - k));
   }
   __syncthreads();
   // Pass 2: in order, the valid entries get consecutive seq and ring slots.
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kThreads)
       } else {
         local = base + (g - g0);
         if (gen[local] == 0 || seq[local] != 0 ||
-            __ldcg(tag + local) != (((unsigned long long)epoch << 32) | (0xffffffffu - k)))
+            __ldcg(tag + local) != (make_tag(epoch, kTagLowMax - k)))
           e = kErrStale;
         else if (!quantize(prio[k], qz, &q))
           e = kErrBadPriority;
@@ -287,7 +287,7 @@ cudaError_t launch_allocate(AllocState* st, uint32_t ls, uint32_t shard, uint64_
 cudaError_t launch_commit(AllocState* st, uint32_t ls, uint32_t shard, uint64_t Cs, uint32_t n,
                           const uint64_t* idx, const double* prio, Quant qz, uint64_t* key,
                           uint64_t* seq, const uint32_t* gen, uint32_t* ord,
-                          unsigned long long* tag, uint32_t* epoch_dev, TileDirty td,
+                          unsigned long long* tag, uint64_t* epoch_dev, TileDirty td,
                           uint32_t* err, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   count_launch();

@@ -47,6 +47,10 @@ __global__ void __launch_bounds__(kThreads) assign_kernel(const __grid_constant_
     const MboxLayout L = mbox_layout(mm.W, mm.S, mm.MB);
     fifo_totals = mbox_at<ShardTotals>(mm, mm.rank, L.ccnt) + mbox_buf(mm) * mm.S;
   }
+  if (p.xchg && totals == nullptr) {  // timed out: the sample kernel writes GEAR_IDX_NONE
+    for (uint32_t b = tid; b < B; b += kThreads) p.draw_list[b] = p.rank * B + b;
+    return;
+  }
   if (tid < 32) {
     uint64_t Ts = 0;
     if ((uint32_t)lane < S && totals)
@@ -61,7 +65,7 @@ __global__ void __launch_bounds__(kThreads) assign_kernel(const __grid_constant_
     if (fifo_totals) {  // FIFO/LIFO: fewer than K candidates -> EMPTY (merge wrote it)
       uint64_t avail = 0;
       for (uint32_t s = 0; s < S; ++s) avail += __ldcg(&fifo_totals[s].aux);
-      s_bail = avail < K;
+      s_bail = avail < K || (p.fifo_mbox && mbox_failed(p.err));  // timed out: likewise
     }
   }
   __syncthreads();

@@ -87,11 +87,7 @@ __device__ __forceinline__ void decode_task(const CollectParams& p, const uint8_
   const uint64_t rel = task - p.col[c].chunk_begin;
   const uint64_t jt = rel / p.col[c].chunks_per_row;
   *c_out = c;
-  // Rows are visited in the order jt * row_mult mod n (row_mult coprime with
-  // n): rows of one kind that sit together in the request -- e.g. the peer
-  // rows an owner-affine slice puts last -- are spread over the whole launch,
-  // so NVLink / PCIe reads overlap local HBM reads instead of forming a tail.
-  *j_out = p.row_mult > 1 ? (jt * p.row_mult) % p.n : jt;
+  *j_out = jt;
   *k_out = rel - jt * p.col[c].chunks_per_row;
 }
 
@@ -261,119 +257,7 @@ __device__ __forceinline__ void bulk_wait_read(uint32_t n) {
   }
 }
 
-// Out-of-order variant of the issuing lane's ring (tuning "tma_ooo"): a stage
-// is stored as soon as ITS load lands, whichever stage that is, so one slow
-// chunk (a peer row over NVLink, a far DRAM page) no longer holds up the
-// stages behind it.  Stages whose store was issued are recycled in store
-// order: wait_group.read (pending - 1) frees the oldest.
 template <int kStages>
-__device__ __forceinline__ void tma_lane_ooo(const CollectParams& p, uint32_t base,
-                                             uint64_t* bars, uint32_t stage_bytes) {
-  const uint64_t first = blockIdx.x, step = gridDim.x;
-  const uint64_t ntask = p.tma_total > first ? (p.tma_total - first + step - 1) / step : 0;
-  uint8_t* dst[kStages] = {};
-  uint32_t nbytes[kStages] = {};
-  uint32_t phase = 0, loading = 0;  // bit s: stage s has a load in flight
-  int fifo[kStages];                // stages with a store pending, oldest first
-  uint32_t fh = 0, fn = 0;
-  uint64_t next = 0, done = 0;
-  uint32_t free_mask = (1u << kStages) - 1u;
-  while (done < ntask) {
-    // refill: a free stage, else the stage of the oldest pending store
-    while (next < ntask && (free_mask || fn)) {
-      int s;
-      if (free_mask) {
-        s = __ffs(free_mask) - 1;
-        free_mask &= free_mask - 1;
-      } else {
-        bulk_wait_read(fn - 1);  // the oldest store has read its stage
-        s = fifo[fh];
-        fh = (fh + 1) % kStages;
-        --fn;
-      }
-      nbytes[s] = tma_issue_load(p, first + next * step, base + (uint32_t)s * stage_bytes,
-                                 smem_u32(&bars[s]), &dst[s]);
-      loading |= 1u << s;
-      ++next;
-    }
-    // store every stage whose load has landed
-    for (int s = 0; s < kStages; ++s) {
-      if (!((loading >> s) & 1u)) continue;
-      if (!mbar_try_wait(smem_u32(&bars[s]), (phase >> s) & 1u)) continue;
-      phase ^= 1u << s;
-      loading &= ~(1u << s);
-      ++done;
-      if (nbytes[s]) {
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst[s]),
-                     "r"(base + (uint32_t)s * stage_bytes), "r"(nbytes[s])
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        fifo[(fh + fn) % kStages] = s;
-        ++fn;
-      } else {
-        free_mask |= 1u << s;
-      }
-    }
-  }
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-
-// Dynamic variant of the issuing lane's in-order ring: each refill claims the
-// next task from a per-launch counter instead of the static stride, so CTAs
-// slowed by co-resident kernels (the next step's selection) or by slow chunks
-// take fewer tasks.  The last CTA to finish re-arms the counter (graph-safe).
-template <int kStages>
-__device__ __forceinline__ void tma_lane_dynamic(const CollectParams& p, uint32_t base,
-                                                 uint64_t* bars, uint32_t stage_bytes) {
-  unsigned long long* ctr = p.dyn_ctr;  // [0] next task, [1] CTAs done
-  uint8_t* dst[kStages] = {};
-  uint32_t nbytes[kStages] = {};
-  uint32_t phase = 0;
-  int inflight = 0;
-  bool more = true;
-  for (int s = 0; s < kStages; ++s) {
-    const uint64_t task = atomicAdd(ctr, 1ull);
-    if (task >= p.tma_total) {
-      more = false;
-      break;
-    }
-    nbytes[s] = tma_issue_load(p, task, base + (uint32_t)s * stage_bytes, smem_u32(&bars[s]),
-                               &dst[s]);
-    ++inflight;
-  }
-  for (uint64_t n = 0; inflight > 0; ++n) {
-    const int s = (int)(n % kStages);
-    while (!mbar_try_wait(smem_u32(&bars[s]), (phase >> s) & 1u)) {
-    }
-    phase ^= 1u << s;
-    --inflight;
-    if (nbytes[s])
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst[s]),
-                   "r"(base + (uint32_t)s * stage_bytes), "r"(nbytes[s])
-                   : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    if (n >= 1 && more) {  // refill the previous stage (cyclic order is kept)
-      const int sp = (int)((n - 1) % kStages);
-      const uint64_t task = atomicAdd(ctr, 1ull);
-      if (task < p.tma_total) {
-        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        nbytes[sp] = tma_issue_load(p, task, base + (uint32_t)sp * stage_bytes,
-                                    smem_u32(&bars[sp]), &dst[sp]);
-        ++inflight;
-      } else {
-        more = false;
-      }
-    }
-  }
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  __threadfence();
-  if (atomicAdd(ctr + 1, 1ull) == gridDim.x - 1) {  // every CTA has stopped claiming
-    ctr[0] = 0;
-    ctr[1] = 0;
-  }
-}
-
-template <int kStages, bool kOoo>
 __device__ __forceinline__ void tma_body(const CollectParams& p, uint32_t stage_bytes) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[kStages];
@@ -390,14 +274,6 @@ __device__ __forceinline__ void tma_body(const CollectParams& p, uint32_t stage_
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[s])) : "memory");
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  if constexpr (kOoo) {
-    tma_lane_ooo<kStages>(p, smem_u32(smem), bars, stage_bytes);
-    return;
-  }
-  if (p.dyn_ctr != nullptr) {  // tuning "collect_dynamic": tasks claimed from a counter
-    tma_lane_dynamic<kStages>(p, smem_u32(smem), bars, stage_bytes);
-    return;
-  }
   const uint64_t first = blockIdx.x, step = gridDim.x;
   const uint64_t ntask = p.tma_total > first ? (p.tma_total - first + step - 1) / step : 0;
   const uint32_t base = smem_u32(smem);
@@ -458,27 +334,27 @@ int grid_for(K kernel, uint64_t tasks) {
   return (int)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
-template <int kStages, bool kOoo>
+template <int kStages>
 __global__ void __launch_bounds__(kTmaThreads)
     collect_tma_kernel(const __grid_constant__ CollectParams p, uint32_t stage_bytes) {
-  tma_body<kStages, kOoo>(p, stage_bytes);
+  tma_body<kStages>(p, stage_bytes);
 }
 
-template <int kStages, bool kOoo>
+template <int kStages>
 __global__ void __launch_bounds__(kTmaThreads)
     insert_rows_tma_kernel(const __grid_constant__ CollectParams p, uint32_t stage_bytes) {
-  tma_body<kStages, kOoo>(p, stage_bytes);
+  tma_body<kStages>(p, stage_bytes);
 }
 
 }  // namespace
 
 // kStages stages of tma_chunk bytes per CTA, ctas CTAs per SM (192 KB of
 // shared memory per SM either way).
-template <int kStages, bool kOoo>
+template <int kStages>
 cudaError_t launch_tma(const CollectParams& p, int ctas, cudaStream_t s) {
   const uint32_t stage_bytes = p.col[p.tma_cols[0]].chunk;
   const size_t smem = (size_t)kStages * stage_bytes;
-  auto kern = p.meta ? insert_rows_tma_kernel<kStages, kOoo> : collect_tma_kernel<kStages, kOoo>;
+  auto kern = p.meta ? insert_rows_tma_kernel<kStages> : collect_tma_kernel<kStages>;
   static size_t configured[2] = {0, 0};
   size_t& conf = configured[p.meta ? 1 : 0];
   if (smem > conf) {
@@ -495,14 +371,13 @@ cudaError_t launch_tma(const CollectParams& p, int ctas, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <bool kOoo>
 cudaError_t launch_tma_stages(const CollectParams& p, int ctas, cudaStream_t s) {
   switch (p.tma_stages) {
-    case 2: return launch_tma<2, kOoo>(p, ctas, s);
-    case 3: return launch_tma<3, kOoo>(p, ctas, s);
-    case 4: return launch_tma<4, kOoo>(p, ctas, s);
-    case 6: return launch_tma<6, kOoo>(p, ctas, s);
-    default: return launch_tma<8, kOoo>(p, ctas, s);
+    case 2: return launch_tma<2>(p, ctas, s);
+    case 3: return launch_tma<3>(p, ctas, s);
+    case 4: return launch_tma<4>(p, ctas, s);
+    case 6: return launch_tma<6>(p, ctas, s);
+    default: return launch_tma<8>(p, ctas, s);
   }
 }
 
@@ -517,7 +392,7 @@ cudaError_t launch_collect(const CollectParams& p, cudaStream_t s) {
     return cudaGetLastError();
   }
   const int ctas = (int)p.tma_ctas_per_sm;
-  return p.tma_ooo ? launch_tma_stages<true>(p, ctas, s) : launch_tma_stages<false>(p, ctas, s);
+  return launch_tma_stages(p, ctas, s);
 }
 
 cudaError_t launch_insert_meta(const InsMeta* meta, uint32_t m, const OrdRec* ord_recs,

@@ -141,8 +141,9 @@ __global__ void __launch_bounds__(kMergeThreads)
     cand_all = mbox_at<Cand>(m, m.rank, L.cand) + (uint64_t)b * m.S * K;
     totals = mbox_at<ShardTotals>(m, m.rank, L.ccnt) + b * m.S;
   }
+  const bool failed = xchg && mbox_failed(err);  // a timed-out exchange: no candidates
   uint64_t avail = 0;
-  for (uint32_t s = 0; s < S; ++s) avail += totals[s].aux;
+  for (uint32_t s = 0; s < S && !failed; ++s) avail += totals[s].aux;
   if (avail < K) {  // fewer than W*B selectable: EMPTY
     if (t < B) {
       out_idx[t] = kIdxNone;
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kMergeThreads)
       if (out_p) out_p[t] = 0.0;
       if (out_gen) out_gen[t] = 0;
     }
-    if (t == 0) atomicOr(err, kErrEmpty);
+    if (t == 0 && !failed) atomicOr(err, kErrEmpty);
     return;
   }
   if (t >= (uint64_t)S * K) return;

@@ -46,6 +46,13 @@ __device__ __forceinline__ bool mbox_wait(const uint64_t* flags, uint32_t n, uin
   return true;
 }
 
+// True once any exchange of this table timed out (the bit stays latched until
+// gear_table_sync): the SPMD protocol is broken, so consumers of exchanged
+// data write GEAR_IDX_NONE / skip their writes instead of using stale data.
+__device__ __forceinline__ bool mbox_failed(const uint32_t* err) {
+  return (*(const volatile uint32_t*)err & kErrTimeout) != 0;
+}
+
 __device__ __forceinline__ uint32_t mbox_buf(const Mbox& m) { return (uint32_t)(m.epoch & 1); }
 
 // The epochs live in device memory so a captured step stays correct when a
@@ -65,7 +72,7 @@ __device__ __forceinline__ T* mbox_at(const Mbox& m, uint32_t r, uint64_t off) {
 
 // Shard totals: every rank writes its R records to all peers, then flags.
 // Called by one whole block; returns this rank's view of all S totals in
-// its own mailbox (valid after the wait).
+// its own mailbox (valid after the wait), or nullptr after a timeout.
 __device__ __forceinline__ const ShardTotals* mbox_exchange_totals(const Mbox& m,
                                                                    const ShardTotals* local,
                                                                    uint32_t* err) {
@@ -84,6 +91,7 @@ __device__ __forceinline__ const ShardTotals* mbox_exchange_totals(const Mbox& m
     mbox_wait(mbox_at<uint64_t>(m, m.rank, L.tflag) + b * m.W, m.W, m.epoch, err);
   }
   __syncthreads();
+  if (mbox_failed(err)) return nullptr;
   return mbox_at<ShardTotals>(m, m.rank, L.totals) + b * m.S;
 }
 

@@ -103,13 +103,17 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(const __grid_constant_
     totals = mbox_exchange_totals(mm, p.totals_local, p.err);
   } else if (p.xchg == 2) {
     const MboxLayout L = mbox_layout(mm.W, mm.S, mm.MB);
-    totals = mbox_at<ShardTotals>(mm, mm.rank, L.totals) + ((mm.epoch - 1) & 1) * mm.S;
+    totals = mbox_failed(p.err) ? nullptr
+                                : mbox_at<ShardTotals>(mm, mm.rank, L.totals) + ((mm.epoch - 1) & 1) * mm.S;
   }
+  // A timed-out exchange (totals == nullptr): no shard totals, so T = 0 and
+  // every output is GEAR_IDX_NONE (kErrTimeout latched, not kErrEmpty).
+  const bool failed = totals == nullptr;
   // Shard totals -> exclusive offsets (S <= 32: one lane per shard).
   const uint32_t S = p.n_shards;
   uint64_t Ts = 0;
   uint32_t par = 0;
-  if ((uint32_t)lane < S) {
+  if ((uint32_t)lane < S && !failed) {
     const uint64_t tp = __ldcg(&totals[lane].total_and_parity);
     Ts = tp & ((1ull << 62) - 1);
     par = (uint32_t)(tp >> 63);
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(kThreads) sample_kernel(const __grid_constant_
         }
       }
     } else if (lane == 0) {
-      atomicOr(p.err, kErrEmpty);
+      if (!failed) atomicOr(p.err, kErrEmpty);
       if (p.out_gen) p.out_gen[b] = 0;
     }
     if (lane == 0) {

@@ -5,9 +5,10 @@
 // Duplicate ids must resolve deterministically to the LAST entry in (rank,
 // position) order.  Racing stores cannot promise that, so the scatter is two
 // passes over the concatenated entry list: a tag pass does
-// atomicMax(tag[slot], epoch<<32 | k+1) and an apply pass lets only the entry
-// whose tag survived write the key.  The epoch (one per update call) makes the
-// tags of earlier calls smaller, so the tag array never needs clearing; it
+// atomicMax(tag[slot], epoch<<24 | k+1) and an apply pass lets only the entry
+// whose tag survived write the key.  The 40-bit epoch (one per update call)
+// makes the tags of earlier calls smaller, so the tag array never needs
+// clearing (make_tag, gear_internal.h); it
 // lives in device memory and the kernels advance it themselves, so an update
 // captured in a CUDA graph stays correct when the graph is replayed.
 //
@@ -71,15 +72,15 @@ __global__ void __launch_bounds__(kThreads)
     tag_kernel(const UpdRec* __restrict__ recs, uint32_t m, uint64_t local_begin,
                uint64_t local_rows, const uint32_t* __restrict__ gen,
                  const uint64_t* __restrict__ seq, unsigned long long* tag,
-               uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err) {
-  const uint32_t epoch = *epoch_dev + 1;
+               uint64_t* epoch_dev, unsigned long long* n_stale, uint32_t* err) {
+  const uint64_t epoch = *epoch_dev + 1;
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   if (k >= m) return;
   const UpdRec r = recs[k];
   uint64_t local;
   bool stale;
   if (owned_and_fresh(r, local_begin, local_rows, gen, seq, &local, &stale)) {
-    atomicMax(tag + local, ((unsigned long long)epoch << 32) | (unsigned long long)(k + 1));
+    atomicMax(tag + local, make_tag(epoch, k + 1));
   } else if (stale) {
     atomicAdd(n_stale, 1ull);
     atomicOr(err, kErrStale);
@@ -90,16 +91,16 @@ __global__ void __launch_bounds__(kThreads)
     apply_kernel(const UpdRec* __restrict__ recs, uint32_t m, uint64_t local_begin,
                  uint64_t local_rows, const uint32_t* __restrict__ gen,
                  const uint64_t* __restrict__ seq,
-                 const unsigned long long* __restrict__ tag, const uint32_t* epoch_dev,
+                 const unsigned long long* __restrict__ tag, const uint64_t* epoch_dev,
                  uint64_t* key, TileDirty td) {
-  const uint32_t epoch = *epoch_dev + 1;
+  const uint64_t epoch = *epoch_dev + 1;
   const uint32_t k = blockIdx.x * kThreads + threadIdx.x;
   if (k >= m) return;
   const UpdRec r = recs[k];
   uint64_t local;
   bool stale;
   if (owned_and_fresh(r, local_begin, local_rows, gen, seq, &local, &stale) &&
-      tag[local] == (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1))) {
+      tag[local] == (make_tag(epoch, k + 1))) {
     key[local] = r.q;
     mark_tile(td, local);
   }
@@ -119,9 +120,9 @@ __global__ void __launch_bounds__(kFusedThreads)
                  uint64_t n_global, Quant qz, uint64_t local_begin,
                  uint64_t local_rows, const uint32_t* __restrict__ gen,
                  const uint64_t* __restrict__ seq, unsigned long long* tag,
-                 uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err, uint64_t* key,
+                 uint64_t* epoch_dev, unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                  TileDirty td) {
-  const uint32_t epoch = *epoch_dev + 1;  // device-resident: graph-replayable
+  const uint64_t epoch = *epoch_dev + 1;  // device-resident: graph-replayable
   UpdRec r[kFusedPer];
   bool mine[kFusedPer];
   uint64_t loc[kFusedPer];
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(kFusedThreads)
     mine[u] = owned_and_fresh(r[u], local_begin, local_rows, gen, seq, &loc[u], &st);
     stale += st ? 1u : 0u;
     if (mine[u])
-      atomicMax(tag + loc[u], ((unsigned long long)epoch << 32) | (unsigned long long)(k + 1));
+      atomicMax(tag + loc[u], make_tag(epoch, k + 1));
   }
   if (stale) {
     atomicAdd(n_stale, (unsigned long long)stale);
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(kFusedThreads)
   for (int u = 0; u < kFusedPer; ++u) {
     const uint32_t k = threadIdx.x + u * kFusedThreads;
     if (mine[u] && __ldcg(tag + loc[u]) ==
-                       (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1))) {
+                       (make_tag(epoch, k + 1))) {
       key[loc[u]] = r[u].q;
       mark_tile(td, loc[u]);
     }
@@ -184,9 +185,9 @@ __global__ void __launch_bounds__(kFusedThreads)
                 Quant qz, const __grid_constant__ Mbox mb0,
                 uint64_t local_begin, uint64_t local_rows, const uint32_t* __restrict__ gen,
                  const uint64_t* __restrict__ seq,
-                unsigned long long* tag, uint32_t* epoch_dev, unsigned long long* n_stale,
+                unsigned long long* tag, uint64_t* epoch_dev, unsigned long long* n_stale,
                 uint32_t* err, uint64_t* key, TileDirty td) {
-  const uint32_t epoch = *epoch_dev + 1;  // device-resident tag epoch
+  const uint64_t epoch = *epoch_dev + 1;  // device-resident tag epoch
   const Mbox mb = mbox_at_next_epoch(mb0);  // device-resident exchange epoch
   const MboxLayout L = mbox_layout(mb.W, mb.S, mb.MB);
   const uint32_t bsel = mbox_buf(mb);
@@ -219,7 +220,8 @@ __global__ void __launch_bounds__(kFusedThreads)
   }
   __syncthreads();
   const UpdRec* recs = mbox_at<UpdRec>(mb, mb.rank, L.upd) + (uint64_t)bsel * mb.W * mb.MB;
-  const uint32_t m = mb.W * n;
+  // a timed-out exchange: apply nothing (peers' records may be stale)
+  const uint32_t m = mbox_failed(err) ? 0u : mb.W * n;
   UpdRec r[kFusedPer];
   bool mine[kFusedPer];
   uint64_t loc[kFusedPer];
@@ -239,7 +241,7 @@ __global__ void __launch_bounds__(kFusedThreads)
     mine[u] = owned_and_fresh(r[u], local_begin, local_rows, gen, seq, &loc[u], &st);
     stale += st ? 1u : 0u;
     if (mine[u])
-      atomicMax(tag + loc[u], ((unsigned long long)epoch << 32) | (unsigned long long)(k + 1));
+      atomicMax(tag + loc[u], make_tag(epoch, k + 1));
   }
   if (stale) {
     atomicAdd(n_stale, (unsigned long long)stale);
@@ -251,7 +253,7 @@ __global__ void __launch_bounds__(kFusedThreads)
   for (int u = 0; u < kFusedPer; ++u) {
     const uint32_t k = threadIdx.x + u * kFusedThreads;
     if (mine[u] && __ldcg(tag + loc[u]) ==
-                       (((unsigned long long)epoch << 32) | (unsigned long long)(k + 1))) {
+                       (make_tag(epoch, k + 1))) {
       key[loc[u]] = r[u].q;
       mark_tile(td, loc[u]);
     }
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(kFusedThreads)
   }
 }
 
-__global__ void epoch_bump_kernel(uint32_t* epoch_dev) { *epoch_dev += 1; }
+__global__ void epoch_bump_kernel(uint64_t* epoch_dev) { *epoch_dev += 1; }
 
 }  // namespace
 
@@ -274,7 +276,7 @@ cudaError_t launch_update_xchg(const uint64_t* idx, const void* prio, int prio_i
                                Quant qz, const Mbox& mb,
                                uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
                                const uint64_t* seq,
-                               unsigned long long* tag, uint32_t* epoch_dev,
+                               unsigned long long* tag, uint64_t* epoch_dev,
                                unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                TileDirty td, cudaStream_t s) {
   count_launch();
@@ -289,7 +291,7 @@ cudaError_t launch_update_fused(const uint64_t* idx, const void* prio, int prio_
                                 uint64_t n_global, Quant qz,
                                 uint64_t local_begin, uint64_t local_rows, const uint32_t* gen,
                                 const uint64_t* seq,
-                                unsigned long long* tag, uint32_t* epoch_dev,
+                                unsigned long long* tag, uint64_t* epoch_dev,
                                 unsigned long long* n_stale, uint32_t* err, uint64_t* key,
                                 TileDirty td, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
@@ -334,7 +336,7 @@ cudaError_t launch_update_quantize(const uint64_t* idx, const void* prio, int pr
 
 cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                               uint64_t local_rows, const uint32_t* gen, const uint64_t* seq, unsigned long long* tag,
-                              uint32_t* epoch_dev, unsigned long long* n_stale, uint32_t* err,
+                              uint64_t* epoch_dev, unsigned long long* n_stale, uint32_t* err,
                               cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   count_launch();
@@ -346,7 +348,7 @@ cudaError_t launch_update_tag(const UpdRec* recs, uint32_t m, uint64_t local_beg
 cudaError_t launch_update_apply(const UpdRec* recs, uint32_t m, uint64_t local_begin,
                                 uint64_t local_rows, const uint32_t* gen,
                                 const uint64_t* seq,
-                                const unsigned long long* tag, uint32_t* epoch_dev, uint64_t* key,
+                                const unsigned long long* tag, uint64_t* epoch_dev, uint64_t* key,
                                 TileDirty td, cudaStream_t s) {
   if (m == 0) return cudaSuccess;
   count_launch(2);

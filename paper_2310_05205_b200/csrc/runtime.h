@@ -91,6 +91,8 @@ struct gear_table {
   uint64_t qmax = 0;
   gear_removal removal = GEAR_REMOVE_FIFO;
   uint32_t max_batch = 4096;
+  uint32_t seq_len = 0;
+  uint64_t schema_hash = 0;  // FNV-1a over seq_len and every column's name, dtype, shape, placement
   std::vector<gear::ColumnState> cols;
 
   // slot state (rank-local, R*C_s entries)
@@ -156,7 +158,7 @@ struct gear_table {
   double* upd_prio = nullptr;
   double* upd_pow = nullptr;        // [max_batch] p^alpha (alpha != 1)
   uint32_t* upd_gen = nullptr;
-  uint32_t* d_epoch = nullptr;      // update tag epoch (device-resident, advanced by the kernels)
+  uint64_t* d_epoch = nullptr;      // update tag epoch (device-resident, advanced by the kernels)
   uint64_t* d_seed = nullptr;       // device seed counter (gear_sample with GEAR_SAMPLE_DEVICE_SEED)
   unsigned long long* n_stale = nullptr;
   uint32_t* err = nullptr;
@@ -183,11 +185,5 @@ struct gear_table {
   int tma_ctas = 2;                 // TMA collect CTAs per SM
   int tma_stages = 3;               // shared-memory stages per TMA CTA
   int collect_impl = 1;             // 1: TMA bulk copies for large aligned rows, 0: LSU only
-  int tma_ooo = 0;                  // TMA ring stored in completion order
-  int collect_dynamic = 0;          // TMA tasks claimed from a counter
-  static constexpr uint32_t kDynSlots = 8;
-  unsigned long long* dyn_pool = nullptr;  // [kDynSlots][2] task counters
-  uint64_t dyn_slot = 0;
   int collect_peer_lsu = 0;         // W > 1: peer-HBM rows of TMA columns via LSU warps
-  int collect_permute = 0;          // visit rows in a coprime-stride order (measured slower)
 };

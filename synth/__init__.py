@@ -77,9 +77,7 @@ def build(force: bool = False) -> str:
 _lib = None
 
 
-def fill_rows(dst_ptr: int, n_rows: int, row_bytes: int, col: int, first_traj: int,
-              seed: int = DATA_SEED, stream: int = 0):
-    """Write rows first_traj .. first_traj+n_rows-1 of column `col` to device memory."""
+def _load():
     global _lib
     if _lib is None:
         build()
@@ -88,7 +86,26 @@ def fill_rows(dst_ptr: int, n_rows: int, row_bytes: int, col: int, first_traj: i
                                          ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                          ctypes.c_void_p]
         _lib.synth_fill_rows.restype = ctypes.c_int
-    st = _lib.synth_fill_rows(dst_ptr, n_rows, row_bytes, col, first_traj, seed, stream)
+        _lib.synth_fill_rows_ids.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                             ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                             ctypes.c_void_p]
+        _lib.synth_fill_rows_ids.restype = ctypes.c_int
+    return _lib
+
+
+def fill_rows_ids(dst_ptr: int, ids_ptr: int, n_rows: int, row_bytes: int, col: int,
+                  seed: int = DATA_SEED, stream: int = 0):
+    """Write the rows of trajectories ids[0..n_rows) (device u64 array) of
+    column `col` to device memory -- the expected batch of a gather."""
+    st = _load().synth_fill_rows_ids(dst_ptr, ids_ptr, n_rows, row_bytes, col, seed, stream)
+    if st != 0:
+        raise RuntimeError(f"synth_fill_rows_ids: cuda error {st}")
+
+
+def fill_rows(dst_ptr: int, n_rows: int, row_bytes: int, col: int, first_traj: int,
+              seed: int = DATA_SEED, stream: int = 0):
+    """Write rows first_traj .. first_traj+n_rows-1 of column `col` to device memory."""
+    st = _load().synth_fill_rows(dst_ptr, n_rows, row_bytes, col, first_traj, seed, stream)
     if st != 0:
         raise RuntimeError(f"synth_fill_rows: cuda error {st}")
 

@@ -339,6 +339,40 @@ def run_fuzz_case(comm, W, rank, R=2, Cs=400, steps=150, seed=11):
     t.close()
 
 
+def run_timeout_case(comm, W, rank, R=1, Cs=256, B=32):
+    """A broken SPMD sequence: only rank 0 calls gear_sample and then
+    gear_update_priorities.  Its mailbox waits time out after ~4 s; the
+    sample must return GEAR_IDX_NONE everywhere (not ids drawn from stale
+    totals) and latch TIMEOUT, and the update must change no key."""
+    cols = [gear.Column("a", gear.GEAR_U8, (8,))]
+    t = gear.Table(W * R * Cs, 1, cols, comm, shards_per_rank=R, max_batch=256)
+    for ls in range(R):
+        s = rank * R + ls
+        t.insert(s, [torch.zeros((Cs, 8), dtype=torch.uint8, device="cuda")],
+                 synth.priorities(Cs, seed=s) + 0.5)
+    torch.cuda.synchronize()
+    dist.barrier()
+    if rank == 0:
+        key0, _, _ = t.read_state()
+        idx = torch.zeros(B, dtype=torch.int64, device="cuda")
+        w = torch.empty(B, dtype=torch.float32, device="cuda")
+        t.sample(gear.GEAR_PRIORITIZED, B, 5, 0.4, idx, w)
+        torch.cuda.synchronize()
+        err, _ = t.sync()
+        assert err & gear.GEAR_DEVERR_TIMEOUT and not err & gear.GEAR_DEVERR_EMPTY, err
+        assert np.all(idx.cpu().numpy().view(np.uint64) == np.uint64(gear.GEAR_IDX_NONE))
+        ids = torch.arange(B, dtype=torch.int64, device="cuda")
+        gear.gear_update_priorities(t.handle, B, ids, torch.full((B,), 7.0, dtype=torch.float64,
+                                                                device="cuda"), gear.GEAR_F64)
+        torch.cuda.synchronize()
+        err, _ = t.sync()
+        assert err & gear.GEAR_DEVERR_TIMEOUT, err
+        key1, _, _ = t.read_state()
+        assert np.array_equal(key0, key1), "a timed-out update changed keys"
+    dist.barrier()
+    t.close()
+
+
 def main():
     W = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ["RANK"])
@@ -356,10 +390,13 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         comm = gear.comm_from_torch_distributed(local)
     D, H = gear.GEAR_DEVICE, gear.GEAR_HOST
+    quick = os.environ.get("GEAR_DIST_QUICK", "0") == "1"   # smoke(): one case + graph replay
     cases = [(1, [D, D, D], 0, 1), (2, [D, D, D], 1, 1), (1, [H, H, H], 0, 1),
              (2, [D, H, D], 0, 1), (1, [D, D, D], 0, 0), (2, [D, H, D], 1, 0)]
+    if quick:
+        cases = [(2, [D, H, D], 0, 1)]
     for R, pl, removal, xchg in cases:
-        run_case(comm, W, rank, R, pl, removal, xchg=xchg)
+        run_case(comm, W, rank, R, pl, removal, xchg=xchg, steps=1 if quick else 3)
         dist.barrier()
         if rank == 0:
             print(f"case R={R} placements={pl} removal={removal} peer_xchg={xchg}: ok", flush=True)
@@ -367,10 +404,16 @@ def main():
     dist.barrier()
     if rank == 0:
         print("case graph replay (owner-affine, device seed): ok", flush=True)
-    run_fuzz_case(comm, W, rank)
-    dist.barrier()
-    if rank == 0:
-        print("case random collective sequences: ok", flush=True)
+    if not quick:
+        run_fuzz_case(comm, W, rank)
+        dist.barrier()
+        if rank == 0:
+            print("case random collective sequences: ok", flush=True)
+        run_timeout_case(comm, W, rank)
+        dist.barrier()
+        if rank == 0:
+            print("case broken SPMD sequence (mailbox timeout -> GEAR_IDX_NONE, no key change): ok",
+                  flush=True)
     gear.gear_comm_destroy(comm)
     dist.destroy_process_group()
     print(f"rank {rank}: all multi-GPU parity cases ok ({'shared device, host bootstrap' if shared else 'one GPU per rank, NCCL bootstrap'})",

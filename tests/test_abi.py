@@ -85,3 +85,39 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
         gear.load()
     with pytest.raises(ImportError):
         gear.gear_sample(1, gear.GEAR_PRIORITIZED, 4, 1, 0.4, 0, None, None, None, 0)
+
+
+def test_binding_checks_dtypes_and_sizes():
+    """The ctypes binding refuses tensors whose dtype or size would make a
+    kernel read or write past the buffer: checked before the
+    library is called, so no table or GPU is needed."""
+    import numpy as np
+    import pytest
+    import torch
+    import paper_2310_05205_b200 as G
+    i64 = torch.zeros(8, dtype=torch.int64)
+    i32 = torch.zeros(8, dtype=torch.int32)
+    f32 = torch.zeros(8, dtype=torch.float32)
+    f64 = torch.zeros(8, dtype=torch.float64)
+    with pytest.raises(TypeError, match="out_idx"):
+        G.gear_sample(0, G.GEAR_UNIFORM, 8, 1, 0.0, i32)
+    with pytest.raises(TypeError, match="out_w"):
+        G.gear_sample(0, G.GEAR_UNIFORM, 8, 1, 0.0, i64, f64)
+    with pytest.raises(TypeError, match="out_p"):
+        G.gear_sample(0, G.GEAR_UNIFORM, 8, 1, 0.0, i64, f32, f32)
+    with pytest.raises(TypeError, match="out_gen"):
+        G.gear_sample(0, G.GEAR_UNIFORM, 8, 1, 0.0, i64, f32, f64, f32)
+    with pytest.raises(ValueError, match="elements"):
+        G.gear_sample(0, G.GEAR_UNIFORM, 9, 1, 0.0, i64)
+    with pytest.raises(TypeError, match="prio"):
+        G.gear_update_priorities(0, 8, i64, f32, G.GEAR_F64)
+    with pytest.raises(TypeError, match="idx"):
+        G.gear_update_priorities(0, 8, i32, f64, G.GEAR_F64)
+    with pytest.raises(TypeError, match="gen"):
+        G.gear_update_priorities(0, 8, i64, f64, G.GEAR_F64, gen=i64)
+    with pytest.raises(TypeError, match="prio"):
+        G.gear_commit(0, 0, 8, i64, f32)
+    with pytest.raises(TypeError, match="out_idx"):
+        G.gear_allocate(0, 0, 8, np.zeros(8, np.int32))
+    with pytest.raises(TypeError, match="float32 or float64"):
+        G.Table.update_priorities(type("T", (), {"handle": 0})(), i64, torch.zeros(8, dtype=torch.bfloat16))

@@ -69,6 +69,15 @@ def test_random_operation_sequences(torch_cuda, tmp_path, seed, removal, alpha):
             G.gear_table_set_tuning(P.t.handle, "cdf_levels", int(rng.integers(1, 3)))
         elif op == 7 and not saved and step > 40:       # checkpoint round trip
             path = str(tmp_path / f"fuzz_{seed}.gear")
+            ongoing = [(g // Cs, g) for g in range(Cs * R) if P.o.gen[g] > 0 and P.o.seq[g] == 0]
+            if ongoing:                                 # an in-flight allocation: refused
+                with pytest.raises(G.GearError) as e:
+                    P.t.save(path)
+                assert e.value.status == G.GEAR_ERR_STATE
+                for sh in range(R):
+                    ids = np.array([g for q, g in ongoing if q == sh], np.uint64)
+                    if ids.size:
+                        P.commit(sh, ids, synth.priorities(ids.size, seed=step + sh))
             P.t.save(path)
             Q = Pair(capacity=Cs * R, seq_len=2, colspecs=cols, R=R, removal=removal, alpha=alpha,
                      mirror=False)
