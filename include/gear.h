@@ -421,6 +421,13 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
  * pointer may be NULL. */
 gear_status gear_read_state(gear_table* t, uint64_t* key, uint64_t* seq, uint32_t* gen);
 
+/* Diagnostics (tests): the CDF the last gear_sample built, as this rank's R
+ * flat per-shard inclusive prefix sums cdf[ls*C_s + i] = sum of the keys
+ * (UNIFORM: of [key > 0]) of local shard ls up to slot i,
+ * whichever layout (cdf_levels) holds it; host u64[R*C_s], synchronous.
+ * STATE before the first sample. */
+gear_status gear_read_cdf(gear_table* t, uint64_t* cdf);
+
 #ifdef __cplusplus
 }
 #endif

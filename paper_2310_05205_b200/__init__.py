@@ -110,6 +110,7 @@ SIGNATURES = {
     "gear_collect": ([_P, _u32, _P, _u32, _P, _P, _P], _i32),
     "gear_table_sync": ([_P, _P, _P], _i32),
     "gear_read_state": ([_P, _P, _P, _P], _i32),
+    "gear_read_cdf": ([_P, _P], _i32),
     "gear_table_set_tuning": ([_P, ctypes.c_char_p, ctypes.c_int64], _i32),
     "gear_table_save": ([_P, ctypes.c_char_p], _i32),
     "gear_table_load": ([_P, ctypes.c_char_p], _i32),
@@ -419,6 +420,14 @@ def gear_read_state(t: int):
     gen = np.zeros(n, np.uint32)
     _check("gear_read_state", load().gear_read_state(t, _ptr(key), _ptr(seq), _ptr(gen)))
     return key, seq, gen
+
+
+def gear_read_cdf(t: int):
+    """The last built CDF as flat per-shard inclusive prefix sums (u64[R*C_s])."""
+    info = gear_table_info_get(t)
+    out = np.zeros(info["shard_capacity"] * info["shards_per_rank"], np.uint64)
+    _check("gear_read_cdf", load().gear_read_cdf(t, _ptr(out)))
+    return out
 
 
 def gear_table_set_tuning(t: int, key: str, value: int):

@@ -401,10 +401,10 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
     // flat CDF (R*C_s), or tile-local prefixes (R*C_s) + tile prefixes (tiles)
     GEAR_TRY(dalloc(&t->cdf[i], t->Clocal + tiles));
     GEAR_CUDA(cudaMemset(t->cdf[i], 0, (t->Clocal + tiles) * 8));
-    GEAR_TRY(dalloc(&t->scan_status[i], tiles));
-    GEAR_CUDA(cudaMemset(t->scan_status[i], 0, tiles * 8));
-    GEAR_TRY(dalloc(&t->scan_ticket[i], 1));
-    GEAR_CUDA(cudaMemset(t->scan_ticket[i], 0, 4));
+    GEAR_TRY(dalloc(&t->scan_status[i], (size_t)tiles * 16));  // room for a padded layout
+    GEAR_CUDA(cudaMemset(t->scan_status[i], 0, (size_t)tiles * 16 * 8));
+    GEAR_TRY(dalloc(&t->scan_ticket[i], 2));  // [0] counter, [1] scan epoch (flat scan)
+    GEAR_CUDA(cudaMemset(t->scan_ticket[i], 0, 8));
   }
   // two-level CDF bookkeeping: nothing built yet (buffer modes 0) -> the first
   // rebuild of each buffer rescans every tile
@@ -965,8 +965,8 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
                                t->scan2_ctr, t->scan2_ctr + t->R, s));
       else
         GEAR_CUDA(launch_scan(t->key, t->cdf[0], t->cdf[1], t->Cs, t->R, mode, t->d_xep + 3,
-                              t->cdf_totals_local, t->scan_status[0], t->scan_ticket[0],
-                              t->scan_ticket[1], s));
+                              t->cdf_totals_local, t->scan_status[0], t->scan_status[1],
+                              t->scan_ticket[0], t->scan_ticket[1], s));
       t->scan_launches += 1;
       t->cdf_mode = mode;
       t->dirty = false;
@@ -1207,6 +1207,28 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     t->tma_chunk = (uint32_t)value;
   } else {
     return set_error(GEAR_ERR_INVALID_ARG, "bad tuning %s = %lld", key, (long long)value);
+  }
+  return GEAR_OK;
+}
+
+gear_status gear_read_cdf(gear_table* t, uint64_t* cdf) {
+  clear_error();
+  GEAR_TRY(check_table(t));
+  if (cdf == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "cdf is NULL");
+  if (t->cdf_mode < 0) return set_error(GEAR_ERR_STATE, "no CDF built yet (call gear_sample)");
+  GEAR_CUDA(cudaSetDevice(t->device));
+  GEAR_CUDA(cudaDeviceSynchronize());
+  uint64_t par = 0;
+  GEAR_CUDA(cudaMemcpy(&par, t->d_xep + 3, 8, cudaMemcpyDeviceToHost));
+  const uint64_t* buf = t->cdf[par & 1];
+  GEAR_CUDA(cudaMemcpy(cdf, buf, t->Clocal * 8, cudaMemcpyDeviceToHost));
+  if (t->cdf_levels == 2) {  // tile-local prefixes + each shard's prefix of tile totals
+    const uint32_t tps = scan_tiles_per_shard(t->Cs);
+    std::vector<uint64_t> P((size_t)t->R * tps);
+    GEAR_CUDA(cudaMemcpy(P.data(), buf + t->Clocal, P.size() * 8, cudaMemcpyDeviceToHost));
+    for (uint32_t ls = 0; ls < t->R; ++ls)
+      for (uint64_t i = kCdfTile; i < t->Cs; ++i)
+        cdf[ls * t->Cs + i] += P[(size_t)ls * tps + i / kCdfTile - 1];
   }
   return GEAR_OK;
 }

@@ -143,20 +143,6 @@ __global__ void __launch_bounds__(kThreads) insert_rows_kernel(const __grid_cons
 // other warps copy the columns whose rows are not 16-byte aligned.
 constexpr int kTmaThreads = 128;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
 
 // W > 1: the peer-HBM rows of TMA columns, moved over NVLink by the LSU warps
 // with 16-byte loads (many independent loads in flight per warp) instead of

@@ -18,6 +18,9 @@
 // per half-warp).  The last tile to finish its look-back (done counter)
 // clears the status words, the ticket and the counter, so every launch starts
 // from the same state and the launch can be replayed from a CUDA graph.
+#include <algorithm>
+#include <cstdio>
+
 #include "common.cuh"
 
 namespace gear {
@@ -33,153 +36,320 @@ constexpr uint64_t kValMask = (1ull << 62) - 1;
 
 __device__ __forceinline__ int pad(int e) { return e + (e >> 4); }
 
+// Persistent, software-pipelined decoupled look-back scan.
+//
+// kScanCtasPerSm CTAs per SM stay resident and claim 4096-key tiles from an
+// atomic ticket, one per iteration.  Iteration n of a CTA:
+//   1. issues the look-back loads for its PREVIOUS tile n-1 (block-wide: each
+//      thread polls kScanLookPer status words, a window of 512 predecessors
+//      per L2 round trip),
+//   2. claims tile n+1 and starts its TMA bulk load (cp.async.bulk +
+//      mbarrier) into the buffer freed by tile n-2's bulk store,
+//   3. waits for tile n's data, scans it in shared memory (tile-local
+//      inclusive prefix, in place) and publishes its aggregate,
+//   4. consumes the look-back loads of tile n-1 (re-polling words that are
+//      not published yet), publishes its inclusive prefix, adds the prefix to
+//      tile n-1's local prefixes and writes it out with a bulk store.
+// So the L2 round trips of tile n-1's look-back overlap the scan of tile n,
+// and by the time they are consumed every predecessor has published: the
+// tiles being resolved (round j-1) only need the aggregates of their own
+// round and the inclusive prefixes of round j-2, published one iteration
+// earlier.  A tile waits only on tiles with smaller tickets, which running
+// CTAs hold and publish in ticket order (forward progress).  The look-back of
+// a tile that holds the shard's first tile is empty (prefix 0).
+//
+// Round 1's kernel (one CTA per tile, warp-0 look-back after the scan)
+// stalled 7 of 8 warps at the barrier behind a 1.2 us L2 round trip per
+// poll: 0.38 of the HBM copy peak.
+//
+// Shared layout: a tile is kTile consecutive u64 as the bulk copy lands it;
+// thread i owns elements [16i, 16i+16) and touches them in the rotated order
+// (k + i) mod 16, conflict-free per half-warp for 64-bit accesses.
+#ifndef GEAR_STATUS_STRIDE
+#define GEAR_STATUS_STRIDE 16
+#endif
+constexpr int kStatusStride = GEAR_STATUS_STRIDE;  // u64 words between two tiles' status words
+constexpr int kScanBufs = 3;
+constexpr int kScanCtasPerSm = 2;
+#ifndef GEAR_SCAN_LOOK_PER
+#define GEAR_SCAN_LOOK_PER 1
+#endif
+constexpr int kScanLookPer = GEAR_SCAN_LOOK_PER;
+constexpr uint32_t kNoTile = 0xffffffffu;
+
 template <bool kIndicator>
-__global__ void __launch_bounds__(kThreads) scan_kernel(
+__global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
     const uint64_t* __restrict__ key, uint64_t* __restrict__ cdf0, uint64_t* __restrict__ cdf1,
     uint64_t shard_cap, uint32_t tiles_per_shard, uint32_t n_tiles, uint64_t* par_dev,
-    ShardTotals* totals, uint64_t* status, uint32_t* ticket, uint32_t* done) {
-  // The CDF is rebuilt into the buffer peers are NOT reading: the parity of
-  // the last build lives in device memory (graph-replayable) and is flipped
-  // by the last tile; the parity travels with the shard totals.
-  const uint32_t parity = (uint32_t)(ld_relaxed_u64(par_dev) & 1) ^ 1u;
-  uint64_t* __restrict__ cdf = parity ? cdf1 : cdf0;
-  __shared__ uint64_t s_k[kTile + kTile / 16];
-  __shared__ uint32_t s_tile;
-  __shared__ uint64_t s_warp[kThreads / 32];
-  __shared__ uint64_t s_excl;
+    ShardTotals* totals, uint64_t* status0, uint64_t* status1, uint32_t* ticket, uint32_t* done) {
+  extern __shared__ __align__(128) uint64_t s_buf[];  // kScanBufs * kTile
+  __shared__ __align__(8) uint64_t s_bar[kScanBufs];
+  __shared__ uint32_t s_t[kScanBufs];    // ticket held by each buffer
+  __shared__ uint32_t s_tma[kScanBufs];  // 1: the buffer's tile arrives by TMA
+  __shared__ uint64_t s_agg[kScanBufs];  // each buffer's tile aggregate
+  __shared__ uint64_t s_red[kThreads / 32];   // scan: warp totals
+  __shared__ uint64_t s_red2[kThreads / 32];  // look-back: warp partial sums
+  __shared__ uint32_t s_pmask[kScanLookPer][kThreads / 32];
   __shared__ bool s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // The CDF is rebuilt into the buffer peers are NOT reading: the parity of
+  // the last build lives in device memory (graph-replayable) and is flipped
+  // by the last CTA to exit; the parity travels with the shard totals.
+  const uint32_t parity = (uint32_t)(ld_relaxed_u64(par_dev) & 1) ^ 1u;
+  uint64_t* __restrict__ cdf = parity ? cdf1 : cdf0;
+  // Status words: launches of this kernel alternate between two arrays (the
+  // scan epoch in ticket[1], advanced by the last CTA): this launch uses one
+  // and clears the other -- the previous launch's -- for the next launch.
+  const uint32_t epoch = *(volatile uint32_t*)(ticket + 1);
+  uint64_t* __restrict__ status = (epoch & 1) ? status1 : status0;
+  {
+    uint64_t* other = (epoch & 1) ? status0 : status1;
+    for (uint32_t i = blockIdx.x * kThreads + tid; i < n_tiles; i += gridDim.x * kThreads)
+      other[(uint64_t)i * kStatusStride] = 0;
+  }
 
-  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
-  __syncthreads();
-  const uint32_t t = s_tile;
-  const uint32_t shard = t / tiles_per_shard;
-  const uint32_t tt = t - shard * tiles_per_shard;
-  const uint64_t tile_begin = (uint64_t)tt * kTile;                   // within shard
-  const uint64_t gbase = (uint64_t)shard * shard_cap + tile_begin;    // within key[]
-  const uint32_t count = (uint32_t)min((uint64_t)kTile, shard_cap - tile_begin);
-  const bool vec = count == (uint32_t)kTile && (gbase & 1) == 0;
-
-  // HBM -> shared, coalesced.
-  if (vec) {
-    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(key + gbase);
-#pragma unroll
-    for (int it = 0; it < kItems / 2; ++it) {
-      const int vi = it * kThreads + tid;
-      const ulonglong2 x = __ldg(src + vi);
-      const int p = pad(2 * vi);
-      s_k[p] = x.x;
-      s_k[p + 1] = x.y;
+  auto tile_geom = [&](uint32_t t, uint32_t* shard, uint32_t* tt, uint64_t* gbase,
+                       uint32_t* count) {
+    *shard = t / tiles_per_shard;
+    *tt = t - *shard * tiles_per_shard;
+    const uint64_t tb = (uint64_t)*tt * kTile;
+    *gbase = (uint64_t)*shard * shard_cap + tb;
+    *count = (uint32_t)min((uint64_t)kTile, shard_cap - tb);
+  };
+  // thread 0: take the prefetched ticket for buffer b, start its bulk load and
+  // prefetch the next ticket (the atomic's round trip is consumed one
+  // iteration later, off the critical path)
+  uint32_t next_ticket = 0;
+  auto claim = [&](int b) {
+    const uint32_t t = next_ticket;
+    next_ticket = atomicAdd(ticket, 1u);
+    s_t[b] = t < n_tiles ? t : kNoTile;
+    s_tma[b] = 0;
+    if (t >= n_tiles) return;
+    uint32_t sh, tt, count;
+    uint64_t gb;
+    tile_geom(t, &sh, &tt, &gb, &count);
+    if (count == (uint32_t)kTile && (gb & 1) == 0) {
+      s_tma[b] = 1;
+      bulk_g2s(smem_u32(s_buf + (size_t)b * kTile), key + gb, kTile * 8, smem_u32(&s_bar[b]));
     }
-  } else {
+  };
+  // Look-back loads of tile t (window at distances 1 + tid + 256k).
+  auto poll = [&](uint32_t t, int64_t pred, uint64_t* st) {
+    uint32_t sh, tt, count;
+    uint64_t gb;
+    tile_geom(t, &sh, &tt, &gb, &count);
+    const int64_t first = (int64_t)t - (int64_t)tt;
 #pragma unroll
-    for (int it = 0; it < kItems; ++it) {
-      const int e = it * kThreads + tid;
-      s_k[pad(e)] = (uint32_t)e < count ? key[gbase + e] : 0ull;
+    for (int k = 0; k < kScanLookPer; ++k) {
+      const int64_t idx = pred - tid - (int64_t)k * kThreads;
+      st[k] = idx >= first ? ld_relaxed_u64(status + idx * kStatusStride) : kFlagP;
     }
+  };
+  if (tid == 0) {
+    for (int b = 0; b < kScanBufs; ++b) {
+      mbar_init(smem_u32(&s_bar[b]), 1);
+      s_t[b] = kNoTile;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    next_ticket = atomicAdd(ticket, 1u);
+    claim(0);
+    if (s_t[0] != kNoTile) claim(1);
   }
   __syncthreads();
-  uint64_t v[kItems];
-#pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    const uint64_t x = s_k[tid * (kItems + 1) + i];
-    v[i] = kIndicator ? (x > 0 ? 1ull : 0ull) : x;
-  }
-  // Thread-local inclusive prefix.
-#pragma unroll
-  for (int i = 1; i < kItems; ++i) v[i] += v[i - 1];
-  // Warp and block scan of the thread totals.
-  const uint64_t incl = warp_incl_scan_u64(v[kItems - 1], lane);
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  uint64_t warp_excl = 0, agg = 0;
-#pragma unroll
-  for (int w = 0; w < kThreads / 32; ++w) {
-    const uint64_t x = s_warp[w];
-    warp_excl += (w < warp) ? x : 0ull;
-    agg += x;
-  }
-  const uint64_t thread_excl = warp_excl + incl - v[kItems - 1];
 
-  // Publish the aggregate (or the inclusive prefix for a shard's first tile)
-  // and look back over the predecessors of the same shard.
-  if (warp == 0) {
-    uint64_t excl = 0;
-    if (tt == 0) {
-      if (lane == 0) st_relaxed_u64(status + t, kFlagP | agg);
-    } else {
-      if (lane == 0) st_relaxed_u64(status + t, kFlagA | agg);
-      const int64_t first = (int64_t)t - (int64_t)tt;  // shard's first tile
-      int64_t pred = (int64_t)t - 1;
-      while (true) {
-        const int64_t idx = pred - lane;
-        const bool valid = idx >= first;
-        uint64_t s = valid ? ld_relaxed_u64(status + idx) : kFlagP;
-        while (__any_sync(kFull, (s >> 62) == 0)) {
-          if ((s >> 62) == 0) s = ld_relaxed_u64(status + idx);
+  uint32_t phase = 0;  // bit b: parity of buffer b's mbarrier
+#ifdef GEAR_SCAN_PROF
+  uint64_t pr[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pt = clock64(), iters = 0, polls = 0;
+#define PROF(i) do { const uint64_t c_ = clock64(); pr[i] += c_ - pt; pt = c_; } while (0)
+#else
+#define PROF(i) do {} while (0)
+#endif
+  for (uint32_t n = 0;; ++n) {
+    const int b = (int)(n % kScanBufs);
+    const int bp = (int)((n + kScanBufs - 1) % kScanBufs);  // tile n-1 (pending prefix)
+    const int bn = (int)((n + 1) % kScanBufs);              // tile n+1 (in flight)
+    const uint32_t t = s_t[b];
+    const uint32_t tp = n >= 1 ? s_t[bp] : kNoTile;
+    // 1. the look-back loads of tile n-1 fly while tile n is scanned
+    uint64_t st[kScanLookPer];
+    if (tp != kNoTile) poll(tp, (int64_t)tp - 1, st);
+    PROF(0);
+    // 2. scan tile n in place (tile-local inclusive prefix) and publish it
+    if (t != kNoTile) {
+      uint32_t shard, tt, count;
+      uint64_t gbase;
+      tile_geom(t, &shard, &tt, &gbase, &count);
+      uint64_t* buf = s_buf + (size_t)b * kTile;
+      if (s_tma[b]) {
+        while (!mbar_try_wait(smem_u32(&s_bar[b]), (phase >> b) & 1u)) {
         }
-        const unsigned pmask = __ballot_sync(kFull, valid && (s >> 62) == 2);
-        const uint64_t val = valid ? (s & kValMask) : 0ull;
-        if (pmask) {
-          const int lp = __ffs(pmask) - 1;  // closest inclusive predecessor
-          uint64_t part = lane <= lp ? val : 0ull;
+        phase ^= 1u << b;
+      } else {  // a ragged or unaligned tile: plain loads, zero-padded
+        for (int e = tid; e < kTile; e += kThreads)
+          buf[e] = (uint32_t)e < count ? key[gbase + e] : 0ull;
+        __syncthreads();
+      }
+      PROF(1);
+      // thread i owns the 8 pairs [16i + 2j, 16i + 2j + 1] and visits them in
+      // the rotated order j = (k + r) mod 8, r = i mod 8 (128-bit accesses,
+      // conflict-free per quarter-warp); S_k = prefix over the visited pairs,
+      // and the natural prefix of pair j = (k + r) mod 8 is
+      // S_k - S_{7-r} + (k < 8 - r ? total : 0)
+      const int r = tid & 7;
+      ulonglong2* b2 = reinterpret_cast<ulonglong2*>(buf) + tid * (kItems / 2);
+      uint64_t lo[kItems / 2], hi[kItems / 2];
+#pragma unroll
+      for (int k = 0; k < kItems / 2; ++k) {
+        const ulonglong2 x = b2[(k + r) & 7];
+        lo[k] = kIndicator ? (x.x > 0 ? 1ull : 0ull) : x.x;
+        hi[k] = kIndicator ? (x.y > 0 ? 1ull : 0ull) : x.y;
+      }
+      uint64_t run = 0;
+#pragma unroll
+      for (int k = 0; k < kItems / 2; ++k) {
+        lo[k] += run;
+        hi[k] += lo[k];
+        run = hi[k];
+      }
+      const uint64_t total = run;
+      uint64_t s_rot = 0;
+#pragma unroll
+      for (int k = 0; k < kItems / 2; ++k) s_rot = (k == 7 - r) ? hi[k] : s_rot;
+      const uint64_t incl = warp_incl_scan_u64(total, lane);
+      if (lane == 31) s_red[warp] = incl;  // (last read before the previous end-of-iteration barrier)
+      __syncthreads();
+      uint64_t warp_excl = 0, agg = 0;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) {
+        const uint64_t x = s_red[w];
+        warp_excl += (w < warp) ? x : 0ull;
+        agg += x;
+      }
+      const uint64_t base = warp_excl + incl - total;
+#pragma unroll
+      for (int k = 0; k < kItems / 2; ++k) {
+        const uint64_t off = base - s_rot + (k < 8 - r ? total : 0ull);
+        b2[(k + r) & 7] = make_ulonglong2(lo[k] + off, hi[k] + off);
+      }
+      if (tid == 0) {
+        s_agg[b] = agg;
+        // a shard's first tile: its aggregate IS its inclusive prefix
+        st_relaxed_u64(status + (uint64_t)t * kStatusStride, (tt == 0 ? kFlagP : kFlagA) | agg);
+      }
+    }
+    PROF(2);
+    // 3. resolve tile n-1: consume the look-back, publish, add, store
+    if (tp != kNoTile) {
+      uint32_t shard, tt, count;
+      uint64_t gbase;
+      tile_geom(tp, &shard, &tt, &gbase, &count);
+      uint64_t excl = 0;
+      if (tt != 0) {
+        int64_t pred = (int64_t)tp - 1;
+        while (true) {
+#pragma unroll
+          for (int k = 0; k < kScanLookPer; ++k) {
+            const int64_t idx = pred - tid - (int64_t)k * kThreads;
+            while ((st[k] >> 62) == 0) {
+              st[k] = ld_relaxed_u64(status + idx * kStatusStride);
+#ifdef GEAR_SCAN_PROF
+              ++polls;
+#endif
+            }
+          }
+          PROF(6);
+          // closest inclusive prefix: the smallest distance tid + 256k with a
+          // P flag, from one ballot per warp and word
+#pragma unroll
+          for (int k = 0; k < kScanLookPer; ++k) {
+            const unsigned m = __ballot_sync(kFull, (st[k] >> 62) == 2);
+            if (lane == 0) s_pmask[k][warp] = m;
+          }
+          __syncthreads();
+          PROF(7);
+          uint32_t dp = 0xffffffffu;
+#pragma unroll
+          for (int k = kScanLookPer - 1; k >= 0; --k)
+#pragma unroll
+            for (int w = kThreads / 32 - 1; w >= 0; --w) {
+              const unsigned m = s_pmask[k][w];
+              if (m) dp = (uint32_t)(k * kThreads + w * 32 + __ffs(m) - 1);
+            }
+          uint64_t part = 0;
+#pragma unroll
+          for (int k = 0; k < kScanLookPer; ++k)
+            part += ((uint32_t)(tid + k * kThreads) <= dp) ? (st[k] & kValMask) : 0ull;
 #pragma unroll
           for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(kFull, part, d);
-          excl += part;
-          break;
+          if (lane == 0) s_red2[warp] = part;
+          __syncthreads();
+#pragma unroll
+          for (int w = 0; w < kThreads / 32; ++w) excl += s_red2[w];
+          if (dp != 0xffffffffu) break;
+          __syncthreads();  // s_pmask / s_red2 read before the next round
+          pred -= (int64_t)kThreads * kScanLookPer;  // no prefix in this window
+          poll(tp, pred, st);
         }
-        uint64_t part = val;
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(kFull, part, d);
-        excl += part;
-        pred -= 32;
+        if (tid == 0) st_relaxed_u64(status + (uint64_t)tp * kStatusStride, kFlagP | (excl + s_agg[bp]));
       }
-      if (lane == 0) st_relaxed_u64(status + t, kFlagP | (excl + agg));
+      PROF(3);
+      if (tt == tiles_per_shard - 1 && tid == 0) {
+        ShardTotals rec;
+        rec.total_and_parity = (excl + s_agg[bp]) | ((uint64_t)parity << 63);
+        rec.aux = 0;
+        totals[shard] = rec;
+      }
+      // out: prefix + local prefix, coalesced 16-byte stores straight from
+      // registers (the buffer is free as soon as this pass has read it)
+      const uint64_t* buf = s_buf + (size_t)bp * kTile;
+      if (s_tma[bp]) {
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(buf);
+        ulonglong2* dst = reinterpret_cast<ulonglong2*>(cdf + gbase);
+#pragma unroll
+        for (int k = 0; k < kItems / 2; ++k) {
+          const ulonglong2 x = src[k * kThreads + tid];
+          dst[k * kThreads + tid] = make_ulonglong2(x.x + excl, x.y + excl);
+        }
+      } else {
+        for (int e = tid; e < (int)count; e += kThreads) cdf[gbase + e] = buf[e] + excl;
+      }
     }
-    if (lane == 0) {
-      s_excl = excl;
-      // This tile no longer reads or writes status words: count it done.
-      // The fence only has to drain the status store above (the CDF stores
-      // come later), and the last tile to get here re-arms the status
-      // words, the ticket and the counter after its stores.
-      __threadfence();
-      s_last = atomicAdd(done, 1u) == n_tiles - 1;
+    PROF(4);
+    __syncthreads();  // tile n-1's buffer read by every thread: free
+    // 4. claim tile n+2 into tile n-1's buffer, just freed: its load has a
+    //    whole iteration (tile n+1 is already in flight in the third buffer)
+    if (tid == 0 && t != kNoTile) {
+      if (s_t[bn] != kNoTile) claim(bp);
+      else s_t[bp] = kNoTile;  // tickets only grow: nothing more for this CTA
     }
+    // (s_t / s_tma of the claimed buffer are read two iterations from now,
+    // after several barriers)
+    PROF(5);
+#ifdef GEAR_SCAN_PROF
+    ++iters;
+#endif
+    if (t == kNoTile) break;  // tile n-1 was the last: done
+  }
+#ifdef GEAR_SCAN_PROF
+  if (tid == 0 && (blockIdx.x % 37) == 0)
+    printf("scanprof cta %u iters %llu cyc/iter: poll-issue %llu tma-wait %llu scan %llu resolve-spin %llu resolve-bar1 %llu resolve-rest %llu out %llu claim %llu polls %llu\n",
+           blockIdx.x, iters, pr[0] / iters, pr[1] / iters, pr[2] / iters, pr[6] / iters, pr[7] / iters, pr[3] / iters,
+           pr[4] / iters, pr[5] / iters, polls);
+#endif
+  // The last CTA to exit re-arms the ticket and the exit counter and
+  // publishes the new parity.
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  const uint64_t base = s_excl + thread_excl;
-#pragma unroll
-  for (int i = 0; i < kItems; ++i) s_k[tid * (kItems + 1) + i] = base + v[i];
-  __syncthreads();
-
-  // shared -> HBM, coalesced.
-  if (vec) {
-    ulonglong2* dst = reinterpret_cast<ulonglong2*>(cdf + gbase);
-#pragma unroll
-    for (int it = 0; it < kItems / 2; ++it) {
-      const int vi = it * kThreads + tid;
-      const int p = pad(2 * vi);
-      dst[vi] = make_ulonglong2(s_k[p], s_k[p + 1]);
-    }
-  } else {
-#pragma unroll
-    for (int it = 0; it < kItems; ++it) {
-      const int e = it * kThreads + tid;
-      if ((uint32_t)e < count) cdf[gbase + e] = s_k[pad(e)];
-    }
-  }
-  if (tt == tiles_per_shard - 1 && tid == 0) {
-    ShardTotals r;
-    r.total_and_parity = (s_excl + agg) | ((uint64_t)parity << 63);
-    r.aux = 0;
-    totals[shard] = r;
-  }
   if (s_last) {
-    for (uint32_t i = tid; i < n_tiles; i += kThreads) status[i] = 0;
     if (tid == 0) {
       *ticket = 0;
+      ticket[1] = epoch + 1;  // every CTA read the epoch before exiting
       *done = 0;
-      *par_dev = parity;  // every tile read the old parity before counting done
+      *par_dev = parity;  // every CTA read the old parity before exiting
     }
   }
 }
@@ -374,17 +544,32 @@ uint32_t scan_tiles_per_shard(uint64_t shard_cap) {
 
 cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf0, uint64_t* cdf1, uint64_t shard_cap,
                         uint32_t n_shards_local, int indicator, uint64_t* par_dev,
-                        ShardTotals* totals_out, uint64_t* status, uint32_t* ticket,
-                        uint32_t* done, cudaStream_t s) {
+                        ShardTotals* totals_out, uint64_t* status0, uint64_t* status1,
+                        uint32_t* ticket, uint32_t* done, cudaStream_t s) {
   const uint32_t tps = scan_tiles_per_shard(shard_cap);
   const uint32_t n_tiles = tps * n_shards_local;
+  const size_t smem = (size_t)kScanBufs * kTile * 8;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(scan_kernel<true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t grid = std::min<uint32_t>(n_tiles, (uint32_t)sms * kScanCtasPerSm);
   count_launch();
   if (indicator)
-    scan_kernel<true><<<n_tiles, kThreads, 0, s>>>(key, cdf0, cdf1, shard_cap, tps, n_tiles,
-                                                   par_dev, totals_out, status, ticket, done);
+    scan_kernel<true><<<grid, kThreads, smem, s>>>(key, cdf0, cdf1, shard_cap, tps, n_tiles,
+                                                   par_dev, totals_out, status0, status1, ticket, done);
   else
-    scan_kernel<false><<<n_tiles, kThreads, 0, s>>>(key, cdf0, cdf1, shard_cap, tps, n_tiles,
-                                                    par_dev, totals_out, status, ticket, done);
+    scan_kernel<false><<<grid, kThreads, smem, s>>>(key, cdf0, cdf1, shard_cap, tps, n_tiles,
+                                                    par_dev, totals_out, status0, status1, ticket, done);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,61 @@
+"""CDF rebuild throughput at N keys (one shard): the flat decoupled look-back
+scan (cdf_levels 1: every sample after a key write rebuilds the whole CDF) and
+a full two-level rebuild (cdf_levels 2 re-selected: both buffers forgotten).
+Rebuild time = (update of 1 key + sample of 1 draw) - (update + sample without
+rebuild is impossible, so: sample right after a layout switch minus a sample
+with a clean CDF); CUDA events, median of 20.  Run under ncu for kernel
+durations and DRAM bytes:  python tools/scan_bench.py 40000000"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+import paper_2310_05205_b200 as gear  # noqa: E402
+
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 40_000_000
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+t = gear.Table(N, 1, [gear.Column("x", gear.GEAR_U8, (16,))], None, max_batch=4096)
+s = torch.cuda.Stream()
+rows = torch.zeros((1 << 20, 16), dtype=torch.uint8, device="cuda")
+prio = synth.priorities(N, seed=1, zero_frac=0.01)
+for k0 in range(0, N, 1 << 20):
+    m = min(1 << 20, N - k0)
+    gear.gear_insert(t.handle, 0, m, [rows], prio[k0:k0 + m], None, s)
+idx = torch.zeros(1, dtype=torch.int64, device="cuda")
+p1 = torch.ones(1, dtype=torch.float64, device="cuda")
+
+
+def timed(fn):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    fn()
+    e1.record(s)
+    s.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def sample():
+    gear.gear_sample(t.handle, gear.GEAR_PRIORITIZED, 1, 5, 0.4, idx, None, None, None, s)
+
+
+out = {"keys": N, "bytes_per_rebuild": 16 * N}
+for levels in (1, 2):
+    gear.gear_table_set_tuning(t.handle, "cdf_levels", levels)
+    sample()
+    base, full = [], []
+    for i in range(reps):
+        base.append(timed(sample))                      # clean CDF: no rebuild
+        if levels == 1:
+            gear.gear_update_priorities(t.handle, 1, idx, p1, gear.GEAR_F64, None, s)
+        else:
+            gear.gear_table_set_tuning(t.handle, "cdf_levels", 2)   # forget both builds
+        full.append(timed(sample))                      # rebuilds the whole CDF
+    ms = float(np.median(full) - np.median(base))
+    out[f"levels{levels}"] = {"rebuild_us": ms * 1e3, "GBps": 16 * N / (ms / 1e3) / 1e9}
+assert t.sync()[0] == 0
+t.close()
+print(json.dumps(out))
