@@ -48,12 +48,15 @@ for levels in (1, 2):
     sample()
     base, full = [], []
     for i in range(reps):
-        base.append(timed(sample))                      # clean CDF: no rebuild
         if levels == 1:
+            base.append(timed(sample))                  # clean CDF: no rebuild
             gear.gear_update_priorities(t.handle, 1, idx, p1, gear.GEAR_F64, None, s)
+            full.append(timed(sample))                  # rebuilds the whole CDF
         else:
             gear.gear_table_set_tuning(t.handle, "cdf_levels", 2)   # forget both builds
-        full.append(timed(sample))                      # rebuilds the whole CDF
+            full.append(timed(sample))                  # full rebuild of one buffer
+            sample()                                    # ... and of the other
+            base.append(timed(sample))                  # both built: every tile clean
     ms = float(np.median(full) - np.median(base))
     out[f"levels{levels}"] = {"rebuild_us": ms * 1e3, "GBps": 16 * N / (ms / 1e3) / 1e9}
 assert t.sync()[0] == 0
