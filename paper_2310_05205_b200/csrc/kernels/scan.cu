@@ -86,6 +86,8 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
   __shared__ __align__(8) uint64_t s_bar[kScanBufs];
   __shared__ uint32_t s_t[kScanBufs];    // ticket held by each buffer
   __shared__ uint32_t s_tma[kScanBufs];  // 1: the buffer's tile arrives by TMA
+  __shared__ uint32_t s_shard[kScanBufs], s_tt[kScanBufs], s_count[kScanBufs];
+  __shared__ uint64_t s_gbase[kScanBufs];  // each buffer's tile geometry
   __shared__ uint64_t s_agg[kScanBufs];  // each buffer's tile aggregate
   __shared__ uint64_t s_red[kThreads / 32];   // scan: warp totals
   __shared__ uint64_t s_red2[kThreads / 32];  // look-back: warp partial sums
@@ -116,30 +118,36 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
     *gbase = (uint64_t)*shard * shard_cap + tb;
     *count = (uint32_t)min((uint64_t)kTile, shard_cap - tb);
   };
-  // thread 0: take the prefetched ticket for buffer b, start its bulk load and
-  // prefetch the next ticket (the atomic's round trip is consumed one
-  // iteration later, off the critical path)
-  uint32_t next_ticket = 0;
-  auto claim = [&](int b) {
-    const uint32_t t = next_ticket;
-    next_ticket = atomicAdd(ticket, 1u);
+  // thread 0: give buffer b ticket t, cache the tile's geometry and start
+  // its bulk load
+  auto claim_t = [&](int b, uint32_t t) {
     s_t[b] = t < n_tiles ? t : kNoTile;
     s_tma[b] = 0;
     if (t >= n_tiles) return;
     uint32_t sh, tt, count;
     uint64_t gb;
     tile_geom(t, &sh, &tt, &gb, &count);
+    s_shard[b] = sh;
+    s_tt[b] = tt;
+    s_count[b] = count;
+    s_gbase[b] = gb;
     if (count == (uint32_t)kTile && (gb & 1) == 0) {
       s_tma[b] = 1;
       bulk_g2s(smem_u32(s_buf + (size_t)b * kTile), key + gb, kTile * 8, smem_u32(&s_bar[b]));
     }
   };
-  // Look-back loads of tile t (window at distances 1 + tid + 256k).
-  auto poll = [&](uint32_t t, int64_t pred, uint64_t* st) {
-    uint32_t sh, tt, count;
-    uint64_t gb;
-    tile_geom(t, &sh, &tt, &gb, &count);
-    const int64_t first = (int64_t)t - (int64_t)tt;
+  // ... with the prefetched ticket, prefetching the next one (the atomic's
+  // round trip is consumed one iteration later, off the critical path; it is
+  // issued after the previous result was used, so tickets grow)
+  uint32_t next_ticket = 0;
+  auto claim = [&](int b) {
+    const uint32_t t = next_ticket;
+    claim_t(b, t);
+    next_ticket = atomicAdd(ticket, 1u);
+  };
+  // Look-back loads of the tile in buffer b (window at distances 1 + tid + 256k).
+  auto poll = [&](int b, int64_t pred, uint64_t* st) {
+    const int64_t first = (int64_t)s_t[b] - (int64_t)s_tt[b];
 #pragma unroll
     for (int k = 0; k < kScanLookPer; ++k) {
       const int64_t idx = pred - tid - (int64_t)k * kThreads;
@@ -152,9 +160,10 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
       s_t[b] = kNoTile;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t t0 = atomicAdd(ticket, 2u);  // two tickets in one round trip
+    claim_t(0, t0);
+    claim_t(1, t0 + 1);
     next_ticket = atomicAdd(ticket, 1u);
-    claim(0);
-    if (s_t[0] != kNoTile) claim(1);
   }
   __syncthreads();
 
@@ -173,13 +182,12 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
     const uint32_t tp = n >= 1 ? s_t[bp] : kNoTile;
     // 1. the look-back loads of tile n-1 fly while tile n is scanned
     uint64_t st[kScanLookPer];
-    if (tp != kNoTile) poll(tp, (int64_t)tp - 1, st);
+    if (tp != kNoTile) poll(bp, (int64_t)tp - 1, st);
     PROF(0);
     // 2. scan tile n in place (tile-local inclusive prefix) and publish it
     if (t != kNoTile) {
-      uint32_t shard, tt, count;
-      uint64_t gbase;
-      tile_geom(t, &shard, &tt, &gbase, &count);
+      const uint32_t tt = s_tt[b], count = s_count[b];
+      const uint64_t gbase = s_gbase[b];
       uint64_t* buf = s_buf + (size_t)b * kTile;
       if (s_tma[b]) {
         while (!mbar_try_wait(smem_u32(&s_bar[b]), (phase >> b) & 1u)) {
@@ -241,9 +249,8 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
     PROF(2);
     // 3. resolve tile n-1: consume the look-back, publish, add, store
     if (tp != kNoTile) {
-      uint32_t shard, tt, count;
-      uint64_t gbase;
-      tile_geom(tp, &shard, &tt, &gbase, &count);
+      const uint32_t shard = s_shard[bp], tt = s_tt[bp], count = s_count[bp];
+      const uint64_t gbase = s_gbase[bp];
       uint64_t excl = 0;
       if (tt != 0) {
         int64_t pred = (int64_t)tp - 1;
@@ -289,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
           if (dp != 0xffffffffu) break;
           __syncthreads();  // s_pmask / s_red2 read before the next round
           pred -= (int64_t)kThreads * kScanLookPer;  // no prefix in this window
-          poll(tp, pred, st);
+          poll(bp, pred, st);
         }
         if (tid == 0) st_relaxed_u64(status + (uint64_t)tp * kStatusStride, kFlagP | (excl + s_agg[bp]));
       }
