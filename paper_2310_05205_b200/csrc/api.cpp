@@ -609,6 +609,7 @@ gear_status check_table(const gear_table* t) {
 extern "C" {
 
 gear_status gear_table_create(const gear_table_desc* desc, gear_comm* comm, gear_table** out) {
+  GEAR_NVTX("gear_table_create");
   clear_error();
   if (desc == nullptr || out == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "NULL argument");
   *out = nullptr;
@@ -625,6 +626,7 @@ gear_status gear_table_create(const gear_table_desc* desc, gear_comm* comm, gear
 }
 
 gear_status gear_table_destroy(gear_table* t) {
+  GEAR_NVTX("gear_table_destroy");
   if (t == nullptr) return GEAR_OK;
   gear_comm* c = t->comm;
   destroy_table(t);
@@ -633,6 +635,7 @@ gear_status gear_table_destroy(gear_table* t) {
 }
 
 gear_status gear_table_info_get(const gear_table* t, gear_table_info* info) {
+  GEAR_NVTX("gear_table_info_get");
   GEAR_TRY(check_table(t));
   if (info == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "info is NULL");
   info->capacity_global = t->N;
@@ -652,6 +655,7 @@ gear_status gear_table_info_get(const gear_table* t, gear_table_info* info) {
 }
 
 gear_status gear_column_id(const gear_table* t, const char* name, uint32_t* out) {
+  GEAR_NVTX("gear_column_id");
   GEAR_TRY(check_table(t));
   if (name == nullptr || out == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "NULL argument");
   for (uint32_t c = 0; c < t->cols.size(); ++c)
@@ -663,6 +667,7 @@ gear_status gear_column_id(const gear_table* t, const char* name, uint32_t* out)
 }
 
 gear_status gear_column_row_bytes(const gear_table* t, uint32_t col, uint64_t* out) {
+  GEAR_NVTX("gear_column_row_bytes");
   GEAR_TRY(check_table(t));
   if (out == nullptr || col >= t->cols.size())
     return set_error(GEAR_ERR_INVALID_ARG, "bad column %u", col);
@@ -672,6 +677,7 @@ gear_status gear_column_row_bytes(const gear_table* t, uint32_t col, uint64_t* o
 
 gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* const* col_src,
                         const double* prio, uint64_t* out_idx, gear_stream stream) {
+  GEAR_NVTX("gear_insert");
   clear_error();
   GEAR_TRY(check_table(t));
   GEAR_CUDA(cudaSetDevice(t->device));
@@ -800,6 +806,7 @@ gear_status gear_insert(gear_table* t, uint32_t shard, uint32_t n, const void* c
 gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* idx,
                                    const void* prio, gear_dtype prio_dtype, const uint32_t* gen,
                                    gear_stream stream) {
+  GEAR_NVTX("gear_update_priorities");
   clear_error();
   GEAR_TRY(check_table(t));
   GEAR_CUDA(cudaSetDevice(t->device));
@@ -876,6 +883,7 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
 gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint64_t seed,
                         double beta, uint64_t* out_idx, float* out_w, double* out_p,
                         uint32_t* out_gen, uint32_t flags, gear_stream stream) {
+  GEAR_NVTX("gear_sample");
   clear_error();
   GEAR_TRY(check_table(t));
   GEAR_CUDA(cudaSetDevice(t->device));
@@ -1036,6 +1044,7 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
 
 gear_status gear_allocate(gear_table* t, uint32_t shard, uint32_t n, uint64_t* out_idx,
                           gear_stream stream) {
+  GEAR_NVTX("gear_allocate");
   clear_error();
   GEAR_TRY(check_table(t));
   GEAR_CUDA(cudaSetDevice(t->device));
@@ -1060,6 +1069,7 @@ gear_status gear_allocate(gear_table* t, uint32_t shard, uint32_t n, uint64_t* o
 
 gear_status gear_commit(gear_table* t, uint32_t shard, uint32_t n, const uint64_t* idx,
                         const double* prio, gear_stream stream) {
+  GEAR_NVTX("gear_commit");
   clear_error();
   GEAR_TRY(check_table(t));
   GEAR_CUDA(cudaSetDevice(t->device));
@@ -1081,6 +1091,7 @@ gear_status gear_commit(gear_table* t, uint32_t shard, uint32_t n, const uint64_
 }
 
 gear_status gear_column_base(const gear_table* t, uint32_t col, void** out) {
+  GEAR_NVTX("gear_column_base");
   clear_error();
   if (t == nullptr || out == nullptr || col >= t->cols.size())
     return set_error(GEAR_ERR_INVALID_ARG, "bad table, column %u or NULL output", col);
@@ -1090,6 +1101,7 @@ gear_status gear_column_base(const gear_table* t, uint32_t col, void** out) {
 
 gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_t ncols,
                          const uint32_t* col_ids, void* const* out, gear_stream stream) {
+  GEAR_NVTX("gear_collect");
   clear_error();
   GEAR_TRY(check_table(t));
   GEAR_CUDA(cudaSetDevice(t->device));
@@ -1154,6 +1166,7 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
 }
 
 gear_status gear_table_sync(gear_table* t, uint32_t* dev_errors, uint64_t* n_stale) {
+  GEAR_NVTX("gear_table_sync");
   clear_error();
   GEAR_TRY(check_table(t));
   GEAR_CUDA(cudaSetDevice(t->device));
@@ -1171,6 +1184,7 @@ gear_status gear_table_sync(gear_table* t, uint32_t* dev_errors, uint64_t* n_sta
 }
 
 gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value) {
+  GEAR_NVTX("gear_table_set_tuning");
   clear_error();
   GEAR_TRY(check_table(t));
   if (key == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "key is NULL");
@@ -1212,6 +1226,7 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
 }
 
 gear_status gear_read_cdf(gear_table* t, uint64_t* cdf) {
+  GEAR_NVTX("gear_read_cdf");
   clear_error();
   GEAR_TRY(check_table(t));
   if (cdf == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "cdf is NULL");
@@ -1234,6 +1249,7 @@ gear_status gear_read_cdf(gear_table* t, uint64_t* cdf) {
 }
 
 gear_status gear_read_state(gear_table* t, uint64_t* key, uint64_t* seq, uint32_t* gen) {
+  GEAR_NVTX("gear_read_state");
   clear_error();
   GEAR_TRY(check_table(t));
   GEAR_CUDA(cudaSetDevice(t->device));

@@ -149,6 +149,7 @@ gear_status save_to(gear_table* t, FILE* f, const std::vector<AllocState>& a) {
 extern "C" {
 
 gear_status gear_table_save(gear_table* t, const char* path) {
+  GEAR_NVTX("gear_table_save");
   clear_error();
   if (t == nullptr || path == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "NULL argument");
   GEAR_CUDA(cudaSetDevice(t->device));
@@ -190,6 +191,7 @@ gear_status gear_table_save(gear_table* t, const char* path) {
 }
 
 gear_status gear_table_load(gear_table* t, const char* path) {
+  GEAR_NVTX("gear_table_load");
   clear_error();
   if (t == nullptr || path == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "NULL argument");
   GEAR_CUDA(cudaSetDevice(t->device));

@@ -123,6 +123,7 @@ const char* gear_version(void) { return "gear-b200 0.1 (sm_100a)"; }
 uint64_t gear_kernel_launches(void) { return gear::g_launches.load(); }
 
 gear_status gear_get_unique_id(uint8_t out[128]) {
+  GEAR_NVTX("gear_get_unique_id");
   static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
   if (out == nullptr) return gear::set_error(GEAR_ERR_INVALID_ARG, "out is NULL");
   ncclUniqueId id;
@@ -133,6 +134,7 @@ gear_status gear_get_unique_id(uint8_t out[128]) {
 
 gear_status gear_comm_create(int nranks, int rank, const uint8_t id[128], int device,
                              gear_comm** out) {
+  GEAR_NVTX("gear_comm_create");
   gear::clear_error();
   if (out == nullptr || id == nullptr || nranks < 1 || nranks > gear::kMaxRanks || rank < 0 ||
       rank >= nranks || device < 0)
@@ -162,6 +164,7 @@ gear_status gear_comm_create(int nranks, int rank, const uint8_t id[128], int de
 
 gear_status gear_comm_create_host(int nranks, int rank, int device, gear_allgather_fn fn,
                                   void* ctx, gear_comm** out) {
+  GEAR_NVTX("gear_comm_create_host");
   gear::clear_error();
   if (out == nullptr || fn == nullptr || nranks < 1 || nranks > gear::kMaxRanks || rank < 0 ||
       rank >= nranks || device < 0)
@@ -199,6 +202,7 @@ gear_status gear_comm_create_host(int nranks, int rank, int device, gear_allgath
 }
 
 gear_status gear_comm_destroy(gear_comm* c) {
+  GEAR_NVTX("gear_comm_destroy");
   if (c == nullptr) return GEAR_OK;
   cudaSetDevice(c->device);
   if (c->nccl) ncclCommDestroy(c->nccl);

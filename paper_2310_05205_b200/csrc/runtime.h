@@ -2,6 +2,7 @@
 #pragma once
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <string>
@@ -50,6 +51,17 @@ void clear_error();
     gear_status s_ = (x);                \
     if (s_ != GEAR_OK) return s_;        \
   } while (0)
+
+// NVTX range around every C-ABI call (header-only NVTX v3: a no-op unless a
+// tool such as nsys / ncu is attached), so timelines show gear_sample /
+// gear_collect / ... next to the kernels they enqueue.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define GEAR_NVTX(name) ::gear::NvtxRange gear_nvtx_range_(name)
 
 enum class MemKind { Device, HostPinned, HostPageable };
 MemKind mem_kind(const void* p);

@@ -400,7 +400,7 @@ def main():
         dist.barrier()
         if rank == 0:
             print(f"case R={R} placements={pl} removal={removal} peer_xchg={xchg}: ok", flush=True)
-    run_graph_case(comm, W, rank)
+    run_graph_case(comm, W, rank, reps=4 if quick else 48)
     dist.barrier()
     if rank == 0:
         print("case graph replay (owner-affine, device seed): ok", flush=True)

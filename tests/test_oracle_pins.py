@@ -649,3 +649,35 @@ def test_topk_matches_brute_force(oracle_mod):
             st, idx, _, _ = oracle_mod.sample(oracle_mod.TOPK, key, None, Cs, S, 1, 0, len(sel), 0)
             ks = key[idx.astype(np.int64)]
             assert np.all(ks[:-1] >= ks[1:])                      # non-increasing keys
+
+
+def test_owner_affine_hand_worked_fifo(oracle_mod):
+    """Reading Q19's overflow order, pinned by a hand-worked example
+    (tests/golden/owner_affine_fifo.json): a FIFO global batch whose owner
+    pattern was designed through the priorities, the contiguous slices (Q9)
+    and the owner-affine slices written out by hand."""
+    with open(os.path.join(GOLD, "owner_affine_fifo.json")) as f:
+        g = json.load(f)
+    Cs, W, B = g["shard_capacity"], g["n_ranks"], g["batch_per_rank"]
+    t = oracle_mod.Table(Cs, W)
+    for s, pr in enumerate(g["priorities"]):
+        st, ids = t.insert(s, np.array(pr, dtype=np.float64))
+        assert st == 0 and [int(x) for x in ids] == list(range(s * Cs, s * Cs + Cs))
+    st, glob, _, _ = t.sample(oracle_mod.FIFO, 1, 0, W * B, 0)
+    assert st == 0 and [int(x) for x in glob] == g["global_batch"]
+    for r in range(W):
+        st, idx, _, _ = t.sample(oracle_mod.FIFO, W, r, B, 0)
+        assert st == 0 and [int(x) for x in idx] == g["contiguous"][r]
+        st, idx, _, _ = t.sample(oracle_mod.FIFO, W, r, B, 0, owner_affine=True)
+        assert st == 0 and [int(x) for x in idx] == g["owner_affine"][r], r
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 1024, 100_000, 281_600, 1_000_000, 10_000_000,
+                               2 ** 40 + 1, (1 << 62) - 1])
+def test_q_max_is_the_largest_safe_key(oracle_mod, n):
+    """Reading Q3: q_max is the LARGEST key for which N keys sum below 2^62
+    (so the u64 totals and the flag bits of the scan never overflow):
+    N*q_max < 2^62 <= N*(q_max + 1)."""
+    q = int(oracle_mod.q_max(n))
+    assert n * q < (1 << 62)
+    assert n * (q + 1) >= (1 << 62)
