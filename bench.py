@@ -350,8 +350,7 @@ def run_gpu(args):
         barrier()
         err, _ = t.sync()
         assert err == 0, f"device error bits {err} during warm-up"
-        ev = ([torch.cuda.Event(enable_timing=True) for _ in range(args.steps)],
-              [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)])
+        ev = tuple([torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] for _ in range(2))
         clocks = ClockSampler(local)
         clocks.start()
         l0 = gear.gear_kernel_launches()
@@ -370,7 +369,7 @@ def run_gpu(args):
         clk = clocks.stop()
         err, _ = t.sync()
         assert err == 0, f"device error bits {err} in the timed region"
-        coll = float(np.mean([a.elapsed_time(b) for a, b in zip(*ev)]))
+        coll = float(np.mean([a.elapsed_time(b) for a, b in zip(ev[0], ev[1])]))
         # per-step distribution: intervals between consecutive collect ends
         iv = [ev[1][i - 1].elapsed_time(ev[1][i]) for i in range(1, args.steps)]
         pct = ({f"p{q}": float(np.percentile(iv, q)) for q in (10, 50, 90)} if iv else {})
@@ -379,7 +378,7 @@ def run_gpu(args):
 
     def timed_graph(sflags, peer_lsu):
         """The pipelined step captured as ONE CUDA graph of S consecutive steps
-        (S = K when K <= 250): the draw key comes from the table's device seed
+        (S = K when K <= 2000: the collect-stream span then covers the whole timed region): the draw key comes from the table's device seed
         counter and the update epoch, the peer-mailbox epochs and the CDF
         parity are device-resident, so each replay performs S new, different
         (collective) steps.  K/S replays are timed.  Two events (external
@@ -390,7 +389,7 @@ def run_gpu(args):
         collects (an upper bound of the kernel time, so the roofline fraction
         is a lower bound) and can never exceed the time per step.  (Events
         around every collect cost ~6 us per step in the graph: not used.)"""
-        S = next(d for d in range(min(args.steps, 250), 0, -1) if args.steps % d == 0)
+        S = next(d for d in range(min(args.steps, 2000), 0, -1) if args.steps % d == 0)
         gear.gear_table_set_tuning(t.handle, "device_seed", synth.SAMPLE_SEED_BASE + 100000)
         if world > 1:
             gear.gear_table_set_tuning(t.handle, "collect_peer_lsu", peer_lsu)
@@ -459,6 +458,29 @@ def run_gpu(args):
             coll = gev[0].elapsed_time(gev[1]) / S
         return e0.elapsed_time(e1), coll, per_graph * (args.steps // S), S, clk
 
+    def selection_only():
+        """Diagnostic: K steps of the selection alone (sample + update, eager,
+        one stream, no collect), device time per step -- what the pipelined
+        step has to hide behind each collect."""
+        for i in range(args.warmup):
+            gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + i, cfg.beta, idx, w,
+                             None, None, stream, flags=sflags)
+        barrier()
+        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(args.steps):
+            gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + i, cfg.beta, idx, w,
+                             None, None, stream, flags=sflags)
+            if cfg.update:
+                gear.gear_update_priorities(t.handle, B, idx, pool[i % 16], gear.GEAR_F64, None,
+                                            stream)
+        z.record(stream)
+        barrier()
+        err, _ = t.sync()
+        assert err == 0, f"device error bits {err} in the selection-only run"
+        return a.elapsed_time(z) / args.steps
+
+    sel_only_ms = selection_only()
     ms, coll_ms_p, launches, clk = timed(step_pipe)
     coll_src = "eager pipelined run (events on the collect stream around each launch)"
     step_pct = dict(timed.percentiles)
@@ -566,10 +588,10 @@ def run_gpu(args):
     e2e_h2d = 8 * B if cfg.update else 0    # f64 priorities
     e2e_d2h = 12 * B                         # u64 ids + f32 weights
 
-    times = torch.tensor([ms, e2e_ms, coll_ms_p, ms_serial, coll_ms_s], device="cuda")
+    times = torch.tensor([ms, e2e_ms, coll_ms_p, ms_serial, coll_ms_s, sel_only_ms], device="cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
-    ms, e2e_ms, coll_avg, ms_serial, coll_serial = (float(x) for x in times.cpu())
+    ms, e2e_ms, coll_avg, ms_serial, coll_serial, sel_only_ms = (float(x) for x in times.cpu())
 
     traj = world * B * args.steps
     value = traj / (ms / 1e3)
@@ -651,6 +673,9 @@ def run_gpu(args):
                    "note": "sample -> collect -> update on one stream, same K steps"},
         "step_ms_percentiles": {**step_pct, "from": ("eager pipelined run, rank 0: intervals "
                                                      "between consecutive collect completions")},
+        "selection": {"only_ms_per_step": sel_only_ms,
+                      "note": ("sample (+ update) alone, eager, one stream, K steps, max over ranks: "
+                               "the pipelined step hides it behind each collect")},
         "roofline": roof,
         "e2e": {"value": traj / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": e2e_h2d,
                 "d2h_bytes_per_step": e2e_d2h,
