@@ -292,7 +292,11 @@ def run_gpu(args):
     # collection streams: with 2, collect(i) and collect(i+1) may overlap (the
     # next step's rows start streaming while this step's tail drains); each
     # stream has its own output batch
-    cstreams = [torch.cuda.Stream() for _ in range(args.collect_streams)]
+    # --collect-priority high: the collect streams get the higher CUDA stream
+    # priority (the block scheduler then prefers the collect's CTAs over the
+    # selection kernels that overlap it)
+    cprio = -1 if args.collect_priority == "high" else 0
+    cstreams = [torch.cuda.Stream(priority=cprio) for _ in range(args.collect_streams)]
     cstream = cstreams[0]
     with torch.cuda.stream(stream):
         outs2 = [outs] + [[torch.empty_like(o) for o in outs] for _ in range(len(cstreams) - 1)]
@@ -783,6 +787,8 @@ def main():
                     help="override the config's strategy")
     ap.add_argument("--collect-streams", type=int, default=1, choices=[1, 2],
                     help="2: consecutive collects on alternating streams may overlap")
+    ap.add_argument("--collect-priority", default="normal", choices=["normal", "high"],
+                    help="CUDA stream priority of the collect streams")
     ap.add_argument("--graph", type=int, default=1,
                     help="also time the pipelined step captured as a CUDA graph")
     ap.add_argument("--assign", default="owner", choices=["owner", "contiguous"],

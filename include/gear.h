@@ -396,6 +396,10 @@ gear_status gear_table_load(gear_table* t, const char* path);
  *   "update_fused": 1 = priority updates of <= 8192 entries (all ranks) run
  *                   tag + apply in one single-CTA launch (default), 0 = two
  *                   grid-wide launches;
+ *   "collect_evict_first": the collect's bulk copies carry an L2 evict-first
+ *                   policy (the rows stream through once and stop evicting
+ *                   the selection's keys / CDFs / mailboxes): -1 = auto, on
+ *                   at W > 1 (default), 0 = off, 1 = on;
  *   "collect_peer_lsu": W > 1: 1 = the peer-HBM rows of bulk-copied (TMA)
  *                   columns are moved by the LSU warps instead of the bulk
  *                   pipeline (+3% collect throughput when few rows are

@@ -1129,6 +1129,7 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
   cp.n = n;
   cp.err = t->err;
   cp.self_rank = t->rank;
+  cp.evict_first = t->evict_first < 0 ? (t->W > 1 ? 1u : 0u) : (uint32_t)t->evict_first;
   cp.tma_ctas_per_sm = (uint32_t)t->tma_ctas;
   cp.tma_stages = (uint32_t)t->tma_stages;
   for (uint32_t c = 0; c < ncols; ++c) {
@@ -1205,6 +1206,8 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     GEAR_CUDA(cudaMemset(t->cdf_buf_mode, 0, 8));  // both buffers: full rebuild
     t->cdf_levels = (int)value;
     t->dirty = true;
+  } else if (!strcmp(key, "collect_evict_first") && value >= -1 && value <= 1) {
+    t->evict_first = (int)value;
   } else if (!strcmp(key, "collect_peer_lsu") && (value == 0 || value == 1)) {
     t->collect_peer_lsu = (int)value;
   } else if (!strcmp(key, "update_fused") && (value == 0 || value == 1)) {

@@ -200,6 +200,7 @@ struct CollectParams {
   uint32_t n;
   uint32_t self_rank;                 // this rank (peer rows: owner != self_rank)
   uint32_t any_peer_lsu;              // some column has peer_lsu
+  uint32_t evict_first;               // bulk copies with an L2 evict-first policy
   uint32_t* err;
 };
 

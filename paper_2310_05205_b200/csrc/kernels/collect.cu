@@ -169,11 +169,51 @@ __device__ __forceinline__ void collect_peer_rows(const CollectParams& p, uint64
   }
 }
 
+// L2 policy of the collect's bulk copies (tuning "collect_evict_first",
+// default on at W > 1): the rows stream through once, so they can be marked
+// evict-first and not push the selection's working set (keys, CDFs,
+// mailboxes) out of L2 while the next step's selection runs next to this
+// collect.  Measured (profiles/r02_ef): +7% at c2 TopK and +0.6% at c2 on 4
+// GPUs, but -2.4% at c2 on 1 GPU, where the selection is small and hidden.
+__device__ __forceinline__ uint64_t collect_l2_policy(bool evict_first) {
+  uint64_t pol = 0;
+  if (evict_first) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// pol == 0: plain copy
+__device__ __forceinline__ void bulk_load_hint(uint32_t stage_addr, const void* src, uint32_t bytes,
+                                               uint32_t bar, uint64_t pol) {
+  if (pol)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            stage_addr),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            stage_addr),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_store_hint(void* dst, uint32_t src, uint32_t bytes, uint64_t pol) {
+  if (pol)
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+                 "r"(src), "r"(bytes), "l"(pol)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+                 "r"(bytes)
+                 : "memory");
+}
+
 // Issue the bulk load of TMA task `task` into stage `s` (mbarrier bars[s]).
 // Returns the bytes moved (0 for an invalid id: the barrier is still armed).
 __device__ __forceinline__ uint32_t tma_issue_load(const CollectParams& p, uint64_t task,
                                                    uint32_t stage_addr, uint32_t bar,
-                                                   uint8_t** dst) {
+                                                   uint8_t** dst, uint64_t pol) {
   uint32_t c;
   uint64_t j, k;
   decode_task(p, p.tma_cols, p.n_tma, task, &c, &j, &k);
@@ -190,11 +230,8 @@ __device__ __forceinline__ uint32_t tma_issue_load(const CollectParams& p, uint6
     *dst = col.out + local * col.rb + off;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            stage_addr),
-        "l"(col.src[0] + (uint64_t)p.meta[j].src_row * col.rb + off), "r"(bytes), "r"(bar)
-        : "memory");
+    bulk_load_hint(stage_addr, col.src[0] + (uint64_t)p.meta[j].src_row * col.rb + off, bytes, bar,
+                   pol);
     return bytes;
   }
   const uint64_t g = __ldg(p.idx + j);
@@ -215,11 +252,7 @@ __device__ __forceinline__ uint32_t tma_issue_load(const CollectParams& p, uint6
   *dst = col.out + j * col.rb + off;
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          stage_addr),
-      "l"(col.src[owner] + local * col.rb + off), "r"(bytes), "r"(bar)
-      : "memory");
+  bulk_load_hint(stage_addr, col.src[owner] + local * col.rb + off, bytes, bar, pol);
   return bytes;
 }
 
@@ -228,21 +261,6 @@ __device__ __forceinline__ uint32_t tma_issue_load(const CollectParams& p, uint6
 // flight while task n is stored; the stage of task n-1 is refilled (task
 // n-1+kStages) once its store has finished reading shared memory
 // (wait_group.read 1: only the store of task n may still be reading).
-// Waits until at most n of this thread's bulk groups are still reading
-// shared memory (the PTX operand must be an immediate).
-__device__ __forceinline__ void bulk_wait_read(uint32_t n) {
-  switch (n) {
-    case 0: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
-    case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
-    case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
-    case 3: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
-    case 4: asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory"); break;
-    case 5: asm volatile("cp.async.bulk.wait_group.read 5;" ::: "memory"); break;
-    case 6: asm volatile("cp.async.bulk.wait_group.read 6;" ::: "memory"); break;
-    default: asm volatile("cp.async.bulk.wait_group.read 7;" ::: "memory"); break;
-  }
-}
-
 template <int kStages>
 __device__ __forceinline__ void tma_body(const CollectParams& p, uint32_t stage_bytes) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -263,27 +281,26 @@ __device__ __forceinline__ void tma_body(const CollectParams& p, uint32_t stage_
   const uint64_t first = blockIdx.x, step = gridDim.x;
   const uint64_t ntask = p.tma_total > first ? (p.tma_total - first + step - 1) / step : 0;
   const uint32_t base = smem_u32(smem);
+  const uint64_t pol = collect_l2_policy(p.evict_first != 0);
   uint8_t* dst[kStages] = {};
   uint32_t nbytes[kStages] = {};
   uint32_t phase = 0;
   for (uint64_t n = 0; n < ntask && n < (uint64_t)kStages; ++n)
     nbytes[n] = tma_issue_load(p, first + n * step, base + (uint32_t)n * stage_bytes,
-                               smem_u32(&bars[n]), &dst[n]);
+                               smem_u32(&bars[n]), &dst[n], pol);
   for (uint64_t n = 0; n < ntask; ++n) {
     const int s = (int)(n % kStages);
     while (!mbar_try_wait(smem_u32(&bars[s]), (phase >> s) & 1u)) {
     }
     phase ^= 1u << s;
-    if (nbytes[s])
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst[s]),
-                   "r"(base + (uint32_t)s * stage_bytes), "r"(nbytes[s])
-                   : "memory");
+    if (nbytes[s]) bulk_store_hint(dst[s], base + (uint32_t)s * stage_bytes, nbytes[s], pol);
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     if (n >= 1 && n - 1 + kStages < ntask) {
       const int sp = (int)((n - 1) % kStages);
       asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       nbytes[sp] = tma_issue_load(p, first + (n - 1 + kStages) * step,
-                                  base + (uint32_t)sp * stage_bytes, smem_u32(&bars[sp]), &dst[sp]);
+                                  base + (uint32_t)sp * stage_bytes, smem_u32(&bars[sp]), &dst[sp],
+                                  pol);
     }
   }
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");

@@ -372,6 +372,11 @@ __global__ void __launch_bounds__(kSortThreads)
 
 uint32_t topk_max_k() { return 8192; }
 
+#ifndef GEAR_TOPK_KEYS_PER_CTA
+#define GEAR_TOPK_KEYS_PER_CTA 256
+#endif
+constexpr uint64_t kTopkKeysPerCta = GEAR_TOPK_KEYS_PER_CTA;
+
 cudaError_t launch_topk_local(const uint64_t* key, uint64_t shard_cap, uint64_t q_max,
                               uint32_t n_shards_local,
                               uint32_t first_shard, uint32_t K, Cand* cand_tmp, Cand* cand_out,
@@ -380,10 +385,12 @@ cudaError_t launch_topk_local(const uint64_t* key, uint64_t shard_cap, uint64_t 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // CTAs per shard: ~2 waves of the GPU over all local shards, >= 1 slice of 256 keys
+  // CTAs per shard: ~2 waves of the GPU over all local shards, >= 1 slice of
+  // kTopkKeysPerCta keys (256; 4096 and 16384 measured 8% / 27% slower at c2
+  // TopK, W = 4: profiles/r02_topk)
   uint32_t G = (uint32_t)(2 * sms) / n_shards_local;
   G = G < 1 ? 1 : G;
-  const uint64_t max_g = (shard_cap + kThreads - 1) / kThreads;
+  const uint64_t max_g = (shard_cap + kTopkKeysPerCta - 1) / kTopkKeysPerCta;
   G = (uint64_t)G > max_g ? (uint32_t)max_g : G;
   G = G > kTopkMaxCtas ? kTopkMaxCtas : G;
   const dim3 grid(G, n_shards_local);

@@ -197,5 +197,6 @@ struct gear_table {
   int tma_ctas = 2;                 // TMA collect CTAs per SM
   int tma_stages = 3;               // shared-memory stages per TMA CTA
   int collect_impl = 1;             // 1: TMA bulk copies for large aligned rows, 0: LSU only
+  int evict_first = -1;             // collect copies L2 evict-first: -1 auto (W > 1), 0, 1
   int collect_peer_lsu = 0;         // W > 1: peer-HBM rows of TMA columns via LSU warps
 };

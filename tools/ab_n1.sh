@@ -1,0 +1,18 @@
+#!/bin/bash
+# A/B of library variants on the 1-GPU bench: tools/ab_n1.sh outdir "bench args" lib1 lib2 ...
+out=gpurun_out/$1; args=$2; shift 2
+mkdir -p $out
+for lib in "$@"; do
+  if [ "$lib" = default ]; then L=paper_2310_05205_b200/libgear.so; else L=paper_2310_05205_b200/ab/libgear_$lib.so; fi
+  GEAR_LIB=$L timeout 900 python bench.py $args 2>> $out/err_$lib.log | tail -1 > $out/bench1_$lib.json
+  python - $out/bench1_$lib.json $lib <<'PY'
+import json, sys
+try:
+    d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
+    r = d["roofline"]
+    print(sys.argv[2], "N=1 value %.3fM" % (d["value"] / 1e6), "ms %.4f" % d["ms_per_step"], "coll %.4f" % r["avg_launch_ms"],
+          "frac %.3f" % r["frac"], "sel_only %.4f" % d["selection"]["only_ms_per_step"], "e2e %.3fM" % (d["e2e"]["value"] / 1e6))
+except Exception as e:
+    print(sys.argv[2], "failed", e)
+PY
+done
