@@ -482,9 +482,19 @@ def run_gpu(args):
         barrier()
         err, _ = t.sync()
         assert err == 0, f"device error bits {err} in the selection-only run"
-        return a.elapsed_time(z) / args.steps
+        total = a.elapsed_time(z) / args.steps
+        # the sample call alone (no update: the CDF stays clean after the first)
+        a.record(stream)
+        for i in range(args.steps):
+            gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + i, cfg.beta, idx, w,
+                             None, None, stream, flags=sflags)
+        z.record(stream)
+        barrier()
+        selection_only.sample_ms = a.elapsed_time(z) / args.steps
+        return total
 
     sel_only_ms = selection_only()
+    sel_sample_ms = selection_only.sample_ms
     ms, coll_ms_p, launches, clk = timed(step_pipe)
     coll_src = "eager pipelined run (events on the collect stream around each launch)"
     step_pct = dict(timed.percentiles)
@@ -592,10 +602,11 @@ def run_gpu(args):
     e2e_h2d = 8 * B if cfg.update else 0    # f64 priorities
     e2e_d2h = 12 * B                         # u64 ids + f32 weights
 
-    times = torch.tensor([ms, e2e_ms, coll_ms_p, ms_serial, coll_ms_s, sel_only_ms], device="cuda")
+    times = torch.tensor([ms, e2e_ms, coll_ms_p, ms_serial, coll_ms_s, sel_only_ms, sel_sample_ms],
+                         device="cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
-    ms, e2e_ms, coll_avg, ms_serial, coll_serial, sel_only_ms = (float(x) for x in times.cpu())
+    ms, e2e_ms, coll_avg, ms_serial, coll_serial, sel_only_ms, sel_sample_ms = (float(x) for x in times.cpu())
 
     traj = world * B * args.steps
     value = traj / (ms / 1e3)
@@ -615,12 +626,28 @@ def run_gpu(args):
     pcie_gbs, pcie_src = PCIE_H2D_GBS, "constant: pinned H2D cudaMemcpy probe of round 1 (profiles/r01_probe_2gpu.jsonl)"
     nvl_gbs, nvl_src = NVLINK_PEER_GBS, "constant: cudaMemcpyPeer pull probe of round 1 (profiles/r01_probe_2gpu.jsonl)"
     barrier()
+    seq_ceiling = None
     if host_bytes > 0:
         try:
             pcie_gbs = probe_h2d_gbs()
             pcie_src = "measured in this run: pinned host -> GPU cudaMemcpy of 1 GiB, best of 3"
         except Exception as e:  # noqa: BLE001
             pcie_src += f" (live probe failed: {e!r})"
+        # context: the same collect kernel on its best-case access pattern (B
+        # consecutive rows of this rank's shard: sequential host reads), what
+        # SM-initiated zero-copy reads reach on this box
+        if dev_bytes == 0:
+            seq = torch.arange(rank * (capacity // world), rank * (capacity // world) + B,
+                               dtype=torch.int64, device="cuda")
+            for _ in range(3):
+                gear.gear_collect(t.handle, B, seq, col_ids, outs, stream)
+            a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(20):
+                gear.gear_collect(t.handle, B, seq, col_ids, outs, stream)
+            z.record(stream)
+            stream.synchronize()
+            seq_ceiling = host_bytes / (a.elapsed_time(z) / 20 / 1e3) / 1e9
     if world > 1 and remote > 0:
         try:
             nvl_gbs = probe_peer_gbs(local, world)
@@ -637,6 +664,13 @@ def run_gpu(args):
     roof = {"bound": bound, "achieved": alg / (coll_avg / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
             "peak_source": {"hbm": hbm_src, "nvlink": nvl_src, "pcie": pcie_src}[bound]}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["probes"] = {"pcie_h2d_GBps": pcie_gbs, "pcie_source": pcie_src,
+                      "nvlink_pull_GBps": nvl_gbs, "nvlink_source": nvl_src}
+    if seq_ceiling and bound == "pcie":
+        roof["sequential_rows_GBps"] = seq_ceiling
+        roof["frac_of_sequential"] = roof["achieved"] / seq_ceiling
+        roof["sequential_note"] = ("context, not the peak: the same collect kernel gathering B "
+                                   "consecutive rows (sequential host reads), 20 launches")
     if roof["frac"] < 0.2:  # e.g. c1: a few hundred KB per launch
         roof["note"] = ("latency-bound: %.0f KB per collect launch, far below what saturates %s"
                         % (alg / 1e3, bound.upper()))
@@ -677,7 +711,7 @@ def run_gpu(args):
                    "note": "sample -> collect -> update on one stream, same K steps"},
         "step_ms_percentiles": {**step_pct, "from": ("eager pipelined run, rank 0: intervals "
                                                      "between consecutive collect completions")},
-        "selection": {"only_ms_per_step": sel_only_ms,
+        "selection": {"only_ms_per_step": sel_only_ms, "sample_only_ms": sel_sample_ms,
                       "note": ("sample (+ update) alone, eager, one stream, K steps, max over ranks: "
                                "the pipelined step hides it behind each collect")},
         "roofline": roof,

@@ -47,7 +47,7 @@ def test_multi_gpu_parity(n):
     _run(n, 29533 + n, {"GEAR_SHARED_DEVICE": "0"})
 
 
-@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("n", [2, 4, 8])
 def test_shared_device_parity(n):
     if _ngpus() < 1:
         pytest.skip("needs a GPU")
