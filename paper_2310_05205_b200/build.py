@@ -16,8 +16,13 @@ import sysconfig
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "libgear.so")
+# A/B variants (tools): GEAR_BUILD_VARIANT=name GEAR_NVCC_EXTRA="-DX=1" builds
+# ab/libgear_<name>.so from build_<name>/ (load it with GEAR_LIB=...)
+VARIANT = os.environ.get("GEAR_BUILD_VARIANT", "")
+EXTRA = os.environ.get("GEAR_NVCC_EXTRA", "").split()
+OBJ = os.path.join(HERE, "build" + (f"_{VARIANT}" if VARIANT else ""))
+LIB = (os.path.join(HERE, "ab", f"libgear_{VARIANT}.so") if VARIANT
+       else os.path.join(HERE, "libgear.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -44,7 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     hdr_mtime = max(os.path.getmtime(h) for h in _headers())
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", *ARCH,
-              "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include")]
+              "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nccl, "include"), *EXTRA]
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     objs, procs = [], []
     for src in sources():
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")

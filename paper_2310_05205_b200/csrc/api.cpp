@@ -199,7 +199,7 @@ void destroy_table(gear_table* t) {
   dfree(t->n_stale); dfree(t->err); dfree(t->d_epoch); dfree(t->d_seed); dfree(t->d_xep);
   for (auto& b : t->col_idx) dfree(b.p);
   dfree(t->d_meta); dfree(t->d_ord); dfree(t->d_out); dfree(t->d_rows);
-  dfree(t->d_prio_ins); dfree(t->d_alloc); dfree(t->ins_bad);
+  dfree(t->d_prio_ins); dfree(t->d_alloc); dfree(t->ins_bad); dfree(t->dyn_pool);
   if (t->h_prio) cudaFreeHost(t->h_prio);
   if (t->h_out) cudaFreeHost(t->h_out);
   if (t->staging_ev) cudaEventDestroy(t->staging_ev);
@@ -245,6 +245,9 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   if (const char* e = getenv("GEAR_COLLECT_CHUNK")) t->chunk_bytes = (uint32_t)atoi(e);
   if (const char* e = getenv("GEAR_TMA_CHUNK")) t->tma_chunk = (uint32_t)atoi(e);
   if (const char* e = getenv("GEAR_COLLECT_PEER_LSU")) t->collect_peer_lsu = atoi(e) != 0;
+  if (const char* e = getenv("GEAR_PEER_XCHG")) t->peer_xchg = atoi(e) != 0;  // A/B (same on every rank)
+  if (const char* e = getenv("GEAR_COLLECT_DYNAMIC")) t->collect_dynamic = atoi(e);
+  if (const char* e = getenv("GEAR_COLLECT_EVICT_FIRST")) t->evict_first = atoi(e);
   if (const char* e = getenv("GEAR_TMA_STAGES")) {
     const int v = atoi(e);
     if (v == 2 || v == 3 || v == 4 || v == 6 || v == 8) t->tma_stages = v;
@@ -510,6 +513,8 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_CUDA(cudaHostAlloc((void**)&t->h_out, MB * sizeof(uint64_t), cudaHostAllocDefault));
   GEAR_TRY(dalloc(&t->d_prio_ins, MB));
   GEAR_TRY(dalloc(&t->d_alloc, t->R));
+  GEAR_TRY(dalloc(&t->dyn_pool, 2 * gear_table::kDynSlots));
+  GEAR_CUDA(cudaMemset(t->dyn_pool, 0, 2 * gear_table::kDynSlots * sizeof(unsigned long long)));
   GEAR_TRY(dalloc(&t->ins_bad, 1));
   GEAR_CUDA(cudaMemset(t->ins_bad, 0, 4));
   {
@@ -1130,6 +1135,8 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
   cp.err = t->err;
   cp.self_rank = t->rank;
   cp.evict_first = t->evict_first < 0 ? (t->W > 1 ? 1u : 0u) : (uint32_t)t->evict_first;
+  if (t->collect_dynamic < 0 ? t->W > 1 : t->collect_dynamic != 0)  // rotating counter pairs:
+    cp.dyn_ctr = t->dyn_pool + 2 * (t->dyn_slot++ % gear_table::kDynSlots);  // overlapping collects differ
   cp.tma_ctas_per_sm = (uint32_t)t->tma_ctas;
   cp.tma_stages = (uint32_t)t->tma_stages;
   for (uint32_t c = 0; c < ncols; ++c) {
@@ -1206,6 +1213,8 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     GEAR_CUDA(cudaMemset(t->cdf_buf_mode, 0, 8));  // both buffers: full rebuild
     t->cdf_levels = (int)value;
     t->dirty = true;
+  } else if (!strcmp(key, "collect_dynamic") && value >= -1 && value <= 1) {
+    t->collect_dynamic = (int)value;
   } else if (!strcmp(key, "collect_evict_first") && value >= -1 && value <= 1) {
     t->evict_first = (int)value;
   } else if (!strcmp(key, "collect_peer_lsu") && (value == 0 || value == 1)) {

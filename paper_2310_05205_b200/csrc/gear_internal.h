@@ -201,6 +201,7 @@ struct CollectParams {
   uint32_t self_rank;                 // this rank (peer rows: owner != self_rank)
   uint32_t any_peer_lsu;              // some column has peer_lsu
   uint32_t evict_first;               // bulk copies with an L2 evict-first policy
+  unsigned long long* dyn_ctr;        // non-null: TMA tasks claimed from this counter pair
   uint32_t* err;
 };
 

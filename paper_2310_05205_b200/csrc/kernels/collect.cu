@@ -256,6 +256,67 @@ __device__ __forceinline__ uint32_t tma_issue_load(const CollectParams& p, uint6
   return bytes;
 }
 
+// Dynamic variant of the issuing lane's in-order ring (tuning
+// "collect_dynamic", default on at W > 1): each task is claimed from a
+// per-launch counter instead of the static stride, so a CTA that starts late
+// -- at W > 1 the next step's selection kernels (a 1024-thread assign CTA,
+// spinning mailbox waits) can hold an SM's registers when the collect
+// launches -- simply takes fewer tasks instead of finishing last with a full
+// share.  The ticket for the next refill is fetched one task ahead, so the
+// atomic's round trip stays off the critical path; the last CTA to finish
+// re-arms the counter pair (graph-safe).
+template <int kStages>
+__device__ __forceinline__ void tma_lane_dynamic(const CollectParams& p, uint32_t base,
+                                                 uint64_t* bars, uint32_t stage_bytes,
+                                                 uint64_t pol) {
+  unsigned long long* ctr = p.dyn_ctr;  // [0] next task, [1] CTAs done
+  uint8_t* dst[kStages] = {};
+  uint32_t nbytes[kStages] = {};
+  uint32_t phase = 0;
+  int inflight = 0;
+  bool more = true;
+  uint64_t next = atomicAdd(ctr, 1ull);  // prefetched ticket
+  for (int s = 0; s < kStages; ++s) {
+    const uint64_t task = next;
+    if (task >= p.tma_total) {
+      more = false;
+      break;
+    }
+    next = atomicAdd(ctr, 1ull);
+    nbytes[s] = tma_issue_load(p, task, base + (uint32_t)s * stage_bytes, smem_u32(&bars[s]),
+                               &dst[s], pol);
+    ++inflight;
+  }
+  for (uint64_t n = 0; inflight > 0; ++n) {
+    const int s = (int)(n % kStages);
+    while (!mbar_try_wait(smem_u32(&bars[s]), (phase >> s) & 1u)) {
+    }
+    phase ^= 1u << s;
+    --inflight;
+    if (nbytes[s]) bulk_store_hint(dst[s], base + (uint32_t)s * stage_bytes, nbytes[s], pol);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (n >= 1 && more) {  // refill the previous stage (cyclic order is kept)
+      const int sp = (int)((n - 1) % kStages);
+      const uint64_t task = next;
+      if (task < p.tma_total) {
+        next = atomicAdd(ctr, 1ull);
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        nbytes[sp] = tma_issue_load(p, task, base + (uint32_t)sp * stage_bytes,
+                                    smem_u32(&bars[sp]), &dst[sp], pol);
+        ++inflight;
+      } else {
+        more = false;
+      }
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __threadfence();
+  if (atomicAdd(ctr + 1, 1ull) == gridDim.x - 1) {  // every CTA has stopped claiming
+    ctr[0] = 0;
+    ctr[1] = 0;
+  }
+}
+
 // Pipeline of the issuing lane, over its tasks n = 0, 1, ... (task id
 // blockIdx.x + n * gridDim.x):  loads of tasks n+1 .. n+kStages-1 are in
 // flight while task n is stored; the stage of task n-1 is refilled (task
@@ -282,6 +343,10 @@ __device__ __forceinline__ void tma_body(const CollectParams& p, uint32_t stage_
   const uint64_t ntask = p.tma_total > first ? (p.tma_total - first + step - 1) / step : 0;
   const uint32_t base = smem_u32(smem);
   const uint64_t pol = collect_l2_policy(p.evict_first != 0);
+  if (p.dyn_ctr != nullptr) {
+    tma_lane_dynamic<kStages>(p, base, bars, stage_bytes, pol);
+    return;
+  }
   uint8_t* dst[kStages] = {};
   uint32_t nbytes[kStages] = {};
   uint32_t phase = 0;

@@ -97,9 +97,9 @@ __global__ void __launch_bounds__(kLocalThreads)
   }
   __syncthreads();
   if (tid == 0) {
-    __threadfence_system();
+    mbox_producer_fence();
     for (uint32_t r = 0; r < m.W; ++r)
-      st_release_sys_u64(mbox_at<uint64_t>(m, r, L.cflag) + b * m.S + shard, m.epoch);
+      mbox_publish(mbox_at<uint64_t>(m, r, L.cflag) + b * m.S + shard, m.epoch);
   }
 }
 

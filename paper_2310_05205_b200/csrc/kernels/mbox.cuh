@@ -2,15 +2,29 @@
 //
 // Producer: plain stores of the payload into every peer's mailbox (CUDA-IPC
 // mapped device memory, so each store crosses NVLink), a block barrier, then
-// one thread issues a system-scope fence and a release store of the epoch
-// into the peer's flag slot for this producer.  Consumer: one thread spins
-// with acquire loads on its own mailbox flags until every producer has
-// published this epoch (flags only grow), a block barrier, then the block
+// ONE thread issues ONE system-scope fence (fence.acq_rel.sys) followed by
+// relaxed system-scope stores of the epoch into each peer's flag slot for
+// this producer -- the fence + strong-store release pattern of the PTX memory
+// model, covering the payload stores the barrier ordered before the fence.
+// Consumer: one thread polls its own mailbox flags with relaxed system-scope
+// loads until every producer has published this epoch (flags only grow), then
+// ONE fence.acq_rel.sys (acquire pattern), a block barrier, and the block
 // reads the payload with L1-bypassing loads.  A spin longer than ~4 s latches
 // kErrTimeout and gives up instead of hanging the GPU.
+//
+// Round 1 used a release store per peer flag and an acquire load per poll:
+// each compiles to a MEMBAR.ALL.SYS, which drains the SM's outstanding
+// memory operations -- with a zero-copy collect running on the same SMs the
+// per-poll / per-flag system barriers cost c3 (4 KB host rows) 6-16% at N=4
+// (profiles/r02_multi: mailbox vs NCCL exchange, protocol A/B).
+// GEAR_MBOX_PROTO=0 builds the round-1 protocol for A/B.
 #pragma once
 
 #include "common.cuh"
+
+#ifndef GEAR_MBOX_PROTO
+#define GEAR_MBOX_PROTO 1
+#endif
 
 namespace gear {
 
@@ -20,8 +34,18 @@ __device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p) {
   return v;
 }
 
+__device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void st_release_sys_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ uint64_t global_ns() {
@@ -30,12 +54,35 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 
+// Producer, by the one publishing thread after the block barrier that follows
+// the payload stores: the release fence ...
+__device__ __forceinline__ void mbox_producer_fence() {
+#if GEAR_MBOX_PROTO
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+#else
+  __threadfence_system();
+#endif
+}
+
+// ... then one flag store per peer (after mbox_producer_fence).
+__device__ __forceinline__ void mbox_publish(uint64_t* flag, uint64_t epoch) {
+#if GEAR_MBOX_PROTO
+  st_relaxed_sys_u64(flag, epoch);
+#else
+  st_release_sys_u64(flag, epoch);
+#endif
+}
+
 // Spin until flags[0..n) >= epoch.  Returns false on timeout (error latched).
 __device__ __forceinline__ bool mbox_wait(const uint64_t* flags, uint32_t n, uint64_t epoch,
                                           uint32_t* err) {
   const uint64_t t0 = global_ns();
   for (uint32_t i = 0; i < n; ++i) {
+#if GEAR_MBOX_PROTO
+    while (ld_relaxed_sys_u64(flags + i) < epoch) {
+#else
     while (ld_acquire_sys_u64(flags + i) < epoch) {
+#endif
       if (global_ns() - t0 > 4000000000ull) {
         atomicOr(err, kErrTimeout);
         return false;
@@ -43,12 +90,12 @@ __device__ __forceinline__ bool mbox_wait(const uint64_t* flags, uint32_t n, uin
       __nanosleep(64);
     }
   }
+#if GEAR_MBOX_PROTO
+  asm volatile("fence.acq_rel.sys;" ::: "memory");  // acquire: the relaxed loads saw the flags
+#endif
   return true;
 }
 
-// True once any exchange of this table timed out (the bit stays latched until
-// gear_table_sync): the SPMD protocol is broken, so consumers of exchanged
-// data write GEAR_IDX_NONE / skip their writes instead of using stale data.
 __device__ __forceinline__ bool mbox_failed(const uint32_t* err) {
   return (*(const volatile uint32_t*)err & kErrTimeout) != 0;
 }
@@ -85,9 +132,9 @@ __device__ __forceinline__ const ShardTotals* mbox_exchange_totals(const Mbox& m
   }
   __syncthreads();
   if (tid == 0) {
-    __threadfence_system();
+    mbox_producer_fence();
     for (uint32_t r = 0; r < m.W; ++r)
-      st_release_sys_u64(mbox_at<uint64_t>(m, r, L.tflag) + b * m.W + m.rank, m.epoch);
+      mbox_publish(mbox_at<uint64_t>(m, r, L.tflag) + b * m.W + m.rank, m.epoch);
     mbox_wait(mbox_at<uint64_t>(m, m.rank, L.tflag) + b * m.W, m.W, m.epoch, err);
   }
   __syncthreads();

@@ -350,22 +350,22 @@ __global__ void __launch_bounds__(kSortThreads)
   // The last CTA of the shard publishes the list length and the epoch flag.
   __syncthreads();
   if (tid == 0) {
-    __threadfence_system();
+    mbox_producer_fence();
     s_last = atomicAdd(&st[ls].ctr, 1u) == gridDim.x - 1;
     if (s_last) st[ls].ctr = 0;
   }
   __syncthreads();
   if (!s_last || tid != 0) return;
-  __threadfence_system();
+  mbox_producer_fence();
   const MboxLayout L = mbox_layout(m.W, m.S, m.MB);
   const uint32_t b = mbox_buf(m);
   ShardTotals t;
   t.total_and_parity = 0;
   t.aux = n_out;
   for (uint32_t r = 0; r < m.W; ++r) mbox_at<ShardTotals>(m, r, L.ccnt)[b * m.S + shard] = t;
-  __threadfence_system();
+  mbox_producer_fence();
   for (uint32_t r = 0; r < m.W; ++r)
-    st_release_sys_u64(mbox_at<uint64_t>(m, r, L.cflag) + b * m.S + shard, m.epoch);
+    mbox_publish(mbox_at<uint64_t>(m, r, L.cflag) + b * m.S + shard, m.epoch);
 }
 
 }  // namespace

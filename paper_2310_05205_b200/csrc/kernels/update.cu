@@ -213,9 +213,9 @@ __global__ void __launch_bounds__(kFusedThreads)
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    mbox_producer_fence();
     for (uint32_t dst = 0; dst < mb.W; ++dst)
-      st_release_sys_u64(mbox_at<uint64_t>(mb, dst, L.uflag) + bsel * mb.W + mb.rank, mb.epoch);
+      mbox_publish(mbox_at<uint64_t>(mb, dst, L.uflag) + bsel * mb.W + mb.rank, mb.epoch);
     mbox_wait(mbox_at<uint64_t>(mb, mb.rank, L.uflag) + bsel * mb.W, mb.W, mb.epoch, err);
   }
   __syncthreads();
