@@ -396,10 +396,10 @@ gear_status gear_table_load(gear_table* t, const char* path);
  *   "update_fused": 1 = priority updates of <= 8192 entries (all ranks) run
  *                   tag + apply in one single-CTA launch (default), 0 = two
  *                   grid-wide launches;
- *   "collect_dynamic": the bulk pipeline claims its tasks from a per-launch
- *                   counter instead of a static stride, so CTAs that start
- *                   late (an SM held by a concurrent selection kernel) take
- *                   fewer tasks: -1 = auto, on at W > 1 (default), 0, 1;
+ *   "collect_dynamic": 1 = the bulk pipeline claims its tasks from a
+ *                   per-launch counter (default), so CTAs that start late (an
+ *                   SM held by a concurrent selection kernel) or hit slow
+ *                   rows take fewer tasks; 0 = a static stride;
  *   "collect_evict_first": the collect's bulk copies carry an L2 evict-first
  *                   policy (the rows stream through once and stop evicting
  *                   the selection's keys / CDFs / mailboxes): -1 = auto, on
