@@ -397,9 +397,10 @@ gear_status gear_table_load(gear_table* t, const char* path);
  *                   tag + apply in one single-CTA launch (default), 0 = two
  *                   grid-wide launches;
  *   "collect_dynamic": 1 = the bulk pipeline claims its tasks from a
- *                   per-launch counter (default), so CTAs that start late (an
- *                   SM held by a concurrent selection kernel) or hit slow
- *                   rows take fewer tasks; 0 = a static stride;
+ *                   per-launch counter, so CTAs that start late (an SM held
+ *                   by a concurrent selection kernel) or hit slow rows take
+ *                   fewer tasks; 0 = a static stride; -1 = auto (default):
+ *                   dynamic at W > 1 or when host-resident rows are read;
  *   "collect_evict_first": the collect's bulk copies carry an L2 evict-first
  *                   policy (the rows stream through once and stop evicting
  *                   the selection's keys / CDFs / mailboxes): -1 = auto, on

@@ -1135,8 +1135,15 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
   cp.err = t->err;
   cp.self_rank = t->rank;
   cp.evict_first = t->evict_first < 0 ? (t->W > 1 ? 1u : 0u) : (uint32_t)t->evict_first;
-  if (t->collect_dynamic != 0)  // rotating counter pairs:
-    cp.dyn_ctr = t->dyn_pool + 2 * (t->dyn_slot++ % gear_table::kDynSlots);  // overlapping collects differ
+  bool any_host = false;
+  for (uint32_t c = 0; c < ncols; ++c)
+    any_host |= col_ids[c] < t->cols.size() && t->cols[col_ids[c]].placement == GEAR_HOST;
+  // dynamic task claiming: auto = at W > 1 (selection kernels next to the
+  // collect) or with host rows (uneven PCIe row latencies); HBM-only at W = 1
+  // keeps the static stride (measured 1% faster at c2)
+  const bool dynamic = t->collect_dynamic < 0 ? (t->W > 1 || any_host) : t->collect_dynamic != 0;
+  if (dynamic)  // rotating counter pairs: overlapping collects differ
+    cp.dyn_ctr = t->dyn_pool + 2 * (t->dyn_slot++ % gear_table::kDynSlots);
   cp.tma_ctas_per_sm = (uint32_t)t->tma_ctas;
   cp.tma_stages = (uint32_t)t->tma_stages;
   for (uint32_t c = 0; c < ncols; ++c) {
@@ -1213,7 +1220,7 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     GEAR_CUDA(cudaMemset(t->cdf_buf_mode, 0, 8));  // both buffers: full rebuild
     t->cdf_levels = (int)value;
     t->dirty = true;
-  } else if (!strcmp(key, "collect_dynamic") && (value == 0 || value == 1)) {
+  } else if (!strcmp(key, "collect_dynamic") && value >= -1 && value <= 1) {
     t->collect_dynamic = (int)value;
   } else if (!strcmp(key, "collect_evict_first") && value >= -1 && value <= 1) {
     t->evict_first = (int)value;

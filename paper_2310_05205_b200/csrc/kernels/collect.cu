@@ -257,8 +257,9 @@ __device__ __forceinline__ uint32_t tma_issue_load(const CollectParams& p, uint6
 }
 
 // Dynamic variant of the issuing lane's in-order ring (tuning
-// "collect_dynamic", default on: +6% c2 TopK at N=4, +3% c3 at N=1, neutral
-// at c2 N=1 -- profiles/r02_multi): each task is claimed from a
+// "collect_dynamic", default on at W > 1 or with host rows: +6% c2 TopK at
+// N=4, +3% c3 at N=1; off for HBM rows at W = 1, where it cost ~1% at c2 --
+// profiles/r02_multi): each task is claimed from a
 // per-launch counter instead of the static stride, so a CTA that starts late
 // -- at W > 1 the next step's selection kernels (a 1024-thread assign CTA,
 // spinning mailbox waits) can hold an SM's registers when the collect
