@@ -403,8 +403,9 @@ gear_status gear_table_load(gear_table* t, const char* path);
  *                   dynamic at W > 1 or when host-resident rows are read;
  *   "collect_evict_first": the collect's bulk copies carry an L2 evict-first
  *                   policy (the rows stream through once and stop evicting
- *                   the selection's keys / CDFs / mailboxes): -1 = auto, on
- *                   at W > 1 (default), 0 = off, 1 = on;
+ *                   the selection's keys / CDFs / mailboxes): -1 = auto
+ *                   (default): on at W > 1 after a TopK selection, 0 = off,
+ *                   1 = on;
  *   "collect_peer_lsu": W > 1: 1 = the peer-HBM rows of bulk-copied (TMA)
  *                   columns are moved by the LSU warps instead of the bulk
  *                   pipeline (+3% collect throughput when few rows are

@@ -901,6 +901,7 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
   const bool dseed = (flags & GEAR_SAMPLE_DEVICE_SEED) != 0;
   if ((int)strategy < GEAR_FIFO || (int)strategy > GEAR_TOPK)
     return set_error(GEAR_ERR_INVALID_ARG, "bad strategy %d", (int)strategy);
+  t->last_topk = strategy == GEAR_TOPK;
   if (B > t->max_batch) return set_error(GEAR_ERR_INVALID_ARG, "B %u > max_batch %u", B, t->max_batch);
   if (B == 0) return GEAR_OK;
   if (out_idx == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "out_idx is NULL");
@@ -1134,7 +1135,11 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
   cp.n = n;
   cp.err = t->err;
   cp.self_rank = t->rank;
-  cp.evict_first = t->evict_first < 0 ? (t->W > 1 ? 1u : 0u) : (uint32_t)t->evict_first;
+  // L2 evict-first bulk copies: auto = at W > 1 after a TopK selection, whose
+  // grid-wide radix passes re-read the keys from L2 while this collect runs
+  // (+7-11% c2 TopK at N=4); for the other strategies it cost ~1.5% (c2, N=2/4)
+  cp.evict_first = t->evict_first < 0 ? (t->W > 1 && t->last_topk ? 1u : 0u)
+                                      : (uint32_t)t->evict_first;
   bool any_host = false;
   for (uint32_t c = 0; c < ncols; ++c)
     any_host |= col_ids[c] < t->cols.size() && t->cols[col_ids[c]].placement == GEAR_HOST;

@@ -197,7 +197,8 @@ struct gear_table {
   int tma_ctas = 2;                 // TMA collect CTAs per SM
   int tma_stages = 3;               // shared-memory stages per TMA CTA
   int collect_impl = 1;             // 1: TMA bulk copies for large aligned rows, 0: LSU only
-  int evict_first = -1;             // collect copies L2 evict-first: -1 auto (W > 1), 0, 1
+  int evict_first = -1;             // collect copies L2 evict-first: -1 auto (W > 1 after TopK), 0, 1
+  bool last_topk = false;           // the most recent gear_sample was TopK
   int collect_dynamic = -1;         // TMA tasks from a counter: -1 auto (W > 1 or host rows), 0, 1
   static constexpr uint32_t kDynSlots = 8;
   unsigned long long* dyn_pool = nullptr;  // [kDynSlots][2] task counters (rotating)
