@@ -25,6 +25,9 @@
 #ifndef GEAR_MBOX_PROTO
 #define GEAR_MBOX_PROTO 1
 #endif
+#ifndef GEAR_MBOX_SLEEP_NS
+#define GEAR_MBOX_SLEEP_NS 64
+#endif
 
 namespace gear {
 
@@ -87,7 +90,7 @@ __device__ __forceinline__ bool mbox_wait(const uint64_t* flags, uint32_t n, uin
         atomicOr(err, kErrTimeout);
         return false;
       }
-      __nanosleep(64);
+      __nanosleep(GEAR_MBOX_SLEEP_NS);
     }
   }
 #if GEAR_MBOX_PROTO
