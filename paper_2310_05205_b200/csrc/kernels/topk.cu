@@ -24,6 +24,8 @@
 // The global merge is the FIFO/LIFO merge with the TopK order (fifo.cu).
 // Every launch is stream-ordered and every counter re-arms itself, so the
 // sequence can be captured in a CUDA graph.
+#include <cooperative_groups.h>
+
 #include "mbox.cuh"
 
 namespace gear {
@@ -304,6 +306,212 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---- small shards: the whole local select in ONE launch on a thread-block
+// cluster (B200 distributed shared memory) --------------------------------
+// kClusterCtas CTAs of one cluster share a shard (a contiguous slice each).
+// Every step that the grid-wide path does with a separate launch and global
+// atomics -- stats, each radix pass, the counts -- is a cluster barrier here:
+// each CTA builds its partial (count, max, 256-bin histogram, gt/eq counts)
+// in its own shared memory and every CTA reads all of them through DSMEM
+// (cluster.map_shared_rank) and takes the same decision.  The candidates go
+// to the same unsorted list and totals as write_kernel's, for sort_kernel.
+constexpr int kClusterCtas = 8;          // portable cluster size
+constexpr int kClusterThreads = 512;
+// Shards up to 64 K keys (c2 at W >= 2): the cluster holds 8 SMs for the
+// select, so bigger shards keep the grid-wide path, which at c2 W = 1
+// (100 K keys) measured 2.6% faster next to the collect (profiles/r02_topk2).
+constexpr uint64_t kClusterMaxKeys = 1u << 16;
+
+namespace cg = cooperative_groups;
+
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterThreads)
+    topk_cluster_kernel(const uint64_t* __restrict__ key, uint64_t shard_cap, uint32_t K,
+                        uint32_t first_shard, Cand* __restrict__ cand_out,
+                        ShardTotals* __restrict__ totals_out) {
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ uint32_t s_hist[256];
+  __shared__ uint32_t s_scan[kClusterThreads / 32];
+  __shared__ uint32_t s_cnt, s_gt, s_eq;
+  __shared__ unsigned long long s_max;
+  __shared__ uint64_t s_prefix, s_mask;
+  __shared__ uint32_t s_kremain, s_all, s_eqall;
+  __shared__ int s_shift;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t cr = cluster.block_rank();
+  const uint32_t ls = blockIdx.y;
+  const Slice sl = cta_slice(shard_cap, kClusterCtas, cr);
+  const uint64_t* k = key + (uint64_t)ls * shard_cap;
+
+  // stats: selectable count and maximum key of the shard
+  if (tid == 0) {
+    s_cnt = 0;
+    s_max = 0;
+  }
+  __syncthreads();
+  {
+    uint32_t cnt = 0;
+    unsigned long long mx = 0;
+    for (uint64_t i = sl.begin + tid; i < sl.end; i += kClusterThreads) {
+      const uint64_t x = k[i];
+      cnt += x > 0;
+      mx = x > mx ? x : mx;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      cnt += __shfl_xor_sync(kFull, cnt, d);
+      const unsigned long long o = __shfl_xor_sync(kFull, mx, d);
+      mx = o > mx ? o : mx;
+    }
+    if (lane == 0) {
+      atomicAdd(&s_cnt, cnt);
+      atomicMax(&s_max, mx);
+    }
+  }
+  cluster.sync();
+  if (tid == 0) {
+    uint32_t n = 0;
+    unsigned long long mx = 0;
+    for (int r = 0; r < kClusterCtas; ++r) {
+      n += *cluster.map_shared_rank(&s_cnt, r);
+      const unsigned long long m = *cluster.map_shared_rank(&s_max, r);
+      mx = m > mx ? m : mx;
+    }
+    s_all = n <= K;
+    s_eqall = 0;
+    s_kremain = K;
+    s_prefix = 0;
+    s_mask = 0;
+    s_shift = s_all ? -1 : (mx ? ((63 - __clzll(mx)) / 8) * 8 : 0);
+  }
+  __syncthreads();
+
+  // radix select of the K-th largest key, one byte per pass from the top
+  while (s_shift >= 0) {
+    const int shift = s_shift;
+    const uint64_t prefix = s_prefix, mask = s_mask;
+    cluster.sync();  // every CTA is done reading the previous pass's histograms
+    for (int b = tid; b < 256; b += kClusterThreads) s_hist[b] = 0;
+    __syncthreads();
+    for (uint64_t i = sl.begin + tid; i < sl.end; i += kClusterThreads) {
+      const uint64_t x = k[i];
+      if (x > 0 && (x & mask) == prefix) atomicAdd(&s_hist[(x >> shift) & 255], 1u);
+    }
+    cluster.sync();  // every CTA's histogram is complete
+    // the shard's histogram (thread t < 256 owns bin 255 - t, summed over the
+    // cluster through DSMEM), then the digit: the largest v whose suffix
+    // count reaches k_remain (block-wide inclusive scan over t)
+    uint32_t h = 0;
+    if (tid < 256)
+      for (int r = 0; r < kClusterCtas; ++r) h += cluster.map_shared_rank(s_hist, r)[255 - tid];
+    uint32_t suf = h;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(kFull, suf, d);
+      if (lane >= d) suf += o;
+    }
+    if (lane == 31) s_scan[warp] = suf;
+    __syncthreads();
+    for (int w = 0; w < warp && tid < 256; ++w) suf += s_scan[w];
+    const uint32_t kk = s_kremain;
+    __syncthreads();  // s_kremain read by every thread before it changes
+    if (tid < 256 && suf >= kk && suf - h < kk) {  // exactly one thread
+      const uint32_t v = 255 - tid;
+      const uint32_t need = kk - (suf - h);
+      s_prefix = prefix | ((uint64_t)v << shift);
+      s_mask = mask | (255ull << shift);
+      s_kremain = need;
+      const bool small = h - need <= kTopkEqMax;  // as hist_kernel
+      s_eqall = small ? 1u : 0u;
+      s_shift = (small || shift == 0) ? -1 : shift - 8;
+    }
+    __syncthreads();
+  }
+
+  // counts of keys > T* and == T* per CTA, offsets from the CTAs before it
+  TopkState S{};
+  S.all = s_all;
+  S.prefix = s_prefix;
+  S.mask = s_mask;
+  const uint32_t need = s_all ? 0u : (s_eqall ? 0xffffffffu : s_kremain);
+  if (tid == 0) s_gt = s_eq = 0;
+  __syncthreads();
+  {
+    uint32_t g = 0, e = 0;
+    for (uint64_t i = sl.begin + tid; i < sl.end; i += kClusterThreads) {
+      bool gt, eq;
+      classify(S, k[i], &gt, &eq);
+      g += gt;
+      e += eq;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      g += __shfl_xor_sync(kFull, g, d);
+      e += __shfl_xor_sync(kFull, e, d);
+    }
+    if (lane == 0) {
+      atomicAdd(&s_gt, g);
+      atomicAdd(&s_eq, e);
+    }
+  }
+  cluster.sync();
+  uint32_t base_gt = 0, eq_seen = 0, tg = 0, te = 0;
+  for (int r = 0; r < kClusterCtas; ++r) {
+    const uint32_t g = *cluster.map_shared_rank(&s_gt, r), e = *cluster.map_shared_rank(&s_eq, r);
+    if (r < (int)cr) {
+      base_gt += g;
+      eq_seen += e;
+    }
+    tg += g;
+    te += e;
+  }
+  cluster.sync();  // no DSMEM access after this: any CTA may exit
+  const uint32_t cap = K + kTopkEqMax;
+  const uint32_t tot = min(cap, tg + min(need, te));
+
+  // write: compaction in slot order (ties: the first `need` in slot order)
+  uint32_t taken = base_gt + min(need, eq_seen);
+  Cand* out = cand_out + (uint64_t)ls * cap;
+  for (uint64_t i0 = sl.begin; i0 < sl.end; i0 += kClusterThreads) {
+    const uint64_t i = i0 + tid;
+    const uint64_t x = i < sl.end ? k[i] : 0;
+    bool gt = false, eq = false;
+    if (i < sl.end) classify(S, x, &gt, &eq);
+    const unsigned mg = __ballot_sync(kFull, gt), me = __ballot_sync(kFull, eq);
+    if (lane == 0) s_scan[warp] = (__popc(me) << 16) | __popc(mg);
+    __syncthreads();
+    uint32_t gt_before = 0, eq_before = 0, gt_total = 0, eq_total = 0;
+    for (int w = 0; w < kClusterThreads / 32; ++w) {
+      const uint32_t c = s_scan[w];
+      if (w < warp) {
+        gt_before += c & 0xffff;
+        eq_before += c >> 16;
+      }
+      gt_total += c & 0xffff;
+      eq_total += c >> 16;
+    }
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t my_eq_rank = eq_seen + eq_before + __popc(me & lt);
+    const uint32_t eq_taken_before = min(need, my_eq_rank) - min(need, eq_seen);
+    if (gt || (eq && my_eq_rank < need)) {
+      Cand c;
+      c.seq = x;
+      c.shard = first_shard + ls;
+      c.slot = (uint32_t)i;
+      const uint32_t pos = taken + gt_before + __popc(mg & lt) + eq_taken_before;
+      if (pos < cap) out[pos] = c;
+    }
+    taken += gt_total + (min(need, eq_seen + eq_total) - min(need, eq_seen));
+    eq_seen += eq_total;
+    __syncthreads();
+  }
+  if (cr == 0 && tid == 0) {  // candidates for the sort, list length for the merge
+    ShardTotals t;
+    t.total_and_parity = tot;
+    t.aux = min(tot, K);
+    totals_out[ls] = t;
+  }
+}
+
 // Candidate order of TopK: larger key first, then smaller slot.
 __device__ __forceinline__ bool before(const Cand& a, const Cand& b) {
   return a.seq > b.seq || (a.seq == b.seq && a.slot < b.slot);
@@ -372,6 +580,15 @@ __global__ void __launch_bounds__(kSortThreads)
 
 uint32_t topk_max_k() { return 8192; }
 
+// GEAR_TOPK_CLUSTER=0 forces the grid-wide path for every shard size (A/B).
+bool topk_cluster_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("GEAR_TOPK_CLUSTER");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
+}
+
 #ifndef GEAR_TOPK_KEYS_PER_CTA
 #define GEAR_TOPK_KEYS_PER_CTA 256
 #endif
@@ -398,13 +615,21 @@ cudaError_t launch_topk_local(const uint64_t* key, uint64_t shard_cap, uint64_t 
   // bytes (6 at c2); the passes after an early exit are no-op launches.
   int passes = 1;
   while (passes < 8 && (q_max >> (8 * passes)) != 0) ++passes;
-  count_launch(4 + passes);
-  stats_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, K, state);
-  for (int pass = 0; pass < passes; ++pass)  // one per key byte from the top
-    hist_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, state);
-  count_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, state, cnt);
-  write_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, K, first_shard, state, cnt, cand_tmp,
-                                         totals_out);
+  if (shard_cap <= kClusterMaxKeys && topk_cluster_enabled()) {
+    // small shards: stats + every radix pass + counts + compaction in one
+    // cluster launch (DSMEM instead of global atomics between launches)
+    count_launch(2);
+    topk_cluster_kernel<<<dim3(kClusterCtas, n_shards_local), kClusterThreads, 0, s>>>(
+        key, shard_cap, K, first_shard, cand_tmp, totals_out);
+  } else {
+    count_launch(4 + passes);
+    stats_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, K, state);
+    for (int pass = 0; pass < passes; ++pass)  // one per key byte from the top
+      hist_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, state);
+    count_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, state, cnt);
+    write_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, K, first_shard, state, cnt, cand_tmp,
+                                           totals_out);
+  }
   const dim3 sgrid((K + kTopkEqMax + kSortWarps - 1) / kSortWarps, n_shards_local);
   sort_kernel<<<sgrid, kSortThreads, 0, s>>>(K, first_shard, cand_tmp, cand_out, totals_out,
                                                 state, mbox ? *mbox : Mbox{}, mbox != nullptr);

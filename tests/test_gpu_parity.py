@@ -254,14 +254,16 @@ def test_topk_with_ties(torch_cuda, R):
     P.close()
 
 
+@pytest.mark.parametrize("Cs", [120_000, 65_000, 60_000])
 @pytest.mark.parametrize("R,kind", [(1, "ties"), (1, "lognormal"), (3, "ties"), (2, "equal")])
-def test_topk_large_multi_cta(torch_cuda, R, kind):
-    """TopK over shards spread across many CTAs per shard (radix-select
-    histograms merged in global memory, offsets across CTAs) at the maximum
+def test_topk_large_multi_cta(torch_cuda, R, kind, Cs):
+    """TopK over shards spread across many CTAs per shard at the maximum
     K = 8192: ties straddling CTA slices, continuous keys (early exit of the
-    select), and every key equal (the K taken are the K smallest slots)."""
+    select), and every key equal (the K taken are the K smallest slots).
+    120 K / 65 K keys per shard take the grid-wide path (radix histograms
+    merged in global memory), 60 K keys the cluster path (histograms merged
+    through distributed shared memory)."""
     cols = [synth.ColSpec("x", "u8", (8,))]
-    Cs = 120_000
     P = _pair(capacity=Cs * R, seq_len=1, colspecs=cols, R=R, max_batch=8192)
     rng = np.random.default_rng(77 + R)
     if kind == "ties":
