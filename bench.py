@@ -568,6 +568,7 @@ def run_gpu(args):
     ev_copied = [torch.cuda.Event() for _ in range(2)]
     np_idx2 = [x.numpy() for x in h_idx2]   # host views of the pinned buffers
     np_w2 = [x.numpy() for x in h_w2]
+    dw2 = [torch.empty(B, dtype=torch.float32, device="cuda") for _ in range(2)]
     consumed = 0.0
 
     def step_e2e(i):
@@ -576,11 +577,14 @@ def run_gpu(args):
             stream.wait_event(ev_collected[b])   # collect(i-2) has read idx2[b]
             stream.wait_event(ev_copied[b])      # and so has its host copy
         gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + 7919 + i, cfg.beta,
-                         idx2[b], h_w2[hb], None, None, stream, flags=sflags)
+                         idx2[b], h_w2[hb] if args.e2e_weights == "host" else dw2[b], None, None,
+                         stream, flags=sflags)
         ev_sampled[b].record(stream)
         xstream.wait_event(ev_sampled[b])
         with torch.cuda.stream(xstream):
             h_idx2[hb].copy_(idx2[b], non_blocking=True)
+            if args.e2e_weights == "device":
+                h_w2[hb].copy_(dw2[b], non_blocking=True)
         ev_copied[b].record(xstream)
         ev_hs[hb].record(xstream)
         if cfg.update:
@@ -835,6 +839,9 @@ def main():
                     help="override the config's strategy")
     ap.add_argument("--collect-streams", type=int, default=1, choices=[1, 2],
                     help="2: consecutive collects on alternating streams may overlap")
+    ap.add_argument("--e2e-weights", default="host", choices=["host", "device"],
+                    help="e2e: the sample kernel writes the IS weights to pinned host memory in "
+                         "place (host) or to HBM, copied with the ids (device)")
     ap.add_argument("--collect-priority", default="normal", choices=["normal", "high"],
                     help="CUDA stream priority of the collect streams")
     ap.add_argument("--graph", type=int, default=1,
