@@ -522,6 +522,228 @@ __global__ void __launch_bounds__(kThreads) scan2_kernel(
   }
 }
 
+// Persistent two-level rebuild (default for large shards; `scan2_kernel`,
+// one CTA per tile, stays for small ones).  2 CTAs per SM; CTA b owns the
+// tiles b, b + G, b + 2G, ...  It first reads the dirty words of its tiles
+// (block-wide, in chunks of kThreads) and compacts the ones to rescan into a
+// shared-memory work list, so a clean tile costs one coalesced word -- the
+// incremental no-op of a 40 M-key table no longer launches 9766 CTAs.  Work
+// tiles stream through three shared-memory buffers: TMA bulk loads
+// (cp.async.bulk + mbarrier) two tiles ahead, the tile-local scan in place
+// (the rotated 128-bit layout of scan_kernel), coalesced 16-B stores.  Each
+// CTA then adds its tiles to every shard's arrival counter in one atomic;
+// the CTA that completes a shard builds that shard's prefix of tile totals,
+// and the last shard flips the parity and records the buffer's mode, as in
+// scan2_kernel.
+template <bool kIndicator>
+__global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan2p_kernel(
+    const uint64_t* __restrict__ key, uint64_t* __restrict__ cdf0, uint64_t* __restrict__ cdf1,
+    uint64_t shard_cap, uint32_t tiles_per_shard, uint32_t n_shards_local, uint64_t* par_dev,
+    ShardTotals* totals, uint32_t* __restrict__ dirty, uint64_t* __restrict__ ttot0,
+    uint64_t* __restrict__ ttot1, uint32_t* buf_mode, uint32_t* shard_ctr, uint32_t* done) {
+  static_assert(kTile == (int)kCdfTile, "tile of the dirty map");
+  extern __shared__ __align__(128) uint64_t s_buf[];  // kScanBufs * kTile
+  __shared__ __align__(8) uint64_t s_bar[kScanBufs];
+  __shared__ uint32_t s_work[kThreads];   // work tiles of the current chunk
+  __shared__ uint32_t s_wdirty[kThreads]; // their dirty words
+  __shared__ uint32_t s_nwork;
+  __shared__ uint32_t s_wcnt[kThreads / 32];
+  __shared__ uint32_t s_shcnt[kMaxShards];  // tiles of each shard this CTA covers
+  __shared__ uint64_t s_red[kThreads / 32];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t par_old = __ldcg(par_dev);
+  const uint32_t mode0 = __ldcg(buf_mode), mode1 = __ldcg(buf_mode + 1);
+  const uint32_t parity = (uint32_t)(par_old & 1) ^ 1u;
+  uint64_t* __restrict__ cdf = parity ? cdf1 : cdf0;
+  uint64_t* __restrict__ ttot = parity ? ttot1 : ttot0;
+  const uint32_t mode = kIndicator ? 2u : 1u;
+  const bool full = (parity ? mode1 : mode0) != mode;
+  const uint32_t bit = 1u << parity;
+  const uint32_t n_tiles = tiles_per_shard * n_shards_local;
+  const uint32_t G = gridDim.x;
+  if (tid < kMaxShards) s_shcnt[tid] = 0;
+  if (tid == 0)
+    for (int b = 0; b < kScanBufs; ++b) mbar_init(smem_u32(&s_bar[b]), 1);
+  if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+
+  auto geom = [&](uint32_t t, uint64_t* gbase, uint32_t* count) {
+    const uint32_t sh = t / tiles_per_shard, tt = t - sh * tiles_per_shard;
+    const uint64_t tb = (uint64_t)tt * kTile;
+    *gbase = (uint64_t)sh * shard_cap + tb;
+    *count = (uint32_t)min((uint64_t)kTile, shard_cap - tb);
+  };
+  // thread 0: start the bulk load of work tile j of the chunk into its buffer
+  auto issue = [&](uint32_t j) {
+    uint64_t gb;
+    uint32_t count;
+    geom(s_work[j], &gb, &count);
+    if (count == (uint32_t)kTile && (gb & 1) == 0)
+      bulk_g2s(smem_u32(s_buf + (size_t)(j % kScanBufs) * kTile), key + gb, kTile * 8,
+               smem_u32(&s_bar[j % kScanBufs]));
+  };
+
+  uint32_t phase = 0;
+  // this CTA's tile list, in chunks of kThreads entries
+  for (uint32_t c0 = 0; blockIdx.x + (uint64_t)c0 * G < n_tiles; c0 += kThreads) {
+    const uint64_t t64 = blockIdx.x + (uint64_t)(c0 + tid) * G;
+    const bool have = t64 < n_tiles;
+    const uint32_t t = (uint32_t)t64;
+    const uint32_t dw = have ? __ldcg(dirty + t) : 0u;
+    const bool work = have && (full || (dw & bit));
+    if (have) atomicAdd(&s_shcnt[t / tiles_per_shard], 1u);
+    // compact the work tiles in tile order
+    const unsigned m = __ballot_sync(kFull, work);
+    if (lane == 0) s_wcnt[warp] = __popc(m);
+    __syncthreads();
+    uint32_t before = 0, nwork = 0;
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) {
+      before += (w < warp) ? s_wcnt[w] : 0u;
+      nwork += s_wcnt[w];
+    }
+    if (work) {
+      const uint32_t pos = before + __popc(m & ((1u << lane) - 1u));
+      s_work[pos] = t;
+      s_wdirty[pos] = dw;
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (uint32_t j = 0; j < nwork && j < 2; ++j) issue(j);
+    for (uint32_t j = 0; j < nwork; ++j) {
+      const int b = (int)(j % kScanBufs);
+      const uint32_t wt = s_work[j];
+      uint64_t gbase;
+      uint32_t count;
+      geom(wt, &gbase, &count);
+      const bool tma = count == (uint32_t)kTile && (gbase & 1) == 0;
+      uint64_t* buf = s_buf + (size_t)b * kTile;
+      if (tma) {
+        while (!mbar_try_wait(smem_u32(&s_bar[b]), (phase >> b) & 1u)) {
+        }
+        phase ^= 1u << b;
+      } else {
+        for (int e = tid; e < kTile; e += kThreads)
+          buf[e] = (uint32_t)e < count ? key[gbase + e] : 0ull;
+        __syncthreads();
+      }
+      const int r = tid & 7;
+      ulonglong2* b2 = reinterpret_cast<ulonglong2*>(buf) + tid * (kItems / 2);
+      uint64_t lo[kItems / 2], hi[kItems / 2];
+#pragma unroll
+      for (int k = 0; k < kItems / 2; ++k) {
+        const ulonglong2 x = b2[(k + r) & 7];
+        lo[k] = kIndicator ? (x.x > 0 ? 1ull : 0ull) : x.x;
+        hi[k] = kIndicator ? (x.y > 0 ? 1ull : 0ull) : x.y;
+      }
+      uint64_t run = 0;
+#pragma unroll
+      for (int k = 0; k < kItems / 2; ++k) {
+        lo[k] += run;
+        hi[k] += lo[k];
+        run = hi[k];
+      }
+      const uint64_t total = run;
+      uint64_t s_rot = 0;
+#pragma unroll
+      for (int k = 0; k < kItems / 2; ++k) s_rot = (k == 7 - r) ? hi[k] : s_rot;
+      const uint64_t incl = warp_incl_scan_u64(total, lane);
+      if (lane == 31) s_red[warp] = incl;
+      __syncthreads();
+      uint64_t warp_excl = 0, agg = 0;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) {
+        const uint64_t x = s_red[w];
+        warp_excl += (w < warp) ? x : 0ull;
+        agg += x;
+      }
+      const uint64_t base = warp_excl + incl - total;
+#pragma unroll
+      for (int k = 0; k < kItems / 2; ++k) {
+        const uint64_t off = base - s_rot + (k < 8 - r ? total : 0ull);
+        b2[(k + r) & 7] = make_ulonglong2(lo[k] + off, hi[k] + off);
+      }
+      __syncthreads();  // the tile's prefixes are in shared memory; s_red read
+      if (tma) {
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(buf);
+        ulonglong2* dst = reinterpret_cast<ulonglong2*>(cdf + gbase);
+#pragma unroll
+        for (int k = 0; k < kItems / 2; ++k) dst[k * kThreads + tid] = src[k * kThreads + tid];
+      } else {
+        for (int e = tid; e < (int)count; e += kThreads) cdf[gbase + e] = buf[e];
+      }
+      if (tid == 0) {
+        ttot[wt] = agg;
+        dirty[wt] = s_wdirty[j] & ~bit;
+      }
+      __syncthreads();  // buffer read by every thread: free for tile j + 3
+      if (tid == 0 && j + 2 < nwork) issue(j + 2);
+    }
+  }
+
+  // Arrivals: this CTA's tiles of every shard in one atomic; the CTA that
+  // completes a shard builds its prefix of tile totals P.
+  __syncthreads();
+  if (tid == 0) __threadfence();  // this CTA's cdf / ttot / dirty writes before its arrivals
+  for (uint32_t ls = 0; ls < n_shards_local; ++ls) {
+    const uint32_t mine = s_shcnt[ls];
+    if (mine == 0) continue;  // block-uniform
+    if (tid == 0) s_last = atomicAdd(shard_ctr + ls, mine) + mine == tiles_per_shard;
+    __syncthreads();
+    const bool last = s_last;
+    __syncthreads();  // s_last read by every thread before the next shard's write
+    if (!last) continue;
+    __threadfence();
+    uint64_t* P = cdf + (uint64_t)n_shards_local * shard_cap + (uint64_t)ls * tiles_per_shard;
+    const uint64_t* tot = ttot + (uint64_t)ls * tiles_per_shard;
+    uint64_t carry = 0;
+    for (uint32_t c0 = 0; c0 < tiles_per_shard; c0 += 4 * kThreads) {
+      uint64_t x[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t c = c0 + 4 * tid + k;
+        x[k] = c < tiles_per_shard ? __ldcg(tot + c) : 0ull;
+      }
+      x[1] += x[0];
+      x[2] += x[1];
+      x[3] += x[2];
+      const uint64_t incl = warp_incl_scan_u64(x[3], lane);
+      __syncthreads();  // s_red of the previous use consumed
+      if (lane == 31) s_red[warp] = incl;
+      __syncthreads();
+      uint64_t warp_excl = 0, agg = 0;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) {
+        const uint64_t y = s_red[w];
+        warp_excl += (w < warp) ? y : 0ull;
+        agg += y;
+      }
+      const uint64_t base = carry + warp_excl + incl - x[3];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t c = c0 + 4 * tid + k;
+        if (c < tiles_per_shard) P[c] = base + x[k];
+      }
+      carry += agg;
+    }
+    if (tid == 0) {
+      ShardTotals rec;
+      rec.total_and_parity = carry | ((uint64_t)parity << 63);
+      rec.aux = 0;
+      totals[ls] = rec;
+      shard_ctr[ls] = 0;
+      __threadfence();
+      if (atomicAdd(done, 1u) == n_shards_local - 1) {  // every shard is built
+        *done = 0;
+        buf_mode[parity] = mode;
+        *par_dev = parity;  // every CTA read the old parity before arriving
+      }
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_scan2(const uint64_t* key, uint64_t* cdf0, uint64_t* cdf1, uint64_t shard_cap,
@@ -531,6 +753,41 @@ cudaError_t launch_scan2(const uint64_t* key, uint64_t* cdf0, uint64_t* cdf1, ui
                          cudaStream_t s) {
   const uint32_t tps = scan_tiles_per_shard(shard_cap);
   const uint32_t n_tiles = tps * n_shards_local;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static const bool persistent = [] {
+    const char* e = getenv("GEAR_SCAN2_PERSISTENT");
+    return e == nullptr || e[0] != '0';
+  }();
+  // persistent rebuild once the table has more tiles than the resident CTAs
+  // (small tables: one CTA per tile launches no idle CTAs and needs no list)
+  if (persistent && n_tiles > (uint32_t)sms * kScanCtasPerSm) {
+    const size_t smem = (size_t)kScanBufs * kTile * 8;
+    static bool configured = false;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(scan2p_kernel<true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(scan2p_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    const uint32_t grid = (uint32_t)sms * kScanCtasPerSm;
+    count_launch();
+    if (indicator)
+      scan2p_kernel<true><<<grid, kThreads, smem, s>>>(key, cdf0, cdf1, shard_cap, tps,
+                                                       n_shards_local, par_dev, totals_out, dirty,
+                                                       ttot, ttot + n_tiles, buf_mode, shard_ctr,
+                                                       done);
+    else
+      scan2p_kernel<false><<<grid, kThreads, smem, s>>>(key, cdf0, cdf1, shard_cap, tps,
+                                                        n_shards_local, par_dev, totals_out, dirty,
+                                                        ttot, ttot + n_tiles, buf_mode, shard_ctr,
+                                                        done);
+    return cudaGetLastError();
+  }
   count_launch();
   if (indicator)
     scan2_kernel<true><<<n_tiles, kThreads, 0, s>>>(key, cdf0, cdf1, shard_cap, tps,
