@@ -27,7 +27,9 @@
  *    (one stream).  Collect outputs must be device memory (or mapped pinned).
  *  - Streams: sample and update of a table must be issued in one order (they
  *    share the keys and, at W > 1, the exchange epochs); collects and writers
- *    may run on other streams ordered by events, as bench.py does.
+ *    may run on other streams ordered by events, as bench.py does.  At most
+ *    64 collects of one table may be in flight at once (each launch takes one
+ *    of 64 rotating task counters).
  *  - The caller owns every argument buffer and must keep it alive until the
  *    stream has reached the call.  The table owns its columns, keys, CDFs and
  *    scratch.

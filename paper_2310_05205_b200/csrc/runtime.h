@@ -200,7 +200,7 @@ struct gear_table {
   int evict_first = -1;             // collect copies L2 evict-first: -1 auto (W > 1 after TopK), 0, 1
   bool last_topk = false;           // the most recent gear_sample was TopK
   int collect_dynamic = -1;         // TMA tasks from a counter: -1 auto (W > 1 or host rows), 0, 1
-  static constexpr uint32_t kDynSlots = 8;
+  static constexpr uint32_t kDynSlots = 64;  // collects of one table in flight at once (gear.h)
   unsigned long long* dyn_pool = nullptr;  // [kDynSlots][2] task counters (rotating)
   uint64_t dyn_slot = 0;
   int collect_peer_lsu = 0;         // W > 1: peer-HBM rows of TMA columns via LSU warps
