@@ -287,6 +287,7 @@ def run_gpu(args):
     if world > 1:
         gear.gear_table_set_tuning(t.handle, "collect_peer_lsu", head_peer_lsu)
     B = cfg.batch
+    NB = args.depth   # id buffers: the selection may run NB - 1 steps ahead of the collect
     ncols = len(t.row_bytes)
     col_ids = list(range(ncols))
     row_total = sum(t.row_bytes)
@@ -315,9 +316,9 @@ def run_gpu(args):
     with torch.cuda.stream(stream):
         outs2 = [outs] + [[torch.empty_like(o) for o in outs] for _ in range(len(cstreams) - 1)]
     with torch.cuda.stream(stream):
-        idx2 = [idx, torch.empty(B, dtype=torch.int64, device="cuda")]
-    ev_sampled = [torch.cuda.Event() for _ in range(2)]
-    ev_collected = [torch.cuda.Event() for _ in range(2)]
+        idx2 = [idx] + [torch.empty(B, dtype=torch.int64, device="cuda") for _ in range(NB - 1)]
+    ev_sampled = [torch.cuda.Event() for _ in range(NB)]
+    ev_collected = [torch.cuda.Event() for _ in range(NB)]
 
     def step_serial(i, ev):
         """sample -> collect -> update, all on one stream."""
@@ -336,8 +337,8 @@ def run_gpu(args):
         keys) stays in order on `stream`, collection runs on `cstream`, so
         collect(i) overlaps update(i) and sample(i+1).  idx is double
         buffered: sample(i+2) waits until collect(i) has read idx[i%2]."""
-        b = i % 2
-        if i >= 2:
+        b = i % NB
+        if i >= NB:
             stream.wait_event(ev_collected[b])
         gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + i, cfg.beta, idx2[b], w,
                          None, None, stream, flags=sflags)
@@ -422,8 +423,8 @@ def run_gpu(args):
                 raise RuntimeError("cudaEventRecordWithFlags(External) failed")
 
         def gstep(i, timing=False):
-            b = i % 2
-            if i >= 2:
+            b = i % NB
+            if i >= NB:
                 stream.wait_event(ev_collected[b])
             gear.gear_sample(t.handle, strategy, B, 0, cfg.beta, idx2[b], w, None, None, stream,
                              flags=sflags | gear.GEAR_SAMPLE_DEVICE_SEED)
@@ -565,16 +566,16 @@ def run_gpu(args):
     h_w2 = [h_w] + [torch.empty(B, dtype=torch.float32, pin_memory=True) for _ in range(NH - 1)]
     ev_hs = [torch.cuda.Event() for _ in range(NH)]
     xstream = torch.cuda.Stream()   # the ids' D2H copy: off the selection / collect streams
-    ev_copied = [torch.cuda.Event() for _ in range(2)]
+    ev_copied = [torch.cuda.Event() for _ in range(NB)]
     np_idx2 = [x.numpy() for x in h_idx2]   # host views of the pinned buffers
     np_w2 = [x.numpy() for x in h_w2]
-    dw2 = [torch.empty(B, dtype=torch.float32, device="cuda") for _ in range(2)]
+    dw2 = [torch.empty(B, dtype=torch.float32, device="cuda") for _ in range(NB)]
     consumed = 0.0
 
     def step_e2e(i):
-        b, hb = i % 2, i % NH
-        if i >= 2:
-            stream.wait_event(ev_collected[b])   # collect(i-2) has read idx2[b]
+        b, hb = i % NB, i % NH
+        if i >= NB:
+            stream.wait_event(ev_collected[b])   # collect(i-NB) has read idx2[b]
             stream.wait_event(ev_copied[b])      # and so has its host copy
         gear.gear_sample(t.handle, strategy, B, synth.SAMPLE_SEED_BASE + 7919 + i, cfg.beta,
                          idx2[b], h_w2[hb] if args.e2e_weights == "host" else dw2[b], None, None,
@@ -634,7 +635,7 @@ def run_gpu(args):
     # NVLink, or host memory over this GPU's PCIe) and written once to local
     # HBM.  The remote fraction is measured on the step's sampled ids.
     Cl = capacity // world
-    own = (idx2[(args.steps - 1) % 2].cpu().numpy().astype(np.uint64) // np.uint64(Cl))
+    own = (idx2[(args.steps - 1) % NB].cpu().numpy().astype(np.uint64) // np.uint64(Cl))
     f_remote = torch.tensor([float(np.mean(own != rank))], device="cuda")
     if world > 1:
         dist.all_reduce(f_remote, op=dist.ReduceOp.MAX)
@@ -839,6 +840,8 @@ def main():
                     help="override the config's strategy")
     ap.add_argument("--collect-streams", type=int, default=1, choices=[1, 2],
                     help="2: consecutive collects on alternating streams may overlap")
+    ap.add_argument("--depth", type=int, default=2,
+                    help="pipeline depth: id buffers, the selection runs up to depth-1 steps ahead")
     ap.add_argument("--e2e-weights", default="host", choices=["host", "device"],
                     help="e2e: the sample kernel writes the IS weights to pinned host memory in "
                          "place (host) or to HBM, copied with the ids (device)")
