@@ -196,7 +196,8 @@ uint64_t gear_kernel_launches(void);
 gear_status gear_get_unique_id(uint8_t out[128]);
 
 /* Collective over all nranks.  `device` is this rank's CUDA device; it is
- * made current.  Peer access is enabled to every other rank's device. */
+ * made current.  (Peer memory is mapped per table, through CUDA IPC, by
+ * gear_table_create.) */
 gear_status gear_comm_create(int nranks, int rank, const uint8_t id[128], int device,
                              gear_comm** out);
 
@@ -233,7 +234,8 @@ gear_status gear_comm_destroy(gear_comm* comm);
  * (u64 fixed point), seq (u64), gen (u32), two CDF buffers and scratch, and
  * exchanges peer pointers (CUDA IPC) so kernels can read peer shards over
  * NVLink.  Errors: INVALID_ARG (N not divisible by S, duplicate or empty
- * names, zero-size rows, S > 32, ncols > 16), OUT_OF_MEMORY, CUDA, NCCL. */
+ * names, zero-size rows, S > 32, ncols > 16, W * max_batch >= 2^24),
+ * OUT_OF_MEMORY, CUDA, NCCL. */
 gear_status gear_table_create(const gear_table_desc* desc, gear_comm* comm, gear_table** out);
 
 /* Collective when the table has a comm.  Frees everything. */
