@@ -545,7 +545,6 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan2p_kernel(
   extern __shared__ __align__(128) uint64_t s_buf[];  // kScanBufs * kTile
   __shared__ __align__(8) uint64_t s_bar[kScanBufs];
   __shared__ uint32_t s_work[kThreads];   // work tiles of the current chunk
-  __shared__ uint32_t s_wdirty[kThreads]; // their dirty words
   __shared__ uint32_t s_nwork;
   __shared__ uint32_t s_wcnt[kThreads / 32];
   __shared__ uint32_t s_shcnt[kMaxShards];  // tiles of each shard this CTA covers
@@ -590,7 +589,8 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan2p_kernel(
     const uint64_t t64 = blockIdx.x + (uint64_t)(c0 + tid) * G;
     const bool have = t64 < n_tiles;
     const uint32_t t = (uint32_t)t64;
-    const uint32_t dw = have ? __ldcg(dirty + t) : 0u;
+    // a full rebuild takes every tile: no dirty word on the critical path
+    const uint32_t dw = (have && !full) ? __ldcg(dirty + t) : 0u;
     const bool work = have && (full || (dw & bit));
     if (have) atomicAdd(&s_shcnt[t / tiles_per_shard], 1u);
     // compact the work tiles in tile order
@@ -606,7 +606,6 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan2p_kernel(
     if (work) {
       const uint32_t pos = before + __popc(m & ((1u << lane) - 1u));
       s_work[pos] = t;
-      s_wdirty[pos] = dw;
     }
     __syncthreads();
     if (tid == 0)
@@ -675,7 +674,7 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan2p_kernel(
       }
       if (tid == 0) {
         ttot[wt] = agg;
-        dirty[wt] = s_wdirty[j] & ~bit;
+        atomicAnd(dirty + wt, ~bit);  // this buffer's bit; the other buffer's stays
       }
       __syncthreads();  // buffer read by every thread: free for tile j + 3
       if (tid == 0 && j + 2 < nwork) issue(j + 2);
