@@ -535,15 +535,24 @@ __global__ void __launch_bounds__(kThreads) scan2_kernel(
 // the CTA that completes a shard builds that shard's prefix of tile totals,
 // and the last shard flips the parity and records the buffer's mode, as in
 // scan2_kernel.
+#ifndef GEAR_S2_CTAS
+#define GEAR_S2_CTAS 2
+#endif
+#ifndef GEAR_S2_BUFS
+#define GEAR_S2_BUFS 3
+#endif
+constexpr int kS2Ctas = GEAR_S2_CTAS;  // scan2p CTAs per SM
+constexpr int kS2Bufs = GEAR_S2_BUFS;  // scan2p tile buffers per CTA (loads kS2Bufs - 1 ahead)
+
 template <bool kIndicator>
-__global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan2p_kernel(
+__global__ void __launch_bounds__(kThreads, kS2Ctas) scan2p_kernel(
     const uint64_t* __restrict__ key, uint64_t* __restrict__ cdf0, uint64_t* __restrict__ cdf1,
     uint64_t shard_cap, uint32_t tiles_per_shard, uint32_t n_shards_local, uint64_t* par_dev,
     ShardTotals* totals, uint32_t* __restrict__ dirty, uint64_t* __restrict__ ttot0,
     uint64_t* __restrict__ ttot1, uint32_t* buf_mode, uint32_t* shard_ctr, uint32_t* done) {
   static_assert(kTile == (int)kCdfTile, "tile of the dirty map");
-  extern __shared__ __align__(128) uint64_t s_buf[];  // kScanBufs * kTile
-  __shared__ __align__(8) uint64_t s_bar[kScanBufs];
+  extern __shared__ __align__(128) uint64_t s_buf[];  // kS2Bufs * kTile
+  __shared__ __align__(8) uint64_t s_bar[kS2Bufs];
   __shared__ uint32_t s_work[kThreads];   // work tiles of the current chunk
   __shared__ uint32_t s_nwork;
   __shared__ uint32_t s_wcnt[kThreads / 32];
@@ -563,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan2p_kernel(
   const uint32_t G = gridDim.x;
   if (tid < kMaxShards) s_shcnt[tid] = 0;
   if (tid == 0)
-    for (int b = 0; b < kScanBufs; ++b) mbar_init(smem_u32(&s_bar[b]), 1);
+    for (int b = 0; b < kS2Bufs; ++b) mbar_init(smem_u32(&s_bar[b]), 1);
   if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
 
@@ -579,8 +588,8 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan2p_kernel(
     uint32_t count;
     geom(s_work[j], &gb, &count);
     if (count == (uint32_t)kTile && (gb & 1) == 0)
-      bulk_g2s(smem_u32(s_buf + (size_t)(j % kScanBufs) * kTile), key + gb, kTile * 8,
-               smem_u32(&s_bar[j % kScanBufs]));
+      bulk_g2s(smem_u32(s_buf + (size_t)(j % kS2Bufs) * kTile), key + gb, kTile * 8,
+               smem_u32(&s_bar[j % kS2Bufs]));
   };
 
   uint32_t phase = 0;
@@ -609,9 +618,9 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan2p_kernel(
     }
     __syncthreads();
     if (tid == 0)
-      for (uint32_t j = 0; j < nwork && j < 2; ++j) issue(j);
+      for (uint32_t j = 0; j < nwork && j < (uint32_t)kS2Bufs - 1; ++j) issue(j);
     for (uint32_t j = 0; j < nwork; ++j) {
-      const int b = (int)(j % kScanBufs);
+      const int b = (int)(j % kS2Bufs);
       const uint32_t wt = s_work[j];
       uint64_t gbase;
       uint32_t count;
@@ -676,8 +685,8 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan2p_kernel(
         ttot[wt] = agg;
         atomicAnd(dirty + wt, ~bit);  // this buffer's bit; the other buffer's stays
       }
-      __syncthreads();  // buffer read by every thread: free for tile j + 3
-      if (tid == 0 && j + 2 < nwork) issue(j + 2);
+      __syncthreads();  // buffer read by every thread: free for tile j + kS2Bufs
+      if (tid == 0 && j + kS2Bufs - 1 < nwork) issue(j + kS2Bufs - 1);
     }
   }
 
@@ -761,8 +770,8 @@ cudaError_t launch_scan2(const uint64_t* key, uint64_t* cdf0, uint64_t* cdf1, ui
   }();
   // persistent rebuild once the table has more tiles than the resident CTAs
   // (small tables: one CTA per tile launches no idle CTAs and needs no list)
-  if (persistent && n_tiles > (uint32_t)sms * kScanCtasPerSm) {
-    const size_t smem = (size_t)kScanBufs * kTile * 8;
+  if (persistent && n_tiles > (uint32_t)sms * kS2Ctas) {
+    const size_t smem = (size_t)kS2Bufs * kTile * 8;
     static bool configured = false;
     if (!configured) {
       cudaError_t e = cudaFuncSetAttribute(scan2p_kernel<true>,
@@ -773,7 +782,7 @@ cudaError_t launch_scan2(const uint64_t* key, uint64_t* cdf0, uint64_t* cdf1, ui
       if (e != cudaSuccess) return e;
       configured = true;
     }
-    const uint32_t grid = (uint32_t)sms * kScanCtasPerSm;
+    const uint32_t grid = (uint32_t)sms * kS2Ctas;
     count_launch();
     if (indicator)
       scan2p_kernel<true><<<grid, kThreads, smem, s>>>(key, cdf0, cdf1, shard_cap, tps,
