@@ -339,6 +339,38 @@ def run_fuzz_case(comm, W, rank, R=2, Cs=400, steps=150, seed=11):
     t.close()
 
 
+def run_host_comm_capture_case(comm, W, rank):
+    """With a host-bootstrapped comm the peer_xchg = 0 exchanges go through the
+    host all-gather: refused (UNSUPPORTED) inside CUDA-graph capture, on every
+    rank alike, and the table still works afterwards."""
+    cols = [gear.Column("a", gear.GEAR_U8, (4,))]
+    t = gear.Table(W * 64, 1, cols, comm, max_batch=64)
+    t.insert(rank, [torch.zeros((64, 4), dtype=torch.uint8, device="cuda")], np.ones(64))
+    torch.cuda.synchronize()
+    dist.barrier()
+    gear.gear_table_set_tuning(t.handle, "peer_xchg", 0)
+    idx = torch.empty(16, dtype=torch.int64, device="cuda")
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    refused = False
+    try:
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+                gear.gear_sample(t.handle, gear.GEAR_UNIFORM, 16, 3, 0.0, idx)
+    except gear.GearError as e:
+        refused = e.status == gear.GEAR_ERR_UNSUPPORTED
+    except RuntimeError:      # the capture itself was invalidated after the refusal
+        refused = True
+    assert refused, "an all-gather through the host callback was captured"
+    torch.cuda.synchronize()
+    dist.barrier()
+    gear.gear_sample(t.handle, gear.GEAR_UNIFORM, 16, 3, 0.0, idx)   # eager: fine
+    torch.cuda.synchronize()
+    assert np.all(idx.cpu().numpy() < W * 64)
+    dist.barrier()
+    t.close()
+
+
 def run_timeout_case(comm, W, rank, R=1, Cs=256, B=32):
     """A broken SPMD sequence: only rank 0 calls gear_sample and then
     gear_update_priorities.  Its mailbox waits time out after ~4 s; the
@@ -409,6 +441,11 @@ def main():
         dist.barrier()
         if rank == 0:
             print("case random collective sequences: ok", flush=True)
+        if shared:
+            run_host_comm_capture_case(comm, W, rank)
+            dist.barrier()
+            if rank == 0:
+                print("case host comm: all-gather refused inside graph capture: ok", flush=True)
         run_timeout_case(comm, W, rank)
         dist.barrier()
         if rank == 0:

@@ -53,6 +53,10 @@ def test_invalid_arguments(torch_cuda):
     _raises(INV, G.gear_allocate, h, 0, 65, torch.zeros(65, dtype=torch.int64, device="cuda"))
     _raises(INV, G.gear_commit, h, 3, 4, idx, np.ones(4))
     _raises(INV, G.gear_column_id, h, "nope")
+    _raises(G.GEAR_ERR_STATE, G.gear_read_cdf, h)                    # no CDF built yet
+    _raises(INV, G.gear_sample, h, G.GEAR_UNIFORM, 8, 1, 0.4, idx, flags=0x4)   # unknown flag
+    _raises(INV, G.gear_table_set_tuning, h, "collect_dynamic", 2)
+    _raises(INV, G.gear_table_set_tuning, h, "collect_evict_first", -2)
     # the table still works after the rejected calls
     t.sample(G.GEAR_UNIFORM, 8, 1, 0.0, idx)
     t.collect(idx, [0], out)
