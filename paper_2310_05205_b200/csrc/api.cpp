@@ -985,6 +985,17 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
       t->cdf_mode = mode;
       t->dirty = false;
     }
+    // If a later step of this call fails (e.g. a host all-gather refused
+    // inside stream capture), the rebuild enqueued above may never run: keep
+    // the host's "CDF is current" flag honest (flat layout) by marking it
+    // dirty again on every error return below.
+    struct DirtyOnError {
+      gear_table* t;
+      bool ok = false;
+      ~DirtyOnError() {
+        if (!ok) t->dirty = true;
+      }
+    } dirty_guard{t};
     // Every step publishes the totals; the exchange is also the barrier that
     // makes every shard's CDF visible before anyone searches it.  W > 1: the
     // first kernel of the step (assign or sample) pushes this rank's totals
@@ -1040,6 +1051,7 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
       sp.draw_list = t->draw_list;
     }
     GEAR_CUDA(launch_sample(sp, s));
+    dirty_guard.ok = true;
   }
   if (h_idx) GEAR_CUDA(cudaMemcpyAsync(out_idx, d_idx, B * 8ull, cudaMemcpyDeviceToHost, s));
   if (h_w) GEAR_CUDA(cudaMemcpyAsync(out_w, d_w, B * 4ull, cudaMemcpyDeviceToHost, s));
