@@ -13,6 +13,15 @@ per rank with per-step priority updates).  N>1 (torchrun, one rank per GPU):
 the same 100K-trajectory table sharded by id over N GPUs, B=512 per rank
 (weak scaling), remote rows read over NVLink by the collect kernel.
 
+Defaults: K = 1000 timed steps, W = 10 warm-up steps.  The headline is the
+pipelined step (selection on one stream, collection on another) with the K
+steps captured as ONE CUDA graph and replayed once inside the timed region;
+the eager pipelined, serial and end-to-end (host buffers) variants, the
+roofline of the collect kernel (its launch time taken from the timed replay),
+live PCIe / NVLink probes, clocks and the selection-only time are in the same
+line; at N > 1 also the other assignment of the global batch (DESIGN.md
+Q9 / Q19).  --impl reference times the CPU oracle on the same workload.
+
 Prints ONE JSON line (rank 0).  Time is measured with CUDA events on the
 launching stream, barrier + synchronize on both sides, max over ranks.
 """
