@@ -437,10 +437,14 @@ def main():
     if rank == 0:
         print("case graph replay (owner-affine, device seed): ok", flush=True)
     if not quick:
-        run_fuzz_case(comm, W, rank)
-        dist.barrier()
-        if rank == 0:
-            print("case random collective sequences: ok", flush=True)
+        # GEAR_FUZZ_STEPS / GEAR_FUZZ_SEEDS: longer soak runs of the same case
+        fuzz_steps = int(os.environ.get("GEAR_FUZZ_STEPS", "150"))
+        for fseed in [int(x) for x in os.environ.get("GEAR_FUZZ_SEEDS", "11").split(",")]:
+            run_fuzz_case(comm, W, rank, steps=fuzz_steps, seed=fseed)
+            dist.barrier()
+            if rank == 0:
+                print(f"case random collective sequences (seed {fseed}, {fuzz_steps} steps): ok",
+                      flush=True)
         if shared:
             run_host_comm_capture_case(comm, W, rank)
             dist.barrier()
