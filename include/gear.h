@@ -326,7 +326,8 @@ gear_status gear_column_base(const gear_table* t, uint32_t col, void** out);
  * last writer wins.  idx / prio / gen may be device memory, pinned host
  * memory (read in place by the kernel over PCIe) or pageable host memory
  * (copied).  Device-side errors (id >= N, bad p, stale) skip the entry and
- * are latched.  n <= max_batch. */
+ * are latched.  n <= max_batch; n == 0 is valid and applies nothing (still
+ * collective at W > 1). */
 gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* idx,
                                    const void* prio, gear_dtype prio_dtype, const uint32_t* gen,
                                    gear_stream stream);
@@ -351,7 +352,9 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
  *  smaller global id, in that order (reading Q20; W*B <= 8192).
  *  flags: 0 or GEAR_SAMPLE_OWNER_AFFINE | GEAR_SAMPLE_DEVICE_SEED (other
  *  bits: INVALID_ARG); same value on every rank.
- *  Nothing selectable: outputs get GEAR_IDX_NONE and EMPTY is latched. */
+ *  Nothing selectable: outputs get GEAR_IDX_NONE and EMPTY is latched.
+ *  B == 0 (on every rank): returns OK with no work (outputs, keys and the
+ *  device seed counter untouched). */
 gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint64_t seed,
                         double beta, uint64_t* out_idx, float* out_w, double* out_p,
                         uint32_t* out_gen, uint32_t flags, gear_stream stream);
@@ -361,7 +364,8 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
  * n * row_bytes(col_ids[c]) bytes.  DEVICE columns are read from local HBM
  * or a peer's HBM over NVLink; HOST columns are read zero-copy over PCIe.
  * Not collective (peers' memory is read directly).  idx: device or host.
- * An id >= N leaves its output row untouched and latches INDEX_RANGE. */
+ * An id >= N leaves its output row untouched and latches INDEX_RANGE.
+ * n == 0 or ncols == 0: OK, no work. */
 gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_t ncols,
                          const uint32_t* col_ids, void* const* out, gear_stream stream);
 

@@ -906,7 +906,6 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
   if (B == 0) return GEAR_OK;
   if (out_idx == nullptr) return set_error(GEAR_ERR_INVALID_ARG, "out_idx is NULL");
   if (!std::isfinite(beta)) return set_error(GEAR_ERR_INVALID_ARG, "beta is not finite");
-  // Outputs: device pointers are written in place, host ones via scratch.
   // Outputs: device and pinned host buffers are written in place by the
   // kernels (pinned ones through their mapped address, over PCIe); pageable
   // host buffers through device scratch and a copy at the end.

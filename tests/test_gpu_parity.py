@@ -515,3 +515,61 @@ def test_host_rows_straddling_registration_pieces(torch_cuda, monkeypatch):
     P.check_collect(np.random.default_rng(3).permutation(N).astype(np.uint64))
     P.check_collect(P.check_sample(G.GEAR_WEIGHTED, 1024, 77))
     P.close()
+
+
+def test_zero_size_calls_are_noops(torch_cuda):
+    """B = 0 / n = 0 (include/gear.h): sample, collect and update return OK
+    without touching their outputs or the table, and without advancing the
+    device seed counter -- the next draw still equals the oracle's."""
+    import oracle
+    torch = torch_cuda
+    cols = [synth.ColSpec("x", "f32", (2,))]
+    P = _pair(capacity=4096, seq_len=1, colspecs=cols, R=2)
+    P.fill(synth.priorities(4096, seed=3, zero_frac=0.05))
+    h = P.t.handle
+    idx = torch.full((8,), 7, dtype=torch.int64, device="cuda")
+    w = torch.full((8,), 3.0, dtype=torch.float32, device="cuda")
+    out = torch.full((8, P.rb[0]), 0xAB, dtype=torch.uint8, device="cuda")
+    G.gear_table_set_tuning(h, "device_seed", 0x5EED)
+    for strat in (G.GEAR_UNIFORM, G.GEAR_PRIORITIZED, G.GEAR_FIFO, G.GEAR_TOPK):
+        G.gear_sample(h, strat, 0, 0, 0.4, idx, w, flags=G.GEAR_SAMPLE_DEVICE_SEED)
+    G.gear_collect(h, 0, idx, [0], [out])
+    G.gear_update_priorities(h, 0, idx, torch.zeros(8, dtype=torch.float64, device="cuda"),
+                             G.GEAR_F64)
+    torch.cuda.synchronize()
+    assert torch.all(idx == 7) and torch.all(w == 3.0) and torch.all(out == 0xAB)
+    err, stale = P.t.sync()
+    assert err == 0 and stale == 0
+    P.check_state()
+    # the seed counter did not move: the first real draw uses seed 0x5EED
+    G.gear_sample(h, G.GEAR_PRIORITIZED, 8, 0, 0.4, idx, w, flags=G.GEAR_SAMPLE_DEVICE_SEED)
+    torch.cuda.synchronize()
+    st, oi, ow, _ = P.o.sample(oracle.PRIORITIZED, 1, 0, 8, 0x5EED, 0.4)
+    assert st == 0
+    assert np.array_equal(idx.cpu().numpy().view(np.uint64), oi)
+    np.testing.assert_allclose(w.cpu().numpy(), ow, rtol=1e-6, atol=0)
+    P.close()
+
+
+@pytest.mark.parametrize("R", [1, 3])
+def test_max_batch_one_million(torch_cuda, R):
+    """A batch at the top of the size range (B = 2^20, W * max_batch < 2^24):
+    ids, IS weights, q/T and every collected row of a 2^20-row prioritized
+    and uniform draw, then a 2^20-entry update with duplicates, then FIFO and
+    LIFO at 2^20 (more candidates than one merge tile)."""
+    cols = [synth.ColSpec("x", "u8", (12,))]
+    B = 1 << 20
+    N = R * 700_001
+    P = _pair(capacity=N, seq_len=1, colspecs=cols, R=R, max_batch=B)
+    P.fill(synth.priorities(N, seed=9, zero_frac=0.1))
+    for strat, seed in ((G.GEAR_PRIORITIZED, 77), (G.GEAR_UNIFORM, 78)):
+        idx = P.check_sample(strat, B, seed)
+        P.check_collect(idx)
+    rng = np.random.default_rng(5)
+    ost, _, err, _ = P.update(idx, rng.lognormal(0, 1, B))
+    assert ost == 0 and err == 0
+    P.check_state()
+    P.check_sample(G.GEAR_PRIORITIZED, B, 79)
+    for strat in (G.GEAR_FIFO, G.GEAR_LIFO):
+        P.check_sample(strat, B // 2, 80)
+    P.close()
