@@ -428,7 +428,16 @@ gear_status gear_table_load(gear_table* t, const char* path);
  *                   decoupled look-back scan, only when the
  *                   host saw a writer call since the last build (so writers
  *                   replayed from a CUDA graph need cdf_levels 2).  The
- *                   sampled ids are identical (synchronises the device).
+ *                   sampled ids are identical (synchronises the device);
+ *   "scan_chunk":   cdf_levels 1 only: 1 = the look-back runs over one
+ *                   contiguous chunk of keys per resident CTA (two passes
+ *                   over the chunk, the second from shared memory / L2),
+ *                   0 = over 4096-key tiles (persistent, pipelined), -1 =
+ *                   auto (default): chunks when the rank's keys are at most
+ *                   GEAR_SCAN_CHUNK_MAX_MB (default 96) MB and span at least
+ *                   one tile per CTA; k >= 2 (tests): chunked on at most k
+ *                   CTAs, each claiming several chunks.  Identical CDF
+ *                   either way.
  * Initial values also come from the environment (GEAR_COLLECT_IMPL=lsu|tma,
  * GEAR_COLLECT_CHUNK, GEAR_TMA_CHUNK).  INVALID_ARG for an unknown key or
  * value. */

@@ -979,7 +979,7 @@ gear_status gear_sample(gear_table* t, gear_strategy strategy, uint32_t B, uint6
       else
         GEAR_CUDA(launch_scan(t->key, t->cdf[0], t->cdf[1], t->Cs, t->R, mode, t->d_xep + 3,
                               t->cdf_totals_local, t->scan_status[0], t->scan_status[1],
-                              t->scan_ticket[0], t->scan_ticket[1], s));
+                              t->scan_ticket[0], t->scan_ticket[1], t->scan_chunk, s));
       t->scan_launches += 1;
       t->cdf_mode = mode;
       t->dirty = false;
@@ -1236,6 +1236,8 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     GEAR_CUDA(cudaMemset(t->cdf_buf_mode, 0, 8));  // both buffers: full rebuild
     t->cdf_levels = (int)value;
     t->dirty = true;
+  } else if (!strcmp(key, "scan_chunk") && value >= -1 && value <= 4096) {
+    t->scan_chunk = (int)value;  // flat CDF kernel choice (same CDF either way)
   } else if (!strcmp(key, "collect_dynamic") && value >= -1 && value <= 1) {
     t->collect_dynamic = (int)value;
   } else if (!strcmp(key, "collect_evict_first") && value >= -1 && value <= 1) {

@@ -277,7 +277,7 @@ void count_launch(uint64_t n = 1);
 cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf0, uint64_t* cdf1, uint64_t shard_cap,
                         uint32_t n_shards_local, int indicator, uint64_t* par_dev,
                         ShardTotals* totals_out, uint64_t* status0, uint64_t* status1, uint32_t* ticket,
-                        uint32_t* done, cudaStream_t s);
+                        uint32_t* done, int chunked, cudaStream_t s);
 uint32_t scan_tiles_per_shard(uint64_t shard_cap);
 // Two-level incremental CDF (scan.cu, scan2_kernel): cdf0/cdf1 hold
 // R*C_s tile-local prefixes followed by R*tiles_per_shard tile prefixes;

@@ -36,6 +36,26 @@ constexpr uint64_t kValMask = (1ull << 62) - 1;
 
 __device__ __forceinline__ int pad(int e) { return e + (e >> 4); }
 
+// GEAR_SCAN_TL (A/B builds only): per-CTA timeline of the persistent scans,
+// %globaltimer (ns) at entry, at the phase boundaries and at exit, printed by
+// every 8th CTA.
+#ifdef GEAR_SCAN_TL
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_DECL uint64_t tl_[4] = {gtimer(), 0, 0, 0};
+#define TL_MARK(i) do { if (tl_[i] == 0) tl_[i] = gtimer(); } while (0)
+#define TL_PRINT(name) do { if (threadIdx.x == 0 && blockIdx.x % 8 == 0) { unsigned sm_; \
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_)); \
+    printf("TL %s cta %u sm %u %llu %llu %llu %llu\n", name, blockIdx.x, sm_, tl_[0], tl_[1], tl_[2], gtimer()); } } while (0)
+#else
+#define TL_DECL
+#define TL_MARK(i) do {} while (0)
+#define TL_PRINT(name) do {} while (0)
+#endif
+
 // Persistent, software-pipelined decoupled look-back scan.
 //
 // kScanCtasPerSm CTAs per SM stay resident and claim 4096-key tiles from an
@@ -98,6 +118,7 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
   __shared__ __align__(8) uint64_t s_free[kScanBufs];  // GEAR_SCAN_FREEBAR: buffer read by every warp
   __shared__ bool s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  TL_DECL
   // The CDF is rebuilt into the buffer peers are NOT reading: the parity of
   // the last build lives in device memory (graph-replayable) and is flipped
   // by the last CTA to exit; the parity travels with the shard totals.
@@ -370,6 +391,7 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
            blockIdx.x, iters, pr[0] / iters, pr[1] / iters, pr[2] / iters, pr[6] / iters, pr[7] / iters, pr[3] / iters,
            pr[4] / iters, pr[5] / iters, polls);
 #endif
+  TL_PRINT("tile");
   // The last CTA to exit re-arms the ticket and the exit counter and
   // publishes the new parity.
   if (tid == 0) {
@@ -384,6 +406,311 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
       *done = 0;
       *par_dev = parity;  // every CTA read the old parity before exiting
     }
+  }
+}
+
+// Chunked decoupled look-back (K1c; `cdf_levels = 1` for mid-sized tables).
+//
+// The look-back runs over CHUNKS -- contiguous key ranges, one per resident
+// CTA -- instead of 4096-key tiles, so it is resolved once per CTA instead of
+// once per tile:
+//   phase 1: stream the chunk's tiles (TMA, kCBufs ahead) and reduce each to
+//            its tile sum; the last kCBufs tiles stay in shared memory;
+//            publish the chunk aggregate (flag A; flag P for a shard's first
+//            chunk) -- the same 64-bit flag+value status word as scan_kernel;
+//   look-back: block-wide over up to 2 * kThreads predecessors per round trip
+//            (every chunk of a shard is in flight at once, so the first
+//            window normally reaches the shard's first chunk), publish P;
+//   phase 2: scan the chunk's tiles in REVERSE order -- the resident ones
+//            first, then the most recently streamed (still in L2 while the
+//            table's keys are a fraction of the 126 MB L2), each tile's
+//            prefix being the chunk prefix + the tile sums before it -- and
+//            write the CDF with streaming (evict-first) stores.
+// DRAM traffic stays 8 B read + 8 B written per key as long as the keys
+// re-read in phase 2 hit L2, and HBM sees a read phase and a write phase
+// instead of a per-tile mix; the per-tile look-back pipeline of scan_kernel
+// (and its fill / drain) is gone.  Chunk boundaries are key offsets rounded to
+// 16 keys, so every CTA gets the same work (+- 16 keys); a chunk's last tile
+// is ragged (masked).  Chunks are claimed from the ticket, so a chunk only
+// waits on chunks that already run (forward progress), and the kernel shares
+// scan_kernel's status arrays / epoch / ticket / exit counter protocol.
+#ifndef GEAR_CHUNK_BUFS
+#define GEAR_CHUNK_BUFS 3
+#endif
+#ifndef GEAR_CHUNK_L2
+#define GEAR_CHUNK_L2 0
+#endif
+#ifndef GEAR_CHUNK_CTAS
+#define GEAR_CHUNK_CTAS 2
+#endif
+#ifndef GEAR_CHUNKS_PER_CTA
+#define GEAR_CHUNKS_PER_CTA 1
+#endif
+constexpr int kCBufs = GEAR_CHUNK_BUFS;
+constexpr int kChunksPerCta = GEAR_CHUNKS_PER_CTA;  // chunks per CTA (a CTA's phase 1 overlaps others' phase 2)
+constexpr int kChunkCtasPerSm = GEAR_CHUNK_CTAS;
+constexpr int kMaxChunkTiles = 64;  // tile sums kept in shared memory
+
+__device__ __forceinline__ void st_stream_u64x2(uint64_t* p, uint64_t a, uint64_t b) {
+  asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+template <bool kIndicator>
+__global__ void __launch_bounds__(kThreads, kChunkCtasPerSm) scan_chunk_kernel(
+    const uint64_t* __restrict__ key, uint64_t* __restrict__ cdf0, uint64_t* __restrict__ cdf1,
+    uint64_t shard_cap, uint32_t chunks_per_shard, uint32_t n_chunks, uint32_t n_status_clear,
+    uint64_t* par_dev, ShardTotals* totals, uint64_t* status0, uint64_t* status1,
+    uint32_t* ticket, uint32_t* done) {
+  extern __shared__ __align__(128) uint64_t s_buf[];  // kCBufs * kTile
+  __shared__ __align__(8) uint64_t s_bar[kCBufs];
+  __shared__ uint64_t s_tsum[kMaxChunkTiles];  // phase 1: tile sums; phase 2: tile prefixes
+  __shared__ uint64_t s_red[2][kThreads / 32];
+  __shared__ uint32_t s_pmask[2][kThreads / 32];
+  __shared__ uint64_t s_excl;
+  __shared__ uint32_t s_chunk;
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  TL_DECL
+  const uint32_t parity = (uint32_t)(ld_relaxed_u64(par_dev) & 1) ^ 1u;
+  uint64_t* __restrict__ cdf = parity ? cdf1 : cdf0;
+  const uint32_t epoch = *(volatile uint32_t*)(ticket + 1);
+  uint64_t* __restrict__ status = (epoch & 1) ? status1 : status0;
+  {
+    uint64_t* other = (epoch & 1) ? status0 : status1;
+    for (uint32_t i = blockIdx.x * kThreads + tid; i < n_status_clear; i += gridDim.x * kThreads)
+      other[(uint64_t)i * kStatusStride] = 0;
+  }
+  if (tid == 0) {
+    for (int b = 0; b < kCBufs; ++b) mbar_init(smem_u32(&s_bar[b]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t phase = 0;  // bit b: parity of buffer b's mbarrier
+
+  while (true) {
+    if (tid == 0) s_chunk = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t c = s_chunk;
+    if (c >= n_chunks) break;
+    const uint32_t shard = c / chunks_per_shard, ci = c - shard * chunks_per_shard;
+    // chunk ci of the shard: keys [k0, k1), k0 rounded down to 16 keys
+    const uint64_t k0 = ((uint64_t)ci * shard_cap / chunks_per_shard) & ~15ull;
+    const uint64_t k1 = ci + 1 == chunks_per_shard
+                            ? shard_cap
+                            : (((uint64_t)(ci + 1) * shard_cap / chunks_per_shard) & ~15ull);
+    const uint32_t nt = (uint32_t)((k1 - k0 + kTile - 1) / kTile);
+    const uint64_t sbase = (uint64_t)shard * shard_cap;
+    auto tcount = [&](uint32_t j) { return (uint32_t)min((uint64_t)kTile, k1 - k0 - (uint64_t)j * kTile); };
+    auto is_tma = [&](uint32_t j) {
+      return ((sbase + k0 + (uint64_t)j * kTile) & 1) == 0 && (tcount(j) & 1) == 0;
+    };
+    // thread 0: bulk load of tile j into its buffer j % kCBufs (GEAR_CHUNK_L2:
+    // phase-1 loads marked evict-last, phase-2 reloads evict-first)
+    auto issue = [&](uint32_t j, bool reload) {
+      if (!is_tma(j)) return;
+      const uint32_t dst = smem_u32(s_buf + (size_t)(j % kCBufs) * kTile);
+      const uint64_t* src = key + sbase + k0 + (uint64_t)j * kTile;
+      const uint32_t bytes = tcount(j) * 8, bar = smem_u32(&s_bar[j % kCBufs]);
+#if GEAR_CHUNK_L2
+      uint64_t pol;
+      if (reload)
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      else
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+              dst),
+          "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+          : "memory");
+#else
+      (void)reload;
+      bulk_g2s(dst, src, bytes, bar);
+#endif
+    };
+    // every thread: tile j is in its buffer (TMA wait, or plain zero-padded loads)
+    auto land = [&](uint32_t j) {
+      const int b = (int)(j % kCBufs);
+      if (is_tma(j)) {
+        while (!mbar_try_wait(smem_u32(&s_bar[b]), (phase >> b) & 1u)) {
+        }
+        phase ^= 1u << b;
+      } else {
+        uint64_t* buf = s_buf + (size_t)b * kTile;
+        const uint64_t* src = key + sbase + k0 + (uint64_t)j * kTile;
+        const uint32_t count = tcount(j);
+        for (int e = tid; e < kTile; e += kThreads) buf[e] = (uint32_t)e < count ? src[e] : 0ull;
+        __syncthreads();
+      }
+    };
+    if (tid == 0)
+      for (uint32_t j = 0; j < nt && j < (uint32_t)kCBufs; ++j) issue(j, false);
+
+    // phase 1: tile sums
+    for (uint32_t j = 0; j < nt; ++j) {
+      land(j);
+      const uint32_t count = tcount(j);
+      const ulonglong2* b2 = reinterpret_cast<const ulonglong2*>(s_buf + (size_t)(j % kCBufs) * kTile);
+      uint64_t sum = 0;
+#pragma unroll
+      for (int k = 0; k < kItems / 2; ++k) {
+        const uint32_t e = 2u * (uint32_t)(k * kThreads + tid);
+        const ulonglong2 x = b2[k * kThreads + tid];
+        const uint64_t a = e < count ? x.x : 0ull, bb = e + 1 < count ? x.y : 0ull;
+        sum += kIndicator ? (uint64_t)(a > 0) + (uint64_t)(bb > 0) : a + bb;
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(kFull, sum, d);
+      if (lane == 0) s_red[j & 1][warp] = sum;
+      __syncthreads();  // buffer j % kCBufs read by every thread; s_red[j & 1] complete
+      if (tid == 0) {
+        uint64_t ts = 0;
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) ts += s_red[j & 1][w];
+        s_tsum[j] = ts;
+        if (j + kCBufs < nt) issue(j + kCBufs, false);  // the last kCBufs tiles stay resident
+      }
+    }
+    __syncthreads();  // s_tsum complete
+    TL_MARK(1);
+    // chunk aggregate -> status; tile sums -> tile-exclusive prefixes (thread 0)
+    if (tid == 0) {
+      uint64_t run = 0;
+      for (uint32_t j = 0; j < nt; ++j) {
+        const uint64_t x = s_tsum[j];
+        s_tsum[j] = run;
+        run += x;
+      }
+      st_relaxed_u64(status + (uint64_t)c * kStatusStride, (ci == 0 ? kFlagP : kFlagA) | run);
+      s_excl = run;  // (aggregate, until the look-back below)
+    }
+    __syncthreads();
+    const uint64_t agg = s_excl;
+    // look-back over the shard's preceding chunks, 2 * kThreads per round
+    uint64_t excl = 0;
+    if (ci != 0) {
+      const int64_t first = (int64_t)c - (int64_t)ci;
+      int64_t pred = (int64_t)c - 1;
+      while (true) {
+        uint64_t st[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int64_t idx = pred - tid - (int64_t)k * kThreads;
+          st[k] = idx >= first ? ld_relaxed_u64(status + idx * kStatusStride) : kFlagP;
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int64_t idx = pred - tid - (int64_t)k * kThreads;
+          while ((st[k] >> 62) == 0) st[k] = ld_relaxed_u64(status + idx * kStatusStride);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const unsigned m = __ballot_sync(kFull, (st[k] >> 62) == 2);
+          if (lane == 0) s_pmask[k][warp] = m;
+        }
+        __syncthreads();
+        uint32_t dp = 0xffffffffu;
+#pragma unroll
+        for (int k = 1; k >= 0; --k)
+#pragma unroll
+          for (int w = kThreads / 32 - 1; w >= 0; --w) {
+            const unsigned m = s_pmask[k][w];
+            if (m) dp = (uint32_t)(k * kThreads + w * 32 + __ffs(m) - 1);
+          }
+        uint64_t part = 0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          part += ((uint32_t)(tid + k * kThreads) <= dp) ? (st[k] & kValMask) : 0ull;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(kFull, part, d);
+        if (lane == 0) s_red[0][warp] = part;
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < kThreads / 32; ++w) excl += s_red[0][w];
+        __syncthreads();  // s_pmask / s_red read before their next use
+        if (dp != 0xffffffffu) break;
+        pred -= 2 * kThreads;  // no inclusive prefix in this window
+      }
+      if (tid == 0) st_relaxed_u64(status + (uint64_t)c * kStatusStride, kFlagP | (excl + agg));
+    }
+    if (tid == 0 && ci + 1 == chunks_per_shard) {
+      ShardTotals rec;
+      rec.total_and_parity = (excl + agg) | ((uint64_t)parity << 63);
+      rec.aux = 0;
+      totals[shard] = rec;
+    }
+
+    TL_MARK(2);
+    // phase 2: tiles in reverse order; tile j - kCBufs is loaded into tile j's
+    // buffer once tile j is written out
+    const int r = tid & 7;
+    for (int64_t jj = (int64_t)nt - 1; jj >= 0; --jj) {
+      const uint32_t j = (uint32_t)jj;
+      if (j + kCBufs < nt) land(j);  // reloaded (the resident ones landed in phase 1)
+      const uint32_t count = tcount(j);
+      uint64_t* buf = s_buf + (size_t)(j % kCBufs) * kTile;
+      ulonglong2* b2 = reinterpret_cast<ulonglong2*>(buf) + tid * (kItems / 2);
+      uint64_t lo[kItems / 2], hi[kItems / 2];
+#pragma unroll
+      for (int k = 0; k < kItems / 2; ++k) {
+        const uint32_t e = (uint32_t)(tid * kItems + 2 * ((k + r) & 7));
+        const ulonglong2 x = b2[(k + r) & 7];
+        const uint64_t a = e < count ? x.x : 0ull, bb = e + 1 < count ? x.y : 0ull;
+        lo[k] = kIndicator ? (a > 0 ? 1ull : 0ull) : a;
+        hi[k] = kIndicator ? (bb > 0 ? 1ull : 0ull) : bb;
+      }
+      uint64_t run = 0;
+#pragma unroll
+      for (int k = 0; k < kItems / 2; ++k) {
+        lo[k] += run;
+        hi[k] += lo[k];
+        run = hi[k];
+      }
+      const uint64_t total = run;
+      uint64_t s_rot = 0;
+#pragma unroll
+      for (int k = 0; k < kItems / 2; ++k) s_rot = (k == 7 - r) ? hi[k] : s_rot;
+      const uint64_t incl = warp_incl_scan_u64(total, lane);
+      if (lane == 31) s_red[j & 1][warp] = incl;
+      __syncthreads();
+      uint64_t warp_excl = excl + s_tsum[j];  // chunk prefix + tile prefix
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) warp_excl += (w < warp) ? s_red[j & 1][w] : 0ull;
+      const uint64_t base = warp_excl + incl - total;
+#pragma unroll
+      for (int k = 0; k < kItems / 2; ++k) {
+        const uint64_t off = base - s_rot + (k < 8 - r ? total : 0ull);
+        b2[(k + r) & 7] = make_ulonglong2(lo[k] + off, hi[k] + off);
+      }
+      __syncthreads();  // the tile's CDF is in shared memory
+      uint64_t* dst = cdf + sbase + k0 + (uint64_t)j * kTile;
+      if (count == (uint32_t)kTile && ((sbase + k0) & 1) == 0) {
+        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(buf);
+#pragma unroll
+        for (int k = 0; k < kItems / 2; ++k) {
+          const ulonglong2 x = src[k * kThreads + tid];
+          st_stream_u64x2(dst + 2 * (k * kThreads + tid), x.x, x.y);
+        }
+      } else {
+        for (int e = tid; e < (int)count; e += kThreads) dst[e] = buf[e];
+      }
+      __syncthreads();  // buffer read by every thread
+      if (tid == 0 && j >= (uint32_t)kCBufs) issue(j - kCBufs, true);
+    }
+  }
+  TL_PRINT("chunk");
+  // The last CTA to exit re-arms the ticket and the exit counter and
+  // publishes the new parity (as scan_kernel).
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && tid == 0) {
+    *ticket = 0;
+    ticket[1] = epoch + 1;
+    *done = 0;
+    *par_dev = parity;
   }
 }
 
@@ -585,6 +912,7 @@ __global__ void __launch_bounds__(kThreads, kS2Ctas) scan2p_kernel(
   __shared__ uint64_t s_red[kThreads / 32];
   __shared__ bool s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  TL_DECL
   const uint64_t par_old = __ldcg(par_dev);
   const uint32_t mode0 = __ldcg(buf_mode), mode1 = __ldcg(buf_mode + 1);
   const uint32_t parity = (uint32_t)(par_old & 1) ^ 1u;
@@ -718,6 +1046,7 @@ __global__ void __launch_bounds__(kThreads, kS2Ctas) scan2p_kernel(
   // Arrivals: this CTA's tiles of every shard in one atomic; the CTA that
   // completes a shard builds its prefix of tile totals P.
   __syncthreads();
+  TL_MARK(1);
   if (tid == 0) __threadfence();  // this CTA's cdf / ttot / dirty writes before its arrivals
   for (uint32_t ls = 0; ls < n_shards_local; ++ls) {
     const uint32_t mine = s_shcnt[ls];
@@ -775,6 +1104,7 @@ __global__ void __launch_bounds__(kThreads, kS2Ctas) scan2p_kernel(
     }
     __syncthreads();
   }
+  TL_PRINT("s2p");
 }
 
 }  // namespace
@@ -842,9 +1172,58 @@ uint32_t scan_tiles_per_shard(uint64_t shard_cap) {
 cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf0, uint64_t* cdf1, uint64_t shard_cap,
                         uint32_t n_shards_local, int indicator, uint64_t* par_dev,
                         ShardTotals* totals_out, uint64_t* status0, uint64_t* status1,
-                        uint32_t* ticket, uint32_t* done, cudaStream_t s) {
+                        uint32_t* ticket, uint32_t* done, int chunked, cudaStream_t s) {
   const uint32_t tps = scan_tiles_per_shard(shard_cap);
   const uint32_t n_tiles = tps * n_shards_local;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // Chunked look-back (scan_chunk_kernel): one chunk per resident CTA, so
+  // its phase-2 re-read hits L2 while the rank's keys are a fraction of it.
+  // chunked: 1 = whenever the geometry allows, 0 = never, -1 = auto (keys of
+  // the rank <= chunk_max_bytes, and at least one tile per CTA); >= 2: as 1
+  // for a grid of that many CTAs (tests).
+  {
+    // (chunked >= 2: chunks sized for that many CTAs, and at most that many
+    // CTAs, so chunks are long -- phase-2 reloads -- and CTAs claim several)
+    const uint32_t G = chunked >= 2 ? (uint32_t)chunked : (uint32_t)sms * kChunkCtasPerSm;
+    uint64_t cps = std::min<uint64_t>(std::max<uint64_t>(1, (uint64_t)G * kChunksPerCta / n_shards_local), tps);
+    const uint64_t max_keys = (uint64_t)kMaxChunkTiles * kTile - 32;
+    cps = std::max<uint64_t>(cps, (shard_cap + max_keys - 1) / max_keys);
+    const uint64_t n_chunks = cps * n_shards_local;
+    static const uint64_t chunk_max_bytes = [] {
+      const char* e = getenv("GEAR_SCAN_CHUNK_MAX_MB");
+      return (uint64_t)(e ? atoll(e) : 96) << 20;
+    }();
+    const bool fits = n_chunks <= n_tiles && shard_cap >= cps * 16;
+    const bool want = chunked >= 1 ||
+                      (chunked == -1 && (uint64_t)n_shards_local * shard_cap * 8 <= chunk_max_bytes &&
+                       n_tiles >= G);
+    if (fits && want) {
+      const size_t smem = (size_t)kCBufs * kTile * 8;
+      static bool configured = false;
+      if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(scan_chunk_kernel<true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(scan_chunk_kernel<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured = true;
+      }
+      const uint32_t grid = (uint32_t)std::min<uint64_t>(n_chunks, G);
+      count_launch();
+      if (indicator)
+        scan_chunk_kernel<true><<<grid, kThreads, smem, s>>>(
+            key, cdf0, cdf1, shard_cap, (uint32_t)cps, (uint32_t)n_chunks, n_tiles, par_dev,
+            totals_out, status0, status1, ticket, done);
+      else
+        scan_chunk_kernel<false><<<grid, kThreads, smem, s>>>(
+            key, cdf0, cdf1, shard_cap, (uint32_t)cps, (uint32_t)n_chunks, n_tiles, par_dev,
+            totals_out, status0, status1, ticket, done);
+      return cudaGetLastError();
+    }
+  }
   const size_t smem = (size_t)kScanBufs * kTile * 8;
   static bool configured = false;
   if (!configured) {
@@ -856,9 +1235,6 @@ cudaError_t launch_scan(const uint64_t* key, uint64_t* cdf0, uint64_t* cdf1, uin
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint32_t grid = std::min<uint32_t>(n_tiles, (uint32_t)sms * kScanCtasPerSm);
   count_launch();
   if (indicator)

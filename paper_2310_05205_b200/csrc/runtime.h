@@ -122,6 +122,7 @@ struct gear_table {
   int cdf_mode = -1;      // -1 none, 0 weighted keys, 1 indicator
   bool dirty = true;
   int cdf_levels = 2;     // 1: flat CDF (decoupled look-back), 2: two-level incremental
+  int scan_chunk = -1;    // flat CDF: 1 chunked look-back, 0 per-tile look-back, -1 auto by size
   uint32_t* tile_dirty = nullptr;    // [R*tiles] bit b: tile changed since buffer b's build
   uint64_t* tile_tot = nullptr;      // [2][R*tiles] each buffer's tile totals
   uint32_t* cdf_buf_mode = nullptr;  // [2] mode each buffer was built in (0 none, 1 w, 2 ind)

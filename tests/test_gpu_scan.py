@@ -37,14 +37,21 @@ def _check_cdf(P, R, Cs, indicator):
                                  f"(tile {bad[0] // 4096})")
 
 
-@pytest.mark.parametrize("levels", [1, 2])
-@pytest.mark.parametrize("R,Cs", [(1, 3_000_017), (3, 700_001)])
-def test_cdf_every_entry(torch_cuda, levels, R, Cs):
+# (cdf_levels, scan_chunk): the flat look-back over 4096-key tiles (chunk 0),
+# over one chunk per CTA (chunk 1), over chunks with the grid capped at 7 CTAs
+# so every CTA claims several chunks (chunk 7), and the two-level layout
+LAYOUTS = [(1, 0), (1, 1), (1, 7), (2, -1)]
+
+
+@pytest.mark.parametrize("levels,chunk", LAYOUTS)
+@pytest.mark.parametrize("R,Cs", [(1, 3_000_017), (3, 700_001), (8, 150_003)])
+def test_cdf_every_entry(torch_cuda, levels, chunk, R, Cs):
     import paper_2310_05205_b200 as G
     from gpu_harness import Pair
     P = Pair(capacity=Cs * R, seq_len=1, colspecs=[synth.ColSpec("x", "u8", (1,))], R=R,
              mirror=False)
     G.gear_table_set_tuning(P.t.handle, "cdf_levels", levels)
+    G.gear_table_set_tuning(P.t.handle, "scan_chunk", chunk)
     prio = synth.priorities(Cs * R, seed=11, zero_frac=0.05)
     for s in range(R):
         P.t.insert(s, [np.zeros((Cs, 1), np.uint8)], prio[s * Cs:(s + 1) * Cs])
@@ -78,8 +85,10 @@ def test_cdf_layout_switches(torch_cuda):
         P.t.insert(s, [np.zeros((Cs, 1), np.uint8)], prio[s * Cs:(s + 1) * Cs])
         P.o.insert(s, prio[s * Cs:(s + 1) * Cs])
     rng = np.random.default_rng(9)
-    for rnd, levels in enumerate([1, 1, 2, 1, 2, 2, 1, 1, 1]):
+    seq = [(1, 0), (1, 1), (2, -1), (1, 0), (2, -1), (2, -1), (1, 1), (1, 0), (1, 1), (1, 5)]
+    for rnd, (levels, chunk) in enumerate(seq):
         G.gear_table_set_tuning(P.t.handle, "cdf_levels", levels)
+        G.gear_table_set_tuning(P.t.handle, "scan_chunk", chunk)
         P.check_sample(G.GEAR_PRIORITIZED, 2048, 300 + rnd)
         _check_cdf(P, R, Cs, indicator=False)
         ids = rng.integers(0, Cs * R, 512).astype(np.uint64)

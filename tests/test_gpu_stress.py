@@ -32,31 +32,34 @@ def torch_cuda():
     return torch
 
 
-CASES = [  # (R, Cs, B, cdf_levels, strategy, steps per graph, replays)
-    (1, 4096, 64, 1, "prioritized", 10, 60),
-    (3, 1500, 37, 2, "prioritized", 10, 60),
-    (8, 700, 1000, 1, "weighted", 5, 60),
-    (5, 9000, 512, 2, "uniform", 10, 40),
-    (2, 20000, 256, 1, "prioritized", 8, 40),
-    (4, 3000, 128, 2, "topk", 10, 40),
-    (2, 2500, 96, 1, "fifo", 5, 40),
-    (1, 30000, 4096, 2, "prioritized", 4, 40),
+CASES = [  # (R, Cs, B, cdf_levels, strategy, steps per graph, replays, scan_chunk)
+    (1, 4096, 64, 1, "prioritized", 10, 60, 0),
+    (3, 1500, 37, 2, "prioritized", 10, 60, -1),
+    (8, 700, 1000, 1, "weighted", 5, 60, 1),
+    (5, 9000, 512, 2, "uniform", 10, 40, -1),
+    (2, 20000, 256, 1, "prioritized", 8, 40, 0),
+    (2, 20000, 256, 1, "prioritized", 8, 40, 3),
+    (3, 50000, 512, 1, "uniform", 8, 40, 1),
+    (4, 3000, 128, 2, "topk", 10, 40, -1),
+    (2, 2500, 96, 1, "fifo", 5, 40, -1),
+    (1, 30000, 4096, 2, "prioritized", 4, 40, -1),
 ]
 
 
-@pytest.mark.parametrize("case", CASES, ids=[f"R{c[0]}-Cs{c[1]}-B{c[2]}-L{c[3]}-{c[4]}" for c in CASES])
+@pytest.mark.parametrize("case", CASES, ids=[f"R{c[0]}-Cs{c[1]}-B{c[2]}-L{c[3]}-{c[4]}-K{c[7]}" for c in CASES])
 def test_graph_replay_stress(torch_cuda, case):
     import oracle
     import paper_2310_05205_b200 as G
     from gpu_harness import ORACLE_STRATEGY, Pair
     torch = torch_cuda
-    R, Cs, B, levels, sname, S, reps = case
+    R, Cs, B, levels, sname, S, reps, chunk = case
     cols = [synth.ColSpec("obs", "f32", (3,)), synth.ColSpec("tok", "u8", (5,))]
     N = R * Cs
     P = Pair(capacity=N, seq_len=2, colspecs=cols, R=R, max_batch=max(4096, B))
     P.fill(synth.priorities(N, seed=R * 7 + B, zero_frac=0.05))
     h = P.t.handle
     G.gear_table_set_tuning(h, "cdf_levels", levels)
+    G.gear_table_set_tuning(h, "scan_chunk", chunk)
     strat = G.STRATEGIES[sname]
     ostrat = ORACLE_STRATEGY[strat]
     seed0, beta = 0x5EED1000 + B, 0.4

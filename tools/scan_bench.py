@@ -4,7 +4,9 @@ a full two-level rebuild (cdf_levels 2 re-selected: both buffers forgotten).
 Rebuild time = (update of 1 key + sample of 1 draw) - (update + sample without
 rebuild is impossible, so: sample right after a layout switch minus a sample
 with a clean CDF); CUDA events, median of 20.  Run under ncu for kernel
-durations and DRAM bytes:  python tools/scan_bench.py 40000000"""
+durations and DRAM bytes:  python tools/scan_bench.py 40000000 [reps] [variants]
+(variants: comma list of levels1_tile, levels1_chunk, levels2).  Also times a
+device copy of the same bytes (the size-matched streaming ceiling)."""
 import json
 import os
 import sys
@@ -43,8 +45,12 @@ def sample():
 
 
 out = {"keys": N, "bytes_per_rebuild": 16 * N}
-for levels in (1, 2):
+variants = [("levels1_tile", 1, 0), ("levels1_chunk", 1, 1), ("levels2", 2, -1)]
+if len(sys.argv) > 3:
+    variants = [v for v in variants if v[0] in sys.argv[3].split(",")]
+for name, levels, chunk in variants:
     gear.gear_table_set_tuning(t.handle, "cdf_levels", levels)
+    gear.gear_table_set_tuning(t.handle, "scan_chunk", chunk)
     sample()
     base, full = [], []
     for i in range(reps):
@@ -58,7 +64,16 @@ for levels in (1, 2):
             sample()                                    # ... and of the other
             base.append(timed(sample))                  # both built: every tile clean
     ms = float(np.median(full) - np.median(base))
-    out[f"levels{levels}"] = {"rebuild_us": ms * 1e3, "GBps": 16 * N / (ms / 1e3) / 1e9}
+    out[name] = {"rebuild_us": ms * 1e3, "GBps": 16 * N / (ms / 1e3) / 1e9,
+                 "frac_of_6456": 16 * N / (ms / 1e3) / 1e9 / 6456.2}
+# size-matched copy: the same bytes (N u64 read + N u64 written) as one
+# device-to-device copy, the ceiling a streaming kernel of this size reaches
+a = torch.empty(N, dtype=torch.int64, device="cuda")
+b = torch.empty_like(a)
+with torch.cuda.stream(s):
+    cp = [timed(lambda: b.copy_(a)) for _ in range(reps)]
+ms = float(np.median(cp))
+out["copy_same_bytes"] = {"us": ms * 1e3, "GBps": 16 * N / (ms / 1e3) / 1e9}
 assert t.sync()[0] == 0
 t.close()
 print(json.dumps(out))
