@@ -90,9 +90,6 @@ __device__ __forceinline__ uint64_t gtimer() {
 #endif
 constexpr int kStatusStride = GEAR_STATUS_STRIDE;  // u64 words between two tiles' status words
 constexpr int kScanBufs = 3;
-#ifndef GEAR_SCAN_FREEBAR
-#define GEAR_SCAN_FREEBAR 0
-#endif
 constexpr int kScanCtasPerSm = 2;
 #ifndef GEAR_SCAN_LOOK_PER
 #define GEAR_SCAN_LOOK_PER 1
@@ -115,7 +112,6 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
   __shared__ uint64_t s_red[kThreads / 32];   // scan: warp totals
   __shared__ uint64_t s_red2[kThreads / 32];  // look-back: warp partial sums
   __shared__ uint32_t s_pmask[kScanLookPer][kThreads / 32];
-  __shared__ __align__(8) uint64_t s_free[kScanBufs];  // GEAR_SCAN_FREEBAR: buffer read by every warp
   __shared__ bool s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   TL_DECL
@@ -182,7 +178,6 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
   if (tid == 0) {
     for (int b = 0; b < kScanBufs; ++b) {
       mbar_init(smem_u32(&s_bar[b]), 1);
-      mbar_init(smem_u32(&s_free[b]), kThreads / 32);
       s_t[b] = kNoTile;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -194,8 +189,6 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
   __syncthreads();
 
   uint32_t phase = 0;  // bit b: parity of buffer b's mbarrier
-  uint32_t fphase = 0;  // bit b: parity of buffer b's free mbarrier (thread 0, GEAR_SCAN_FREEBAR)
-  (void)fphase;
 #ifdef GEAR_SCAN_PROF
   uint64_t pr[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pt = clock64(), iters = 0, polls = 0;
 #define PROF(i) do { const uint64_t c_ = clock64(); pr[i] += c_ - pt; pt = c_; } while (0)
@@ -351,24 +344,6 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
       }
     }
     PROF(4);
-#if GEAR_SCAN_FREEBAR
-    // each warp reports it has read tile n-1's buffer; only thread 0 waits for
-    // all of them before it loads into that buffer -- no block barrier
-    if (tp != kNoTile) {
-      __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_free[bp])) : "memory");
-    }
-    if (tid == 0 && t != kNoTile) {
-      if (tp != kNoTile) {
-        while (!mbar_try_wait(smem_u32(&s_free[bp]), (fphase >> bp) & 1u)) {
-        }
-        fphase ^= 1u << bp;
-      }
-      if (s_t[bn] != kNoTile) claim(bp);
-      else s_t[bp] = kNoTile;
-    }
-#else
     __syncthreads();  // tile n-1's buffer read by every thread: free
     // 4. claim tile n+2 into tile n-1's buffer, just freed: its load has a
     //    whole iteration (tile n+1 is already in flight in the third buffer)
@@ -376,7 +351,6 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
       if (s_t[bn] != kNoTile) claim(bp);
       else s_t[bp] = kNoTile;  // tickets only grow: nothing more for this CTA
     }
-#endif
     // (s_t / s_tma of the claimed buffer are read two iterations from now,
     // after several barriers)
     PROF(5);
