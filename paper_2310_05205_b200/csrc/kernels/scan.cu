@@ -411,9 +411,6 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
 #ifndef GEAR_CHUNK_BUFS
 #define GEAR_CHUNK_BUFS 3
 #endif
-#ifndef GEAR_CHUNK_L2
-#define GEAR_CHUNK_L2 0
-#endif
 #ifndef GEAR_CHUNK_CTAS
 #define GEAR_CHUNK_CTAS 2
 #endif
@@ -473,30 +470,13 @@ __global__ void __launch_bounds__(kThreads, kChunkCtasPerSm) scan_chunk_kernel(
     auto is_tma = [&](uint32_t j) {
       return ((sbase + k0 + (uint64_t)j * kTile) & 1) == 0 && (tcount(j) & 1) == 0;
     };
-    // thread 0: bulk load of tile j into its buffer j % kCBufs (GEAR_CHUNK_L2:
-    // phase-1 loads marked evict-last, phase-2 reloads evict-first)
-    auto issue = [&](uint32_t j, bool reload) {
+    // thread 0: bulk load of tile j into its buffer j % kCBufs (L2 evict-last
+    // hints on phase-1 loads / evict-first on phase-2 reloads were measured no
+    // faster, profiles/r02_scan/chunk)
+    auto issue = [&](uint32_t j) {
       if (!is_tma(j)) return;
-      const uint32_t dst = smem_u32(s_buf + (size_t)(j % kCBufs) * kTile);
-      const uint64_t* src = key + sbase + k0 + (uint64_t)j * kTile;
-      const uint32_t bytes = tcount(j) * 8, bar = smem_u32(&s_bar[j % kCBufs]);
-#if GEAR_CHUNK_L2
-      uint64_t pol;
-      if (reload)
-        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-      else
-        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                   : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-              dst),
-          "l"(src), "r"(bytes), "r"(bar), "l"(pol)
-          : "memory");
-#else
-      (void)reload;
-      bulk_g2s(dst, src, bytes, bar);
-#endif
+      bulk_g2s(smem_u32(s_buf + (size_t)(j % kCBufs) * kTile), key + sbase + k0 + (uint64_t)j * kTile,
+               tcount(j) * 8, smem_u32(&s_bar[j % kCBufs]));
     };
     // every thread: tile j is in its buffer (TMA wait, or plain zero-padded loads)
     auto land = [&](uint32_t j) {
@@ -514,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, kChunkCtasPerSm) scan_chunk_kernel(
       }
     };
     if (tid == 0)
-      for (uint32_t j = 0; j < nt && j < (uint32_t)kCBufs; ++j) issue(j, false);
+      for (uint32_t j = 0; j < nt && j < (uint32_t)kCBufs; ++j) issue(j);
 
     // phase 1: tile sums
     for (uint32_t j = 0; j < nt; ++j) {
@@ -538,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, kChunkCtasPerSm) scan_chunk_kernel(
 #pragma unroll
         for (int w = 0; w < kThreads / 32; ++w) ts += s_red[j & 1][w];
         s_tsum[j] = ts;
-        if (j + kCBufs < nt) issue(j + kCBufs, false);  // the last kCBufs tiles stay resident
+        if (j + kCBufs < nt) issue(j + kCBufs);  // the last kCBufs tiles stay resident
       }
     }
     __syncthreads();  // s_tsum complete
@@ -665,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, kChunkCtasPerSm) scan_chunk_kernel(
           bulk_s2g(dst, smem_u32(buf), kTile * 8);
           if (j >= (uint32_t)kCBufs) {
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            issue(j - kCBufs, true);
+            issue(j - kCBufs);
           }
         }
         continue;
@@ -673,7 +653,7 @@ __global__ void __launch_bounds__(kThreads, kChunkCtasPerSm) scan_chunk_kernel(
       __syncthreads();  // the tile's CDF is in shared memory
       for (int e = tid; e < (int)count; e += kThreads) dst[e] = buf[e];  // ragged / unaligned
       __syncthreads();  // buffer read by every thread
-      if (tid == 0 && j >= (uint32_t)kCBufs) issue(j - kCBufs, true);
+      if (tid == 0 && j >= (uint32_t)kCBufs) issue(j - kCBufs);
     }
     // the next chunk's loads reuse the buffers: every bulk store has read them
     if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
