@@ -845,7 +845,8 @@ __global__ void __launch_bounds__(kThreads) scan2_kernel(
 // incremental no-op of a 40 M-key table no longer launches 9766 CTAs.  Work
 // tiles stream through three shared-memory buffers: TMA bulk loads
 // (cp.async.bulk + mbarrier) two tiles ahead, the tile-local scan in place
-// (the rotated 128-bit layout of scan_kernel), coalesced 16-B stores.  Each
+// (the rotated 128-bit layout of scan_kernel), one TMA bulk store per tile
+// (16-B stores from every thread for a ragged / unaligned tile).  Each
 // CTA then adds its tiles to every shard's arrival counter in one atomic;
 // the CTA that completes a shard builds that shard's prefix of tile totals,
 // and the last shard flips the parity and records the buffer's mode, as in
@@ -987,6 +988,26 @@ __global__ void __launch_bounds__(kThreads, kS2Ctas) scan2p_kernel(
         const uint64_t off = base - s_rot + (k < 8 - r ? total : 0ull);
         b2[(k + r) & 7] = make_ulonglong2(lo[k] + off, hi[k] + off);
       }
+      if (tma) {
+        // one bulk store of the tile (smem -> global) by thread 0; the next
+        // load goes into the PREVIOUS tile's buffer once its store has read
+        // it (only the newest store may still be reading) -- no barrier here
+        // (vs 16-B stores from every thread: full rebuild of 10 M keys 28.6-31.6
+        // instead of 34.0-36.1 us under ncu; event-timed +22% at 5 M keys,
+        // -5% at 20 M, even at 10 / 40 M; profiles/r02_scan/s2store)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();  // the tile's prefixes are in shared memory; s_red read
+        if (tid == 0) {
+          bulk_s2g(cdf + gbase, smem_u32(buf), kTile * 8);
+          ttot[wt] = agg;
+          atomicAnd(dirty + wt, ~bit);  // this buffer's bit; the other buffer's stays
+          if (j + kS2Bufs - 1 < nwork) {
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            issue(j + kS2Bufs - 1);
+          }
+        }
+        continue;
+      }
       __syncthreads();  // the tile's prefixes are in shared memory; s_red read
       if (tma) {
         const ulonglong2* src = reinterpret_cast<const ulonglong2*>(buf);
@@ -1001,9 +1022,16 @@ __global__ void __launch_bounds__(kThreads, kS2Ctas) scan2p_kernel(
         atomicAnd(dirty + wt, ~bit);  // this buffer's bit; the other buffer's stays
       }
       __syncthreads();  // buffer read by every thread: free for tile j + kS2Bufs
-      if (tid == 0 && j + kS2Bufs - 1 < nwork) issue(j + kS2Bufs - 1);
+      if (tid == 0 && j + kS2Bufs - 1 < nwork) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // a bulk-stored buffer
+        issue(j + kS2Bufs - 1);
+      }
     }
+    // the next chunk of the tile list reuses the buffers
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncthreads();
   }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // before the arrivals
 
   // Arrivals: this CTA's tiles of every shard in one atomic; the CTA that
   // completes a shard builds its prefix of tile totals P.
