@@ -98,7 +98,7 @@ typedef enum { GEAR_DEVICE = 0, GEAR_HOST = 1 } gear_placement;
  * importance-sampling weights (q_min/q)^beta over the rank's slice.  TOPK
  * (decentralised like FIFO) selects the W*B selectable
  * trajectories with the largest priority keys, ties by the smaller global id,
- * in that order (W*B <= 8192). */
+ * in that order (W*B <= 129024). */
 typedef enum {
   GEAR_FIFO = 0,
   GEAR_LIFO = 1,
@@ -349,7 +349,7 @@ gear_status gear_update_priorities(gear_table* t, uint32_t n, const uint64_t* id
  *  the kernels through the mapped address, stream-ordered) or pageable host
  *  memory (copied at the end of the call).
  *  TOPK: the W*B selectable trajectories with the largest keys, ties by the
- *  smaller global id, in that order (reading Q20; W*B <= 8192).
+ *  smaller global id, in that order (reading Q20; W*B <= 129024).
  *  flags: 0 or GEAR_SAMPLE_OWNER_AFFINE | GEAR_SAMPLE_DEVICE_SEED (other
  *  bits: INVALID_ARG); same value on every rank.
  *  Nothing selectable: outputs get GEAR_IDX_NONE and EMPTY is latched.

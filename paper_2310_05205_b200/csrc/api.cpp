@@ -489,7 +489,7 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   GEAR_TRY(dalloc(&t->glob_slot, K));
   GEAR_TRY(dalloc(&t->cand_local, t->R * K));
   GEAR_TRY(dalloc(&t->cand_all, t->S * K));
-  GEAR_TRY(dalloc(&t->topk_tmp, t->R * (K + kTopkEqMax)));
+  GEAR_TRY(dalloc(&t->topk_tmp, 2 * t->R * (K + kTopkEqMax)));  // candidates + sorted runs
   GEAR_TRY(dalloc(&t->topk_state, t->R));
   GEAR_CUDA(cudaMemset(t->topk_state, 0, t->R * sizeof(TopkState)));
   GEAR_TRY(dalloc(&t->topk_cnt, (size_t)t->R * kTopkMaxCtas * 2));

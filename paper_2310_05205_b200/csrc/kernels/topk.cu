@@ -519,9 +519,42 @@ __device__ __forceinline__ bool before(const Cand& a, const Cand& b) {
 
 // Rank sort: the position of a candidate is the number of candidates before
 // it in the TopK order (keys and slots are distinct, so the ranks are a
-// permutation).  One warp per candidate: the lanes compare it with a strided
-// 1/32 of the list (L1-resident after the first warps) and sum; kSortWarps
-// candidates per CTA, ceil(K / kSortWarps) CTAs per shard.
+// permutation).
+//  * n <= kSortDirect candidates (one launch, kMerge = false): one warp per
+//    candidate, the lanes compare it with a strided 1/32 of the list
+//    (L1-resident after the first warps) and sum; kSortWarps candidates per
+//    CTA, ceil(n / kSortWarps) CTAs per shard.
+//  * more (kMerge = true, after run_rank_kernel): the list is cut into runs of
+//    kSortRun candidates, each already sorted by run_rank_kernel (the same
+//    warp rank within the run); a candidate's rank is its position in its run
+//    plus, for every other run, the number of that run's candidates before it
+//    -- one binary search per run, one lane per run (<= 32 runs) -- so the
+//    work is O(n log n) instead of O(n^2).
+// The output (and at W > 1 every peer's mailbox) gets the first K ranks.
+constexpr uint32_t kSortDirect = 8192;
+constexpr uint32_t kSortRun = 4096;
+
+__global__ void __launch_bounds__(kSortThreads)
+    run_rank_kernel(uint32_t K, const Cand* __restrict__ unsorted, Cand* __restrict__ runs,
+                    const ShardTotals* __restrict__ totals) {
+  const uint32_t ls = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const uint32_t n = (uint32_t)totals[ls].total_and_parity;
+  const uint32_t i = blockIdx.x * kSortWarps + (threadIdx.x >> 5);
+  if (i >= n) return;
+  const uint64_t cap = (uint64_t)K + kTopkEqMax;
+  const Cand* in = unsorted + (uint64_t)ls * cap;
+  const Cand me = in[i];
+  const uint32_t q0 = i / kSortRun * kSortRun, q1 = min(n, q0 + kSortRun);
+  uint32_t rank = 0;
+#pragma unroll 4
+  for (uint32_t j = q0 + lane; j < q1; j += 32) rank += before(in[j], me);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) rank += __shfl_xor_sync(kFull, rank, d);
+  if (lane == 0) runs[(uint64_t)ls * cap + q0 + rank] = me;
+}
+
+template <bool kMerge>
 __global__ void __launch_bounds__(kSortThreads)
     sort_kernel(uint32_t K, uint32_t first_shard, const Cand* __restrict__ unsorted,
                 Cand* __restrict__ sorted, const ShardTotals* __restrict__ totals, TopkState* st,
@@ -543,10 +576,27 @@ __global__ void __launch_bounds__(kSortThreads)
     const Cand* in = unsorted + (uint64_t)ls * (K + kTopkEqMax);
     const Cand me = in[i];
     uint32_t rank = 0;
-#pragma unroll 4
-    for (uint32_t j = lane; j < n; j += 32) rank += before(in[j], me);
+    if (kMerge) {  // `in` holds sorted runs: position in the own run + searches in the others
+      const uint32_t q = i / kSortRun, runs = (n + kSortRun - 1) / kSortRun;
+      if ((uint32_t)lane < runs && (uint32_t)lane != q) {
+        uint32_t lo = lane * kSortRun, hi = min(n, lo + kSortRun);  // first x with !before(x, me)
+        const uint32_t base = lo;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (before(in[mid], me)) lo = mid + 1;
+          else hi = mid;
+        }
+        rank = lo - base;
+      }
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) rank += __shfl_xor_sync(kFull, rank, d);
+      for (int d = 16; d > 0; d >>= 1) rank += __shfl_xor_sync(kFull, rank, d);
+      rank += i - q * kSortRun;
+    } else {
+#pragma unroll 4
+      for (uint32_t j = lane; j < n; j += 32) rank += before(in[j], me);
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) rank += __shfl_xor_sync(kFull, rank, d);
+    }
     if (rank < K && lane == 0) sorted[(uint64_t)ls * K + rank] = me;
     if (rank < K && xchg && lane < m.W) {  // W > 1: straight into every peer's mailbox too
       const MboxLayout L = mbox_layout(m.W, m.S, m.MB);
@@ -578,7 +628,8 @@ __global__ void __launch_bounds__(kSortThreads)
 
 }  // namespace
 
-uint32_t topk_max_k() { return 8192; }
+// (<= 32 runs of kSortRun candidates, K + kTopkEqMax of them)
+uint32_t topk_max_k() { return 32 * kSortRun - kTopkEqMax; }
 
 // GEAR_TOPK_CLUSTER=0 forces the grid-wide path for every shard size (A/B).
 bool topk_cluster_enabled() {
@@ -630,9 +681,20 @@ cudaError_t launch_topk_local(const uint64_t* key, uint64_t shard_cap, uint64_t 
     write_kernel<<<grid, kThreads, 0, s>>>(key, shard_cap, G, K, first_shard, state, cnt, cand_tmp,
                                            totals_out);
   }
+  // candidates n <= K + kTopkEqMax: the direct rank sort while that bound is
+  // small, runs + merge ranks above it (cand_tmp holds 2 x R x (K + kTopkEqMax))
   const dim3 sgrid((K + kTopkEqMax + kSortWarps - 1) / kSortWarps, n_shards_local);
-  sort_kernel<<<sgrid, kSortThreads, 0, s>>>(K, first_shard, cand_tmp, cand_out, totals_out,
-                                                state, mbox ? *mbox : Mbox{}, mbox != nullptr);
+  if (K + kTopkEqMax <= kSortDirect) {  // (the sort launch is counted above)
+    sort_kernel<false><<<sgrid, kSortThreads, 0, s>>>(K, first_shard, cand_tmp, cand_out,
+                                                      totals_out, state, mbox ? *mbox : Mbox{},
+                                                      mbox != nullptr);
+  } else {
+    Cand* runs = cand_tmp + (uint64_t)n_shards_local * (K + kTopkEqMax);
+    count_launch();  // run_rank_kernel (the sort launch is counted above)
+    run_rank_kernel<<<sgrid, kSortThreads, 0, s>>>(K, cand_tmp, runs, totals_out);
+    sort_kernel<true><<<sgrid, kSortThreads, 0, s>>>(K, first_shard, runs, cand_out, totals_out,
+                                                     state, mbox ? *mbox : Mbox{}, mbox != nullptr);
+  }
   return cudaGetLastError();
 }
 

@@ -160,7 +160,7 @@ struct gear_table {
   uint32_t* glob_slot = nullptr;
   gear::Cand* cand_local = nullptr;  // [R * W*max_batch]
   gear::TopkState* topk_state = nullptr;  // [R]
-  gear::Cand* topk_tmp = nullptr;         // [R * (W*max_batch + kTopkEqMax)] TopK candidates
+  gear::Cand* topk_tmp = nullptr;         // [2][R * (W*max_batch + kTopkEqMax)] TopK candidates, sorted runs
   uint32_t* topk_cnt = nullptr;           // [R][kTopkMaxCtas][2]
   gear::Cand* cand_all = nullptr;    // [S * W*max_batch]
 

@@ -371,6 +371,39 @@ def run_host_comm_capture_case(comm, W, rank):
     t.close()
 
 
+def run_topk_large_case(comm, W, rank, Cs=20000, B=4096):
+    """TopK with K = W*B >= 8192 candidates: the sorted-runs + merge-rank sort
+    (topk.cu) feeding every peer's mailbox, against the oracle (Q20)."""
+    cols = [gear.Column("x", gear.GEAR_U8, (4,))]
+    N = W * Cs
+    t = gear.Table(N, 1, cols, comm, max_batch=B)
+    o = oracle.Table(Cs, W)
+    rng = np.random.default_rng(123)
+    vals = np.array([0.0, 0.5, 1.0, 2.0, 3.0])
+    prio = np.where(rng.random(N) < 0.5, vals[rng.integers(0, len(vals), N)],
+                    synth.priorities(N, seed=3, zero_frac=0.0))
+    for s in range(W):
+        p = prio[s * Cs:(s + 1) * Cs]
+        st, oidx = o.insert(s, p)
+        if s == rank:
+            out = np.zeros(Cs, np.uint64)
+            t.insert(s, [torch.zeros((Cs, 4), dtype=torch.uint8, device="cuda")], p, out)
+            assert np.array_equal(out, oidx)
+    torch.cuda.synchronize()
+    dist.barrier()
+    for b in (B, B // 2 + 3):
+        idx = torch.empty(b, dtype=torch.int64, device="cuda")
+        t.sample(gear.GEAR_TOPK, b, 0, 0.4, idx)
+        torch.cuda.synchronize()
+        st, oi, _, _ = o.sample(oracle.TOPK, W, rank, b, 0, 0.4)
+        assert st == 0, st
+        gi = idx.cpu().numpy().view(np.uint64)
+        assert np.array_equal(gi, oi), f"TopK K={W * b}: ids differ at {np.nonzero(gi != oi)[0][:8]}"
+    err, _ = t.sync()
+    assert err == 0, err
+    t.close()
+
+
 def run_timeout_case(comm, W, rank, R=1, Cs=256, B=32):
     """A broken SPMD sequence: only rank 0 calls gear_sample and then
     gear_update_priorities.  Its mailbox waits time out after ~4 s; the
@@ -450,6 +483,10 @@ def main():
             dist.barrier()
             if rank == 0:
                 print("case host comm: all-gather refused inside graph capture: ok", flush=True)
+        run_topk_large_case(comm, W, rank)
+        dist.barrier()
+        if rank == 0:
+            print(f"case TopK with K = {W} x 4096 (sorted runs + merge ranks, mailboxes): ok", flush=True)
         run_timeout_case(comm, W, rank)
         dist.barrier()
         if rank == 0:

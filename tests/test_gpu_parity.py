@@ -281,6 +281,32 @@ def test_topk_large_multi_cta(torch_cuda, R, kind, Cs):
     P.close()
 
 
+@pytest.mark.parametrize("R,kind,B", [(1, "ties", 32768), (1, "lognormal", 100_000),
+                                      (3, "ties", 20_000), (2, "equal", 7000)])
+def test_topk_beyond_8192(torch_cuda, R, kind, B):
+    """TopK with more candidates than the direct rank sort takes (K + 2048 >
+    8192): sorted runs of 4096 candidates + merge ranks by binary search
+    (topk.cu), up to 25 runs; ties across runs, every key equal (the K
+    smallest slots), K at c5's W=8 batch (32768)."""
+    cols = [synth.ColSpec("x", "u8", (4,))]
+    Cs = 150_000
+    P = _pair(capacity=Cs * R, seq_len=1, colspecs=cols, R=R, max_batch=B)
+    rng = np.random.default_rng(B + R)
+    if kind == "ties":
+        vals = np.array([0.0, 0.5, 1.0, 2.0, 4.0])
+        prio = vals[rng.integers(0, len(vals), size=Cs * R)]
+    elif kind == "lognormal":
+        prio = synth.priorities(Cs * R, seed=6, zero_frac=0.05)
+    else:
+        prio = np.full(Cs * R, 1.5)
+    P.fill(prio)
+    for b in (B, B - 4097):
+        idx = P.check_sample(G.GEAR_TOPK, b, 0)
+        assert idx is not None
+    P.check_collect(idx)
+    P.close()
+
+
 def test_insert_bad_priority_and_device_sources(torch_cuda):
     cols = [synth.ColSpec("a", "u8", (7,)), synth.ColSpec("b", "i32", (3,))]
     P = _pair(capacity=64, seq_len=3, colspecs=cols, R=2)
