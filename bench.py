@@ -858,8 +858,11 @@ def main():
                     help="CUDA stream priority of the collect streams")
     ap.add_argument("--graph", type=int, default=1,
                     help="also time the pipelined step captured as a CUDA graph")
-    ap.add_argument("--assign", default="owner", choices=["owner", "contiguous"],
-                    help="owner-affine (DESIGN.md Q19) or contiguous rank slices of the global batch")
+    ap.add_argument("--assign", default="auto", choices=["auto", "owner", "contiguous"],
+                    help="owner-affine (DESIGN.md Q19) or contiguous rank slices of the global "
+                         "batch; auto: owner-affine when the table has HBM-resident columns, "
+                         "contiguous when every column is host-resident (every GPU reads any "
+                         "host row over its own PCIe: no locality to gain, no assignment kernel)")
     ap.add_argument("--impl", default="gear", choices=["gear", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -868,6 +871,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.assign == "auto":
+        cols = effective_cfg(args).cols
+        args.assign = "owner" if any(c.placement == "device" for c in cols) else "contiguous"
     if args.impl == "reference":
         run_reference(args)
     else:
