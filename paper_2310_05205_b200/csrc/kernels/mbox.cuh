@@ -17,34 +17,21 @@
 // memory operations -- with a zero-copy collect running on the same SMs the
 // per-poll / per-flag system barriers cost c3 (4 KB host rows) 6-16% at N=4
 // (profiles/r02_multi: mailbox vs NCCL exchange, protocol A/B).
-// GEAR_MBOX_PROTO=0 builds the round-1 protocol for A/B.
+// (The round-1 protocol was deleted after the A/B.)
 #pragma once
 
 #include "common.cuh"
 
-#ifndef GEAR_MBOX_PROTO
-#define GEAR_MBOX_PROTO 1
-#endif
 #ifndef GEAR_MBOX_SLEEP_NS
 #define GEAR_MBOX_SLEEP_NS 64
 #endif
 
 namespace gear {
 
-__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
 __device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
-}
-
-__device__ __forceinline__ void st_release_sys_u64(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
@@ -60,20 +47,12 @@ __device__ __forceinline__ uint64_t global_ns() {
 // Producer, by the one publishing thread after the block barrier that follows
 // the payload stores: the release fence ...
 __device__ __forceinline__ void mbox_producer_fence() {
-#if GEAR_MBOX_PROTO
   asm volatile("fence.acq_rel.sys;" ::: "memory");
-#else
-  __threadfence_system();
-#endif
 }
 
 // ... then one flag store per peer (after mbox_producer_fence).
 __device__ __forceinline__ void mbox_publish(uint64_t* flag, uint64_t epoch) {
-#if GEAR_MBOX_PROTO
   st_relaxed_sys_u64(flag, epoch);
-#else
-  st_release_sys_u64(flag, epoch);
-#endif
 }
 
 // Spin until flags[0..n) >= epoch.  Returns false on timeout (error latched).
@@ -81,11 +60,7 @@ __device__ __forceinline__ bool mbox_wait(const uint64_t* flags, uint32_t n, uin
                                           uint32_t* err) {
   const uint64_t t0 = global_ns();
   for (uint32_t i = 0; i < n; ++i) {
-#if GEAR_MBOX_PROTO
     while (ld_relaxed_sys_u64(flags + i) < epoch) {
-#else
-    while (ld_acquire_sys_u64(flags + i) < epoch) {
-#endif
       if (global_ns() - t0 > 4000000000ull) {
         atomicOr(err, kErrTimeout);
         return false;
@@ -93,9 +68,7 @@ __device__ __forceinline__ bool mbox_wait(const uint64_t* flags, uint32_t n, uin
       __nanosleep(GEAR_MBOX_SLEEP_NS);
     }
   }
-#if GEAR_MBOX_PROTO
   asm volatile("fence.acq_rel.sys;" ::: "memory");  // acquire: the relaxed loads saw the flags
-#endif
   return true;
 }
 
