@@ -250,6 +250,17 @@ def effective_cfg(args):
     return cfg
 
 
+def resolve_assign(args):
+    """--assign auto: owner-affine (Q19) when the table has HBM-resident
+    columns (local rows stay HBM-bound), contiguous slices (Q9) when every column
+    is host-resident (any GPU reads any host row over its own PCIe: nothing to
+    gain, and no assignment kernel)."""
+    if args.assign != "auto":
+        return args.assign
+    cols = effective_cfg(args).cols
+    return "owner" if any(c.placement == "device" for c in cols) else "contiguous"
+
+
 def workload_config(cfg, capacity, world, args, cap_note):
     """The `config` object of the JSON line, identical for both arms."""
     import synth
@@ -871,9 +882,7 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.assign == "auto":
-        cols = effective_cfg(args).cols
-        args.assign = "owner" if any(c.placement == "device" for c in cols) else "contiguous"
+    args.assign = resolve_assign(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -36,3 +36,17 @@ def test_reference_arm_json_line():
 
 def test_reference_arm_other_ranks_print_nothing():
     assert _run({"RANK": "1", "WORLD_SIZE": "2"}) == []
+
+
+def test_auto_assignment_by_placement():
+    """--assign auto: owner-affine for tables with HBM columns (c1, c2, c4),
+    contiguous slices for all-host tables (c3, c5); explicit choices stay."""
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+    for cfg, want in (("c1", "owner"), ("c2", "owner"), ("c3", "contiguous"), ("c4", "owner"),
+                      ("c5", "contiguous")):
+        a = argparse.Namespace(config=cfg, strategy=None, assign="auto")
+        assert bench.resolve_assign(a) == want, cfg
+    a = argparse.Namespace(config="c3", strategy=None, assign="owner")
+    assert bench.resolve_assign(a) == "owner"
