@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
   __shared__ uint64_t s_gbase[kScanBufs];  // each buffer's tile geometry
   __shared__ uint64_t s_agg[kScanBufs];  // each buffer's tile aggregate
   __shared__ uint64_t s_red[kThreads / 32];   // scan: warp totals
-  __shared__ uint64_t s_red2[kThreads / 32];  // look-back: warp partial sums
+  __shared__ uint64_t s_part[kScanLookPer][kThreads / 32];  // look-back: warp sums up to its first P
   __shared__ uint32_t s_pmask[kScanLookPer][kThreads / 32];
   __shared__ bool s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -288,34 +288,35 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
           }
           PROF(6);
           // closest inclusive prefix: the smallest distance tid + 256k with a
-          // P flag, from one ballot per warp and word
+          // P flag.  ONE block barrier: every warp publishes its ballot and the
+          // sum of its values up to and including its own first P (all of them
+          // if it has none); the combine walks the (word, warp) pairs in
+          // distance order up to the first one with a P
 #pragma unroll
           for (int k = 0; k < kScanLookPer; ++k) {
             const unsigned m = __ballot_sync(kFull, (st[k] >> 62) == 2);
-            if (lane == 0) s_pmask[k][warp] = m;
+            const int f = m ? __ffs(m) - 1 : 31;
+            uint64_t v = lane <= f ? (st[k] & kValMask) : 0ull;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+            if (lane == 0) {
+              s_pmask[k][warp] = m;
+              s_part[k][warp] = v;
+            }
           }
           __syncthreads();
           PROF(7);
-          uint32_t dp = 0xffffffffu;
-#pragma unroll
-          for (int k = kScanLookPer - 1; k >= 0; --k)
-#pragma unroll
-            for (int w = kThreads / 32 - 1; w >= 0; --w) {
-              const unsigned m = s_pmask[k][w];
-              if (m) dp = (uint32_t)(k * kThreads + w * 32 + __ffs(m) - 1);
-            }
-          uint64_t part = 0;
+          bool found = false;
 #pragma unroll
           for (int k = 0; k < kScanLookPer; ++k)
-            part += ((uint32_t)(tid + k * kThreads) <= dp) ? (st[k] & kValMask) : 0ull;
 #pragma unroll
-          for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(kFull, part, d);
-          if (lane == 0) s_red2[warp] = part;
-          __syncthreads();
-#pragma unroll
-          for (int w = 0; w < kThreads / 32; ++w) excl += s_red2[w];
-          if (dp != 0xffffffffu) break;
-          __syncthreads();  // s_pmask / s_red2 read before the next round
+            for (int w = 0; w < kThreads / 32; ++w)
+              if (!found) {
+                excl += s_part[k][w];
+                found = s_pmask[k][w] != 0;
+              }
+          if (found) break;
+          __syncthreads();  // s_pmask / s_part read before the next round
           pred -= (int64_t)kThreads * kScanLookPer;  // no prefix in this window
           poll(bp, pred, st);
         }
