@@ -409,6 +409,9 @@ __global__ void __launch_bounds__(kThreads, kScanCtasPerSm) scan_kernel(
 // is ragged (masked).  Chunks are claimed from the ticket, so a chunk only
 // waits on chunks that already run (forward progress), and the kernel shares
 // scan_kernel's status arrays / epoch / ticket / exit counter protocol.
+// Measured (profiles/r02_scan/chunk, final_full): 10 M keys 36 us under ncu
+// (scan_kernel ~41), but at 40 M keys most of phase 2's re-read misses L2, so
+// launch_scan picks this kernel only while the rank's keys are <= 96 MB.
 #ifndef GEAR_CHUNK_BUFS
 #define GEAR_CHUNK_BUFS 3
 #endif
