@@ -178,6 +178,7 @@ struct CollectCol {
   uint32_t vec;                       // LSU vector width in bytes: 16, 8, 4, 2 or 1
   uint32_t tma;                       // 1: moved by TMA bulk copies (16-B aligned rows)
   uint32_t peer_lsu;                  // TMA column whose peer-HBM rows the LSU warps move
+  uint32_t host_lsu;                  // TMA column (host-resident) whose rows the LSU warps move
 };
 
 struct CollectParams {
@@ -199,7 +200,7 @@ struct CollectParams {
   uint32_t ncols;
   uint32_t n;
   uint32_t self_rank;                 // this rank (peer rows: owner != self_rank)
-  uint32_t any_peer_lsu;              // some column has peer_lsu
+  uint32_t any_peer_lsu;              // some column has peer_lsu or host_lsu
   uint32_t evict_first;               // bulk copies with an L2 evict-first policy
   unsigned long long* dyn_ctr;        // non-null: TMA tasks claimed from this counter pair
   uint32_t* err;

@@ -144,10 +144,15 @@ __global__ void __launch_bounds__(kThreads) insert_rows_kernel(const __grid_cons
 constexpr int kTmaThreads = 128;
 
 
-// W > 1: the peer-HBM rows of TMA columns, moved over NVLink by the LSU warps
-// with 16-byte loads (many independent loads in flight per warp) instead of
-// the single-lane bulk pipeline, where one slow NVLink chunk would hold up
-// the in-order stages behind it.
+// Rows the LSU warps of the bulk-copy kernel move instead of its single-lane
+// pipeline, with 16-byte loads (8 independent loads in flight per lane):
+//  * W > 1, `peer_lsu` columns: the peer-HBM rows (over NVLink), where one slow
+//    NVLink chunk would hold up the in-order stages behind it;
+//  * `host_lsu` columns (tuning "collect_host_lsu", default on): every row of
+//    a host-resident column (zero-copy over PCIe) -- c3's 4 KB rows: collect
+//    0.0875 -> 0.0853 ms, 0.86 -> 0.88 of the PCIe probe, e2e unchanged; the
+//    all-LSU kernel gains the same but its full-GPU grid delays the next
+//    step's selection (e2e -4.6%, profiles/r02_c3lsu).
 __device__ __forceinline__ void collect_peer_rows(const CollectParams& p, uint64_t warp0,
                                                   uint64_t nwarps, int lane) {
   for (uint64_t task = warp0; task < p.tma_total; task += nwarps) {
@@ -155,11 +160,11 @@ __device__ __forceinline__ void collect_peer_rows(const CollectParams& p, uint64
     uint64_t j, k;
     decode_task(p, p.tma_cols, p.n_tma, task, &c, &j, &k);
     const CollectCol& col = p.col[c];
-    if (!col.peer_lsu) continue;
+    if (!col.peer_lsu && !col.host_lsu) continue;
     const uint64_t g = __ldg(p.idx + j);
     if (g >= p.n_global) continue;  // latched by the TMA lane
     const uint64_t owner = g / p.rows_per_rank;
-    if (owner == p.self_rank) continue;
+    if (!col.host_lsu && owner == p.self_rank) continue;
     const uint64_t local = g - owner * p.rows_per_rank;
     const uint64_t off = k * (uint64_t)col.chunk;
     const uint64_t rem = col.rb - off;
@@ -241,7 +246,7 @@ __device__ __forceinline__ uint32_t tma_issue_load(const CollectParams& p, uint6
     return 0;
   }
   const uint64_t owner = g / p.rows_per_rank;
-  if (col.peer_lsu && owner != p.self_rank) {  // a peer's HBM row: the LSU warps move it
+  if ((col.peer_lsu && owner != p.self_rank) || col.host_lsu) {  // moved by the LSU warps
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
     return 0;
   }

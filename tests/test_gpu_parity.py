@@ -395,12 +395,13 @@ def test_deterministic_across_repeats_and_beta(torch_cuda):
     P.close()
 
 
-@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("impl,host_lsu", [(0, 1), (1, 1), (1, 0)])
 @pytest.mark.parametrize("placement", ["device", "host"])
-def test_collect_large_rows_tma_and_lsu(torch_cuda, impl, placement):
+def test_collect_large_rows_tma_and_lsu(torch_cuda, impl, host_lsu, placement):
     """Rows >= 4 KB with 16-byte alignment take the TMA bulk-copy path
-    (impl 1), the rest the warp-LSU path; ragged last chunks, duplicate ids,
-    three shards, both placements, several chunk sizes."""
+    (impl 1; host-resident ones by that kernel's LSU warps unless host_lsu is
+    0), the rest the warp-LSU path; ragged last chunks, duplicate ids, three
+    shards, both placements, several chunk sizes."""
     cols = [synth.ColSpec("big", "u8", (5008,)), synth.ColSpec("tok", "i32", (256,)),
             synth.ColSpec("odd", "u8", (7,)), synth.ColSpec("f", "f32", (3,))]
     P = _pair(capacity=3 * 97, seq_len=9, colspecs=cols, R=3, placement=placement)
@@ -408,6 +409,7 @@ def test_collect_large_rows_tma_and_lsu(torch_cuda, impl, placement):
     P.fill(synth.priorities(3 * 97, seed=8))
     rng = np.random.default_rng(impl)
     G.gear_table_set_tuning(P.t.handle, "collect_impl", impl)
+    G.gear_table_set_tuning(P.t.handle, "collect_host_lsu", host_lsu)
     for tma_chunk, lsu_chunk in ((32768, 8192), (4096, 512), (16384, 1024)):
         G.gear_table_set_tuning(P.t.handle, "tma_chunk", tma_chunk)
         G.gear_table_set_tuning(P.t.handle, "lsu_chunk", lsu_chunk)
