@@ -414,10 +414,12 @@ gear_status gear_table_load(gear_table* t, const char* path);
  *                   the selection's keys / CDFs / mailboxes): -1 = auto
  *                   (default): on at W > 1 after a TopK selection, 0 = off,
  *                   1 = on;
- *   "collect_host_lsu": 1 (default) = the rows of host-resident columns are
- *                   gathered by the bulk-copy kernel's LSU warps (16-B
- *                   zero-copy loads) instead of its bulk pipeline (+2.5% c3
- *                   throughput); 0 = bulk pipeline;
+ *   "collect_host_lsu": 1 = the rows of host-resident columns are gathered
+ *                   by the bulk-copy kernel's LSU warps (16-B zero-copy
+ *                   loads) instead of its bulk pipeline; 0 = bulk pipeline;
+ *                   -1 = auto (default): LSU warps for host rows of at most
+ *                   16 KB (+2.5% c3 throughput; large host rows keep the
+ *                   bulk pipeline);
  *   "collect_peer_lsu": W > 1: 1 = the peer-HBM rows of bulk-copied (TMA)
  *                   columns are moved by the LSU warps instead of the bulk
  *                   pipeline (+3% collect throughput when few rows are

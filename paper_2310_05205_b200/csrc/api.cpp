@@ -245,7 +245,7 @@ gear_status create_table(const gear_table_desc* d, gear_comm* comm, gear_table* 
   if (const char* e = getenv("GEAR_COLLECT_CHUNK")) t->chunk_bytes = (uint32_t)atoi(e);
   if (const char* e = getenv("GEAR_TMA_CHUNK")) t->tma_chunk = (uint32_t)atoi(e);
   if (const char* e = getenv("GEAR_COLLECT_PEER_LSU")) t->collect_peer_lsu = atoi(e) != 0;
-  if (const char* e = getenv("GEAR_COLLECT_HOST_LSU")) t->collect_host_lsu = atoi(e) != 0;
+  if (const char* e = getenv("GEAR_COLLECT_HOST_LSU")) t->collect_host_lsu = atoi(e) < 0 ? -1 : (atoi(e) != 0);
   if (const char* e = getenv("GEAR_PEER_XCHG")) t->peer_xchg = atoi(e) != 0;  // A/B (same on every rank)
   if (const char* e = getenv("GEAR_COLLECT_DYNAMIC")) t->collect_dynamic = atoi(e);
   if (const char* e = getenv("GEAR_COLLECT_EVICT_FIRST")) t->evict_first = atoi(e);
@@ -1182,7 +1182,11 @@ gear_status gear_collect(gear_table* t, uint32_t n, const uint64_t* idx, uint32_
     if (cc.vec < 16 && cc.chunk % cc.vec) cc.chunk = t->chunk_bytes;
     cc.chunks_per_row = (uint32_t)((cs.rb + cc.chunk - 1) / cc.chunk);
     cc.peer_lsu = (cc.tma && t->W > 1 && cs.placement == GEAR_DEVICE && t->collect_peer_lsu) ? 1u : 0u;
-    cc.host_lsu = (cc.tma && cs.placement == GEAR_HOST && t->collect_host_lsu) ? 1u : 0u;
+    // host rows by the LSU warps: auto = rows of at most one 16 KB bulk task
+    // (c3's 4 KB rows: +2.5%; c4's 449 KB host rows lost 40% e2e at N=4)
+    cc.host_lsu = (cc.tma && cs.placement == GEAR_HOST &&
+                   (t->collect_host_lsu == 1 || (t->collect_host_lsu < 0 && cs.rb <= 16384)))
+                      ? 1u : 0u;
     cp.any_peer_lsu |= cc.peer_lsu | cc.host_lsu;
     if (cc.tma) {
       cc.chunk_begin = cp.tma_total;
@@ -1244,7 +1248,7 @@ gear_status gear_table_set_tuning(gear_table* t, const char* key, int64_t value)
     t->collect_dynamic = (int)value;
   } else if (!strcmp(key, "collect_evict_first") && value >= -1 && value <= 1) {
     t->evict_first = (int)value;
-  } else if (!strcmp(key, "collect_host_lsu") && (value == 0 || value == 1)) {
+  } else if (!strcmp(key, "collect_host_lsu") && value >= -1 && value <= 1) {
     t->collect_host_lsu = (int)value;
   } else if (!strcmp(key, "collect_peer_lsu") && (value == 0 || value == 1)) {
     t->collect_peer_lsu = (int)value;

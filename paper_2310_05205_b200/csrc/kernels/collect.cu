@@ -148,11 +148,13 @@ constexpr int kTmaThreads = 128;
 // pipeline, with 16-byte loads (8 independent loads in flight per lane):
 //  * W > 1, `peer_lsu` columns: the peer-HBM rows (over NVLink), where one slow
 //    NVLink chunk would hold up the in-order stages behind it;
-//  * `host_lsu` columns (tuning "collect_host_lsu", default on): every row of
-//    a host-resident column (zero-copy over PCIe) -- c3's 4 KB rows: collect
-//    0.0875 -> 0.0853 ms, 0.86 -> 0.88 of the PCIe probe, e2e unchanged; the
-//    all-LSU kernel gains the same but its full-GPU grid delays the next
-//    step's selection (e2e -4.6%, profiles/r02_c3lsu).
+//  * `host_lsu` columns (tuning "collect_host_lsu", default: host rows of at
+//    most 16 KB): every row of a host-resident column (zero-copy over PCIe)
+//    -- c3's 4 KB rows: collect 0.0875 -> 0.0853 ms, 0.86 -> 0.88 of the PCIe
+//    probe, e2e -0.7%; the all-LSU kernel gains the same but its full-GPU
+//    grid delays the next step's selection (e2e -4.6%, profiles/r02_c3lsu);
+//    c4's 449 KB host rows lost 40% e2e at N=4 this way, so large rows keep
+//    the bulk pipeline.
 __device__ __forceinline__ void collect_peer_rows(const CollectParams& p, uint64_t warp0,
                                                   uint64_t nwarps, int lane) {
   for (uint64_t task = warp0; task < p.tma_total; task += nwarps) {

@@ -205,5 +205,5 @@ struct gear_table {
   unsigned long long* dyn_pool = nullptr;  // [kDynSlots][2] task counters (rotating)
   uint64_t dyn_slot = 0;
   int collect_peer_lsu = 0;         // W > 1: peer-HBM rows of TMA columns via LSU warps
-  int collect_host_lsu = 1;         // host-resident TMA columns via the TMA kernel's LSU warps
+  int collect_host_lsu = -1;        // host-resident TMA columns via the TMA kernel's LSU warps (-1: rows <= 16 KB)
 };

@@ -395,7 +395,7 @@ def test_deterministic_across_repeats_and_beta(torch_cuda):
     P.close()
 
 
-@pytest.mark.parametrize("impl,host_lsu", [(0, 1), (1, 1), (1, 0)])
+@pytest.mark.parametrize("impl,host_lsu", [(0, 1), (1, 1), (1, 0), (1, -1)])
 @pytest.mark.parametrize("placement", ["device", "host"])
 def test_collect_large_rows_tma_and_lsu(torch_cuda, impl, host_lsu, placement):
     """Rows >= 4 KB with 16-byte alignment take the TMA bulk-copy path
