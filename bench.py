@@ -55,9 +55,9 @@ NVLINK_PEER_GBS = 775.27  # profiles/r01_probe_2gpu.jsonl: cudaMemcpyPeer pull, 
 # dram__bytes_read.sum + dram__bytes_write.sum of one collect launch, from an
 # ncu --set full capture of `bench.py --config X` (tools/run_ncu_suite.sh).
 TRAFFIC = {
-    ("c2_dt_atari", 1, None): ((432.979456 + 384.953344) * 1e6,
-                               "profiles/r02s7/collect_tma_full.ncu-rep (one launch, final round-2 build)"),
-    ("c3_gato_db1", 1, None): (115.2e3, "profiles/r02s7/collect_tma_c3_full.ncu-rep (one launch; "
+    ("c2_dt_atari", 1, None): ((432.961792 + 384.591872) * 1e6,
+                               "profiles/r02s8/collect_tma_full.ncu-rep (one launch, final round-2 build)"),
+    ("c3_gato_db1", 1, None): (109.824e3, "profiles/r02s8/collect_tma_c3_full.ncu-rep (one launch; "
                                "DRAM bytes only: the binding PCIe read is not a DRAM counter)"),
 }
 
