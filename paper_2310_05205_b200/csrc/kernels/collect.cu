@@ -141,7 +141,10 @@ __global__ void __launch_bounds__(kThreads) insert_rows_kernel(const __grid_cons
 // kStages * stage bytes in flight with no register cost, independent of the
 // source (local HBM, a peer's HBM over NVLink, or mapped host memory).  The
 // other warps copy the columns whose rows are not 16-byte aligned.
-constexpr int kTmaThreads = 128;
+#ifndef GEAR_TMA_THREADS
+#define GEAR_TMA_THREADS 128
+#endif
+constexpr int kTmaThreads = GEAR_TMA_THREADS;  // warp 0: the bulk pipeline; the rest: LSU rows
 
 
 // Rows the LSU warps of the bulk-copy kernel move instead of its single-lane
