@@ -159,24 +159,38 @@ _I64 = ("int64", "uint64")
 _I32 = ("int32", "uint32")
 
 
+_DTYPE_NAMES: dict = {}
+
+
 def _dtype_name(x) -> str:
-    return str(x.dtype).replace("torch.", "")
+    d = x.dtype
+    s = _DTYPE_NAMES.get(d)
+    if s is None:
+        s = _DTYPE_NAMES[d] = str(d).replace("torch.", "")
+    return s
 
 
 def _arg(x, kinds, name: str, n: int = 0, fn: str = "") -> int | None:
     """_ptr(x) after checking that a tensor / array argument has one of the
     dtypes `kinds` and at least n elements (a wrong dtype would make the
     kernels read or write past the buffer).  Raw integer addresses are the
-    caller's responsibility."""
+    caller's responsibility.  (Per-call cost matters for small batches: the
+    dtype names are cached.)"""
     if x is None or isinstance(x, int):
-        return _ptr(x)
+        return x
     dt = _dtype_name(x)
     if dt not in kinds:
         raise TypeError(f"{fn}: {name} must have dtype {' or '.join(kinds)}, got {dt}")
-    numel = x.numel() if hasattr(x, "numel") and callable(x.numel) else x.size
+    if isinstance(x, np.ndarray):
+        if x.size < n:
+            raise ValueError(f"{fn}: {name} has {x.size} elements, the call needs {n}")
+        assert x.flags["C_CONTIGUOUS"], "numpy arrays must be contiguous"
+        return x.ctypes.data
+    numel = x.numel()
     if numel < n:
         raise ValueError(f"{fn}: {name} has {numel} elements, the call needs {n}")
-    return _ptr(x)
+    assert x.is_contiguous(), "tensors must be contiguous"
+    return x.data_ptr()
 
 
 def _nbytes(x) -> int | None:
